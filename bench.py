@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark: bootstrapped TFHE gates/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl she|reference]
+
+A step is one pass of the whole hot path (gate prologue,
+blind rotation, sample extract, MUX combine, key switch) over one batch of
+config 1: 4096 independent gates at the TFHE default parameters (N=1024,
+n=500, Bg=2^10, l=2, key switching 2^2 x 8), ops uniform over
+NAND/AND/OR/XOR/XNOR/MUX, input bits uniform (she_inputs).
+Inputs are resident in HBM when the timed region starts; L2 is flushed
+(256 MiB write) between timed steps, outside the per-step CUDA-event pairs.
+
+N > 1 (torchrun): every rank runs its own 4096-gate batch (weak scaling, no
+data-path collective — the gates are independent); value = all ranks' gates
+/ max-over-ranks device time.
+
+--impl reference: the CPU oracle (oracle/, schoolbook TFHE) timed on this
+box's host cores on a bounded sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import re
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import she_inputs as si  # noqa: E402
+
+METRIC = "bootstrapped gates/s"
+UNIT = "gates/s"
+CFG = 1
+COUNT = 4096
+MODMUL_PER_LANE = {1024: 19_456_000, 256: 1_048_576}  # n[(k+1)l+(k+1)](N/2)log2N + n(k+1)l(k+1)N
+WORKLOAD = ("config1: 4096 independent bootstrapped gates, ops uniform over "
+            "NAND/AND/OR/XOR/XNOR/MUX, uniform input bits; TFHE N=1024 k=1 n=500 "
+            "Bg=2^10 l=2 ks 2^2x8 alpha_lwe=2.44e-5 alpha_bk=3.73e-9 (torus32)")
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# roofline peak: Goldilocks modmuls per second the ALUs can issue
+# ---------------------------------------------------------------------------
+def modmul_sass_instructions(lib_path: str) -> float | None:
+    """SASS instructions per gl::mul, from the K6 loop body of libshe.so
+    (non-uniform-datapath instructions of the loop / 8 independent chains)."""
+    try:
+        sass = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True,
+                              timeout=120).stdout
+    except (OSError, subprocess.TimeoutExpired):
+        return None
+    m = re.search(r"Function : \S*modmul_peak_kernel\S*\n(.*?)(?:\n\s*Function :|\Z)", sass, re.S)
+    if not m:
+        return None
+    lines = re.findall(r"/\*([0-9a-f]{4})\*/\s+([^;]+);", m.group(1))
+    ins = [(int(a, 16), t.strip()) for a, t in lines]
+    back = [(a, t) for a, t in ins if t.split()[0].endswith("BRA.U") and "UP0" in t and not t.startswith("@")]
+    for a, t in back:
+        tgt = int(t.split(",")[-1].strip(), 16)
+        if tgt < a:
+            body = [x for addr, x in ins if tgt <= addr < a]
+            vec = [x for x in body if not re.match(r"^(@!?U?P\d+\s+)?U", x) and not x.startswith("NOP")]
+            return len(vec) / 8.0
+    return None
+
+
+def roofline_peak(device: int, lib_path: str, sm_max_mhz: float | None):
+    import torch
+    from paper_1906_00148_b200 import she
+    props = torch.cuda.get_device_properties(device)
+    sms = props.multi_processor_count
+    f = (sm_max_mhz or 1965.0) * 1e6
+    measured, _ = she.modmul_peak(device)
+    ipm = modmul_sass_instructions(lib_path)
+    # 4 SMSPs x 32 lanes issue one instruction per clock each (B300_MICROARCH.md)
+    derived = sms * 4 * 32 * f / ipm if ipm else None
+    peak = max(x for x in (derived, measured) if x)
+    src = (f"max(derived {derived / 1e9:.0f} = {sms} SM x 128 lanes/clk x {f / 1e6:.0f} MHz / "
+           f"{ipm:.1f} SASS instr per modmul, K6 measured {measured / 1e9:.0f}) Gmodmul/s"
+           if derived else f"K6 measured {measured / 1e9:.0f} Gmodmul/s")
+    return peak, measured, derived, ipm, src
+
+
+def read_profile_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("br_kernel_dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# the product arm
+# ---------------------------------------------------------------------------
+def run_she(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1906_00148_b200 import she
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    P = si.CONFIG_PARAMS[CFG]
+    sk, ck = she.she_keygen(P, si.key_seed(CFG))
+    ctx = she.Context(P, ck, device=local, rank=rank, world=world)
+    ops = si.gate_ops(CFG, COUNT)
+    bits = si.gate_input_bits(CFG, COUNT)
+    # every rank evaluates its own batch: distinct ciphertexts (ordinal offset by rank)
+    cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(CFG), 3 * COUNT * rank)
+    cts = cts.reshape(COUNT, 3, -1)
+    lanes = si.br_lanes(ops)
+    stride = P.stride
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).cuda()
+    d_ops = dev(ops.astype(np.uint8))
+    d_a, d_b, d_c = (dev(cts[:, j].copy()) for j in range(3))
+    d_out = torch.empty((COUNT, stride), dtype=torch.int32, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        she.she_gate_batch_ops(ctx, d_ops, d_a, d_b, d_c, d_out, stream)
+
+    peak, k6, derived, ipm, peak_src = roofline_peak(local, she.LIB_PATH, None)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-step event pairs, L2 flushed between ----
+    ctx.enable_timing(True)
+    ctx.timing(reset=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.zero_()
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ctx.enable_timing(False)
+    t = ctx.timing(reset=True)
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        x = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        dev_ms = float(x.item())
+    ms_per_step = dev_ms / args.steps
+    value = world * COUNT * args.steps / (dev_ms * 1e-3)
+
+    # dominant kernel: the blind rotation (K2+K3)
+    br_ms_per_launch = t["br_ms"] / max(1, t["br_launches"])
+    achieved = lanes * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3)
+    roof = {"bound": "alu", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
+            "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": read_profile_traffic(),
+            "kernel": "br_kernel (gate prologue + blind rotation + sample extract)",
+            "algorithmic_per_launch": f"{lanes} BR lanes x {MODMUL_PER_LANE[P.N]} modmul",
+            "kernel_ms_per_launch": round(br_ms_per_launch, 3),
+            "kernel_share_of_step": round(t["br_ms"] / dev_ms, 4) if dev_ms else None,
+            "ks_kernel_ms_per_launch": round(t["ks_ms"] / max(1, t["ks_launches"]), 3),
+            "peak_source": peak_src}
+
+    # ---- end to end through the public host-buffer API (H2D + D2H inside) ----
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+    h_ops = pin((COUNT,), torch.uint8)
+    h_ops[:] = ops
+    h_in = [pin((COUNT, stride), torch.int32).view(np.uint32) for _ in range(3)]
+    for j in range(3):
+        h_in[j][:] = cts[:, j]
+    h_out = pin((COUNT, stride), torch.int32).view(np.uint32)
+    she.she_gate_batch_ops_host(ctx, h_ops, *h_in, h_out, stream)  # warm
+    e2e_s = []
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        she.she_gate_batch_ops_host(ctx, h_ops, *h_in, h_out, stream)
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_total = sum(e2e_s)
+    if world > 1:
+        x = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        e2e_total = float(x.item())
+    # correctness spot check of the e2e output against the device path
+    assert np.array_equal(h_out, d_out.cpu().numpy().view(np.uint32)), "e2e output differs"
+    dec = she.she_decrypt_bits(sk, h_out)
+    want = np.array([si.truth(o, *b) for o, b in zip(ops, bits)])
+    assert np.array_equal(dec, want), "decryption mismatch"
+    e2e = {"value": round(world * COUNT * args.steps / e2e_total, 2), "unit": UNIT,
+           "h2d_bytes_per_step": int(COUNT + 3 * COUNT * stride * 4),
+           "d2h_bytes_per_step": int(COUNT * stride * 4)}
+
+    line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded she_inputs; keys 1001, inputs 2001, ops 4001)",
+            "config": {"workload": WORKLOAD, "gates_per_rank": COUNT, "br_lanes_per_rank": lanes,
+                       "parallelism": f"gate-sharded x{world} (independent batches, no collective)",
+                       "l2": "flushed between timed steps (256 MiB write), outside the event pairs"},
+            "roofline": roof, "clocks": clk, "e2e": e2e,
+            "gpu_launches": int(t["br_launches"] + t["ks_launches"]),
+            "k6_modmul_peak_per_s": round(k6, 1)}
+    if rank == 0:
+        line["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# the CPU oracle: cpu_baseline leg and --impl reference
+# ---------------------------------------------------------------------------
+def _oracle_workload():
+    import oracle
+    P = si.CONFIG_PARAMS[CFG]
+    K = oracle.keygen(P, si.key_seed(CFG))
+    ops = si.gate_ops(CFG, COUNT)
+    bits = si.gate_input_bits(CFG, COUNT)
+    return oracle, P, K, ops, bits
+
+
+def _oracle_sample(oracle, P, K, ops, bits, start: int, size: int):
+    sel = np.arange(start, start + size) % COUNT
+    cts = oracle.encrypt(P, K.s, bits[sel].ravel(), si.input_seed(CFG), 0).reshape(size, 3, -1)
+    t0 = time.perf_counter()
+    out = oracle.gates(K, ops[sel], cts[:, 0].copy(), cts[:, 1].copy(), cts[:, 2].copy())
+    dt = time.perf_counter() - t0
+    return out, dt
+
+
+def cpu_baseline(args):
+    oracle, P, K, ops, bits = _oracle_workload()
+    cores = oracle.threads()
+    size = min(COUNT, 12 * cores)
+    _, dt = _oracle_sample(oracle, P, K, ops, bits, 0, size)
+    return {"value": round(size / dt, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {size} gates of config 1 ({si.br_lanes(ops[:size])} BR lanes), "
+                      f"{dt:.1f} s wall, schoolbook negacyclic products, OpenMP over gates, "
+                      f"gcc {oracle.COMPILER_FLAGS} {oracle.lib().variant}"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    oracle, P, K, ops, bits = _oracle_workload()
+    cores = oracle.threads()
+    per_step_s = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    size = max(cores, int(per_step_s * cores / 0.8))
+    size = min(size, COUNT)
+    for w in range(args.warmup):
+        _oracle_sample(oracle, P, K, ops, bits, w * size, size)
+    times = []
+    for k in range(args.steps):
+        _, dt = _oracle_sample(oracle, P, K, ops, bits, (args.warmup + k) * size, size)
+        times.append(dt)
+    total = sum(times)
+    value = size * args.steps / total
+    sample = f"{size} gates of config 1 per step ({size} of the 4096-gate batch), host cores"
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * total / args.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "gates_per_step": size}, "impl": "reference",
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="she", choices=["she", "reference"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_she(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * she.h — C-ABI of the B200-native batched TFHE gate-bootstrapping engine for
+ * SHE (arxiv 1906.00148): "Shift-accumulation-based LHE-enabled deep neural
+ * network", whose ReLU units, max-pool units, shifts and mixed-bitwidth
+ * accumulators are circuits of bootstrapped TFHE Boolean gates.
+ *
+ * Paper passages the calls follow (PAPER.md line, section):
+ *   client encrypts / server computes blind / client decrypts  :17, :29 (§1, §2)
+ *   epsilon(x, k) / delta(c, k), homomorphic gates, bootstrapping  :31 (§2)
+ *   TFHE over the torus; TLWE / TRLWE / TRGSW                   :35, :188 (§2, §4)
+ *   any 2-input gate (AND, OR, NOT, MUX); >2 inputs split        :110 (§3.1)
+ *   ReLU and max-pool units                                     :92, :110 (F2)
+ *   log-quantised weights; shift = ciphertext rewiring           :118, :142 (§3.2)
+ *   mixed-bitwidth accumulator (b+n bits at level n)             :147, :149 (§3.3)
+ * TFHE internals are not in the paper; conventions R1-R10 are listed in
+ * DESIGN.md §2.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - Torus32: a torus element x in R/Z is the uint32 round(x * 2^32).
+ *  - LWE slot: uint32[she_lwe_stride(p)] = a[0..n-1], b at [n], zero padding.
+ *    A bit m is encrypted with phase b - <a,s> = (m ? +1/8 : -1/8) + noise.
+ *  - Encrypted word: [width][stride] slots, LSB first, two's complement.
+ *  - Host pointers ("host") are ordinary CPU memory; device pointers
+ *    ("device") are CUDA global memory on the context's device (e.g. torch
+ *    tensors); every device call is asynchronous on the given stream.
+ *  - Ownership: the caller owns every buffer passed in; the library owns its
+ *    keys, contexts and scratch, released by the matching *_free / _destroy.
+ *  - Errors: every call returns she_status; no exception crosses the ABI;
+ *    she_last_error() gives a thread-local message for the last failure.
+ *    Asynchronous device faults surface at the next call that synchronises.
+ *  - count == 0 is a no-op returning SHE_OK.
+ */
+#ifndef SHE_H_
+#define SHE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SHE_OK = 0,
+  SHE_ERR_ARG = -1,    /* null pointer, bad op, overlap, out-of-range value */
+  SHE_ERR_PARAMS = -2, /* unsupported parameter set (see she_params)        */
+  SHE_ERR_SHAPE = -3,  /* inconsistent shapes in a layer call               */
+  SHE_ERR_CUDA = -4,   /* CUDA runtime error (message in she_last_error)    */
+  SHE_ERR_NCCL = -5,   /* collective failure                                */
+  SHE_ERR_OOM = -6,    /* device or host allocation failed                  */
+  SHE_ERR_STATE = -7   /* call not valid in the current context state       */
+} she_status;
+
+/* Gate codes.  MUX(a, b, c) = a ? b : c (SPEC.md:128 argument order). */
+typedef enum {
+  SHE_AND = 0, SHE_NAND = 1, SHE_OR = 2, SHE_NOR = 3, SHE_XOR = 4, SHE_XNOR = 5,
+  SHE_MUX = 6, /* 2 blind rotations + 1 key switch (R6)          */
+  SHE_NOT = 7, /* -a, no bootstrapping                                     */
+  SHE_COPY = 8 /* a, no bootstrapping                                      */
+} she_op;
+
+/* TFHE gate-bootstrapping parameters (BASELINE.json configs).  Supported:
+ * k = 1; N in {256, 1024}; n <= 1024; l * bg_bits <= 32; ks_t * ks_base_bits
+ * <= 32; exactness (k+1) l N (Bg/2) 2^31 < (p-1)/2 for p = 2^64 - 2^32 + 1. */
+typedef struct {
+  uint32_t N, k, n, bg_bits, l, ks_base_bits, ks_t;
+  double alpha_lwe, alpha_bk;
+} she_params;
+
+typedef struct she_secret_key she_secret_key;
+typedef struct she_cloud_key she_cloud_key;
+typedef struct she_ctx she_ctx;
+
+/* Words per LWE slot: n+1 rounded up to a multiple of 32 (C0: 160, C1: 512). */
+size_t she_lwe_stride(const she_params* p);
+
+const char* she_last_error(void);
+
+/* ---- client side (host only) -------------------------------------------- */
+
+/* Keygen from a seed (DESIGN.md §3 random-stream layout; R1-R3).  Secret key
+ * s in {0,1}^n, TRLWE key S in {0,1}^N; cloud key = bootstrapping key
+ * BK_i = TRGSW_S(s_i) (uint32[n][2l][2][N], row r = c*l + j) and key-switching
+ * key KSK[i][j][v] = LWE_s(v S_i 2^{32-(j+1)basebits}) (uint32[N][t][base][n+1],
+ * v = 0 rows zero).  Both outputs are library-owned. */
+she_status she_keygen(const she_params* p, uint64_t seed, she_secret_key** sk,
+                      she_cloud_key** ck);
+void she_secret_key_free(she_secret_key* sk);
+void she_cloud_key_free(she_cloud_key* ck);
+
+/* Export the documented layouts into caller buffers (host).  Pass buf = NULL
+ * to query the size in bytes through *len.
+ *   secret key: uint8 s[n] then uint8 S[N]
+ *   cloud key : uint32 bk[n][2l][2][N] then uint32 ksk[N][t][base][n+1]      */
+she_status she_secret_key_export(const she_secret_key* sk, void* buf, size_t* len);
+she_status she_cloud_key_export(const she_cloud_key* ck, void* buf, size_t* len);
+/* Build a cloud key from the exported layout (e.g. received from a client). */
+she_status she_cloud_key_import(const she_params* p, const void* buf, size_t len,
+                                she_cloud_key** ck);
+
+/* epsilon(bits): ciphertext idx draws mask/noise number first_index + idx
+ * (host buffers; out = count * stride uint32, padding zeroed). */
+she_status she_encrypt_bits(const she_secret_key* sk, const uint8_t* bits, size_t count,
+                            uint64_t seed, uint64_t first_index, uint32_t* out);
+/* delta(c): bit = [(int32)(b - <a,s>) >= 0]  (R5). */
+she_status she_decrypt_bits(const she_secret_key* sk, const uint32_t* in, size_t count,
+                            uint8_t* bits);
+
+/* ---- server side (device) ------------------------------------------------ */
+
+/* Create a context on CUDA `device`: uploads BK and KSK, transforms BK into the
+ * Goldilocks NTT domain (with N^-1 folded in) and keeps it resident (L2
+ * persisting window).  rank/world describe the multi-GPU group this context
+ * belongs to (world = 1 for single GPU; the exchange between ranks is done by
+ * the caller's process group). */
+she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int device, int rank,
+                          int world, she_ctx** ctx);
+she_status she_ctx_destroy(she_ctx* ctx);
+/* Block until all work the context enqueued has finished; reports async faults. */
+she_status she_ctx_synchronize(she_ctx* ctx);
+
+/* Per-kernel device timing for measurement (bench.py): when enabled, CUDA
+ * events are recorded on the launch stream around every blind-rotation (K3)
+ * and key-switch (K4) launch; she_ctx_timing synchronises on them and returns
+ * the accumulated milliseconds and launch counts (reset != 0 clears them). */
+she_status she_ctx_enable_timing(she_ctx* ctx, int on);
+she_status she_ctx_timing(she_ctx* ctx, int reset, double* br_ms, double* ks_ms,
+                          uint64_t* br_launches, uint64_t* ks_launches);
+
+/* K6: peak Goldilocks modmul throughput of `device` (independent chains of the
+ * kernel's own field multiplication on every SM; the roofline denominator). */
+she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms);
+
+/* Bootstrapped gates, all with the same op (north_star signature).  a, b, c,
+ * out: device, count slots each (c read only for MUX, b not read for
+ * NOT/COPY; unused pointers may be NULL).  out must not overlap any input.
+ * stream: a cudaStream_t (NULL = legacy default stream). */
+she_status she_gate_batch(she_ctx* ctx, int op, const uint32_t* a, const uint32_t* b,
+                          const uint32_t* c, uint32_t* out, size_t count, void* stream);
+
+/* Mixed-op batch: ops is a DEVICE array of count she_op codes. */
+she_status she_gate_batch_ops(she_ctx* ctx, const uint8_t* ops, const uint32_t* a,
+                              const uint32_t* b, const uint32_t* c, uint32_t* out,
+                              size_t count, void* stream);
+
+/* Same as she_gate_batch_ops with HOST buffers (ops, a, b, c, out): copies in,
+ * evaluates, copies out and synchronises the stream (the end-to-end call). */
+she_status she_gate_batch_ops_host(she_ctx* ctx, const uint8_t* ops, const uint32_t* a,
+                                   const uint32_t* b, const uint32_t* c, uint32_t* out,
+                                   size_t count, void* stream);
+
+/* Wire-table level (the scheduler's unit of work): gate g reads slots
+ * wires[in[3g+j] & 0x7fffffff], negated when bit 31 of in[3g+j] is set, and
+ * writes slot wires[out_idx[g]].  ops, in, out_idx: DEVICE arrays. */
+she_status she_gate_level(she_ctx* ctx, uint32_t* wires, const uint8_t* ops,
+                          const uint32_t* in, const uint32_t* out_idx, size_t count,
+                          void* stream);
+
+/* ---- layer calls (§3; scheduled by the library) ------------------ */
+/* Weight codes (host int8): 0 = zero weight; w = +-(e+1) means sign * 2^-e,
+ * e in 0..7 (PAPER.md:118 weightQ; the term is sign * (x >> e), R12).
+ * Encrypted words in/out are device slot arrays in the layouts given. */
+
+/* conv (no bias) + shift-accumulate: in [H][W][C][w_in][stride], wq [Co][K][K][C],
+ * out [Ho][Wo][Co][*w_out][stride]; accumulators widen 1 bit per tree level up
+ * to acc_cap (16) bits, wrapping at the cap (R13).  relu != 0 applies the
+ * sign-bit ReLU to the outputs (out width then excludes nothing: same w_out). */
+she_status she_conv_shift_acc(she_ctx* ctx, const uint32_t* in, int H, int W, int C, int w_in,
+                              const int8_t* wq, int Co, int K, int stride, int pad, int acc_cap,
+                              int relu, uint32_t* out, int* w_out, void* stream);
+/* fully connected: in [K][w_in][stride], wq [M][K], out [M][*w_out][stride]. */
+she_status she_fc_shift_acc(she_ctx* ctx, const uint32_t* in, int K, int w_in, const int8_t* wq,
+                            int M, int acc_cap, int relu, uint32_t* out, int* w_out,
+                            void* stream);
+/* ReLU on `words` encrypted two's-complement words of `width` bits:
+ * R_i = AND(X_i, NOT sign) (SPEC.md:193-201 reading of PAPER.md F2). */
+she_status she_relu(she_ctx* ctx, const uint32_t* in, size_t words, int width, uint32_t* out,
+                    void* stream);
+/* 2x2 stride-2 max-pool on [H][W][C][w][stride] signed words: each max is a
+ * subtract-comparator sign driving per-bit MUXes (PAPER.md F2). */
+she_status she_maxpool2x2(she_ctx* ctx, const uint32_t* in, int H, int W, int C, int w,
+                          uint32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHE_H_ */

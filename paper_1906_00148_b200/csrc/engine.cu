@@ -1,0 +1,749 @@
+// engine.cu — server side of the B200 gate-bootstrapping engine (sm_100a).
+//
+// Kernels:
+//   K1 bk_transform_kernel  BK -> Goldilocks NTT domain, N^-1 folded (setup)
+//   K2+K3 br_kernel          gate prologue (linear form, modulus switch), blind
+//                            rotation of n CMux iterations with the accumulator
+//                            resident in shared memory, sample extraction
+//   K4 ks_kernel             MUX combine + key switch N -> n
+// One CTA of 4 warps is one blind-rotation lane; a gate is 1 lane (2 for MUX).
+// PAPER.md:31 (bootstrapping), :110 (gates), :188 (TFHE setting, key switching).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "bootstrap_core.cuh"
+#include "common.h"
+#include "keys.h"
+
+using namespace she;
+
+namespace {
+
+constexpr int kWarps = 4;            // 2l rows (l = 2)
+constexpr int kBRThreads = 32 * kWarps;
+constexpr uint32_t kMu = 1u << 29;
+
+// ---------------------------------------------------------------------------
+// gate sources: batch mode (a/b/c/out arrays) or wire-table mode (indices)
+// ---------------------------------------------------------------------------
+struct GateSrc {
+  const uint8_t* ops;  // per-gate ops (device) or nullptr -> uniform_op
+  int uniform_op;
+  const uint32_t* in[3];  // batch mode: slot arrays a, b, c
+  uint32_t* out;          // batch mode output
+  const uint32_t* wires;  // wire mode table (read)
+  uint32_t* out_wires;    // wire mode table (write)
+  const uint32_t* in_idx; // wire mode: 3 per gate, bit 31 = negate
+  const uint32_t* out_idx;
+  uint32_t stride;
+  uint32_t count;
+};
+
+__device__ __forceinline__ int gate_op(const GateSrc& s, uint32_t g) {
+  return s.ops ? (int)s.ops[g] : s.uniform_op;
+}
+__device__ __forceinline__ const uint32_t* gate_in(const GateSrc& s, uint32_t g, int j, bool& neg) {
+  if (s.in_idx) {
+    const uint32_t v = s.in_idx[3 * g + j];
+    neg = (v >> 31) != 0;
+    return s.wires + (size_t)(v & 0x7FFFFFFFu) * s.stride;
+  }
+  neg = false;
+  return s.in[j] + (size_t)g * s.stride;
+}
+__device__ __forceinline__ uint32_t* gate_out(const GateSrc& s, uint32_t g) {
+  if (s.out_idx) return s.out_wires + (size_t)s.out_idx[g] * s.stride;
+  return s.out + (size_t)g * s.stride;
+}
+
+// Linear form of blind-rotation lane h of a gate (DESIGN.md §2 gate table):
+//   c = (0, kappa) + k0 * in[0] + k1 * in[j1]
+struct LaneForm {
+  uint32_t kappa;
+  int k0, k1, j1;
+  bool valid;
+};
+__device__ __forceinline__ LaneForm lane_form(int op, int h) {
+  LaneForm f{0, 0, 0, 1, true};
+  if (op != SHE_MUX && h) f.valid = false;
+  switch (op) {
+    case SHE_AND:  f = {0u - kMu, 1, 1, 1, f.valid}; break;
+    case SHE_NAND: f = {kMu, -1, -1, 1, f.valid}; break;
+    case SHE_OR:   f = {kMu, 1, 1, 1, f.valid}; break;
+    case SHE_NOR:  f = {0u - kMu, -1, -1, 1, f.valid}; break;
+    case SHE_XOR:  f = {2 * kMu, 2, 2, 1, f.valid}; break;
+    case SHE_XNOR: f = {0u - 2 * kMu, -2, -2, 1, f.valid}; break;
+    case SHE_MUX:  f = h ? LaneForm{0u - kMu, -1, 1, 2, true} : LaneForm{0u - kMu, 1, 1, 1, true}; break;
+    default: f.valid = false;  // NOT / COPY: no bootstrapping
+  }
+  return f;
+}
+
+struct BRArgs {
+  GateSrc src;
+  uint32_t lane_base;        // first lane of this launch (lane = 2 g + h)
+  const uint64_t* bk;        // [n][2l][2][N] NTT storage order
+  const uint64_t* tw;        // [L][L]
+  const uint64_t* itw;       // [L][L]
+  uint32_t* ext;             // [lanes][ext_stride] extracted samples (N+1 words)
+  uint32_t ext_stride;
+  br::Geometry geo;
+};
+
+template <class S>
+constexpr size_t br_smem_bytes(uint32_t n) {
+  return (size_t)2 * S::N * 4 + (size_t)kWarps * S::L * (S::L + 1) * 8 + ((n + 1) * 2 + 15) / 16 * 16;
+}
+
+// K2 + K3: gate prologue, blind rotation, sample extraction for one lane.
+template <class S>
+__global__ void __launch_bounds__(kBRThreads) br_kernel(BRArgs args) {
+  constexpr int N = S::N, L = S::L;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* acc = reinterpret_cast<uint32_t*>(smem);
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem + 2 * N * 4);
+  uint16_t* abar = reinterpret_cast<uint16_t*>(buf + kWarps * L * (L + 1));
+
+  const GateSrc& src = args.src;
+  const br::Geometry& geo = args.geo;
+  const uint32_t lane_id = args.lane_base + blockIdx.x;
+  const uint32_t g = lane_id >> 1, h = lane_id & 1;
+  if (g >= src.count) return;
+  const LaneForm f = lane_form(gate_op(src, g), (int)h);
+  if (!f.valid) return;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t n = geo.n;
+
+  // K2: gate linear form and modulus switch to Z_2N (R7).
+  {
+    bool n0, n1;
+    const uint32_t* x0 = gate_in(src, g, 0, n0);
+    const uint32_t* x1 = gate_in(src, g, f.j1, n1);
+    const uint32_t k0 = (uint32_t)(n0 ? -f.k0 : f.k0), k1 = (uint32_t)(n1 ? -f.k1 : f.k1);
+    for (uint32_t k = tid; k <= n; k += kBRThreads) {
+      uint32_t v = k0 * x0[k] + k1 * x1[k];
+      if (k == n) v += f.kappa;
+      abar[k] = (uint16_t)br::modswitch(v, geo.lg2N);
+    }
+  }
+  __syncthreads();
+  // ACC = (0, X^{-bbar} v)
+  {
+    const uint32_t bbar = abar[n];
+    for (int m = tid; m < N; m += kBRThreads) {
+      acc[m] = 0;
+      acc[N + m] = br::testvec_coeff(m, bbar, N);
+    }
+  }
+  __syncthreads();
+
+  uint64_t* row = br::buf_row<S>(buf, warp);
+  const bool active = lane < L;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t a = abar[i];
+    if (a == 0) continue;  // R9 (uniform across the CTA)
+    // forward: decompose row `warp`, pass 1, transpose, twist, pass 2
+    {
+      uint64_t x[L];
+      if (active) {
+        br::load_digits<S>(geo, warp, lane, acc, a, x);
+        br::fwd_pass1_store<S>(lane, x, row);
+      }
+      __syncwarp();
+      if (active) br::fwd_pass2_load<S>(lane, row, args.tw, x);
+      __syncwarp();
+      if (active) br::fwd_pass2_store<S>(lane, x, row);
+    }
+    __syncthreads();
+    br::pointwise<S>(tid, kBRThreads, kWarps, buf, args.bk + (size_t)i * kWarps * 2 * N);
+    __syncthreads();
+    if (warp < 2) {  // inverse of output component c = warp, ACC_c += result
+      uint64_t y[L];
+      if (active) br::inv_pass2_load<S>(lane, row, y);
+      __syncwarp();
+      if (active) br::inv_pass2_store<S>(lane, y, args.itw, row);
+      __syncwarp();
+      if (active) br::inv_pass1_acc<S>(lane, row, acc + warp * N);
+    }
+    __syncthreads();
+  }
+
+  // sample extract: a'_0 = A_0, a'_j = -A_{N-j}, b' = B_0
+  uint32_t* e = args.ext + (size_t)lane_id * args.ext_stride;
+  for (int m = tid; m <= N; m += kBRThreads) {
+    uint32_t v;
+    if (m == 0) v = acc[0];
+    else if (m < N) v = 0u - acc[N - m];
+    else v = acc[N];
+    e[m] = v;
+  }
+}
+
+// K1: BK -> NTT domain (signed lift, N^-1 folded).  One warp per polynomial.
+template <class S>
+__global__ void bk_transform_kernel(const uint32_t* bk, uint64_t* out, const uint64_t* tw,
+                                    uint64_t ninv, uint32_t polys) {
+  constexpr int N = S::N, L = S::L;
+  __shared__ uint64_t row[L * (L + 1)];
+  const uint32_t poly = blockIdx.x;
+  if (poly >= polys) return;
+  const int lane = threadIdx.x;
+  uint64_t x[L];
+  if (lane < L) {
+    br::load_poly_signed<S>(lane, bk + (size_t)poly * N, x);
+    br::fwd_pass1_store<S>(lane, x, row);
+  }
+  __syncwarp();
+  if (lane < L) {
+    br::fwd_pass2_load<S>(lane, row, tw, x);
+    br::fwd_pass2_store_scaled<S>(lane, x, ninv, out + (size_t)poly * N);
+  }
+}
+
+// K4: MUX combine + key switch.  Thread k owns output word k; the CTA owns G
+// gates whose accumulators live in registers.  KSK device layout:
+// [N][t][3][stride] (v = 1..3 rows, padded with zero words).
+struct KSArgs {
+  GateSrc src;
+  const uint32_t* ext;
+  uint32_t ext_stride;
+  const uint32_t* ksk;
+  uint32_t N, n, t;
+};
+
+template <int G, int CH>
+__global__ void __launch_bounds__(512) ks_kernel(KSArgs args) {
+  __shared__ uint32_t ys[G][CH];
+  __shared__ uint32_t bprime[G];
+  __shared__ int gops[G];
+  const GateSrc& src = args.src;
+  const uint32_t k = threadIdx.x, g0 = blockIdx.x * G;
+  const uint32_t N = args.N, n = args.n, t = args.t, stride = src.stride;
+  const uint32_t round = 1u << (32 - 2 * t - 1);  // R10: round to the top 2t bits
+
+  if (k < G) {
+    const uint32_t g = g0 + k;
+    int op = g < src.count ? gate_op(src, g) : -1;
+    gops[k] = op;
+    uint32_t b = 0;
+    if (op >= 0 && op < SHE_NOT) {
+      b = args.ext[(size_t)(2 * g) * args.ext_stride + N];
+      if (op == SHE_MUX) b += args.ext[(size_t)(2 * g + 1) * args.ext_stride + N] + kMu;
+    }
+    bprime[k] = b;
+  }
+  __syncthreads();
+  uint32_t acc[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) acc[q] = (k == n) ? bprime[q] : 0u;
+
+  for (uint32_t i0 = 0; i0 < N; i0 += CH) {
+    __syncthreads();
+    for (uint32_t idx = k; idx < (uint32_t)G * CH; idx += blockDim.x) {
+      const uint32_t q = idx / CH, ii = idx % CH, g = g0 + q;
+      const int op = gops[q];
+      uint32_t y = 0;  // digits of 0 are 0: gates without KS subtract nothing
+      if (op >= 0 && op < SHE_NOT) {
+        uint32_t a = args.ext[(size_t)(2 * g) * args.ext_stride + i0 + ii];
+        if (op == SHE_MUX) a += args.ext[(size_t)(2 * g + 1) * args.ext_stride + i0 + ii];
+        y = a + round;
+      }
+      ys[q][ii] = y;
+    }
+    __syncthreads();
+    for (uint32_t ii = 0; ii < CH; ++ii) {
+      const uint32_t* rows = args.ksk + (size_t)(i0 + ii) * t * 3 * stride + k;
+      for (uint32_t j = 0; j < t; ++j) {
+        const uint32_t r1 = __ldg(rows + (size_t)(3 * j + 0) * stride);
+        const uint32_t r2 = __ldg(rows + (size_t)(3 * j + 1) * stride);
+        const uint32_t r3 = __ldg(rows + (size_t)(3 * j + 2) * stride);
+        const uint32_t sh = 30 - 2 * j;
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const uint32_t d = (ys[q][ii] >> sh) & 3u;
+          const uint32_t r = d == 0 ? 0u : d == 1 ? r1 : d == 2 ? r2 : r3;
+          acc[q] -= r;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const uint32_t g = g0 + q;
+    const int op = gops[q];
+    if (op < 0) continue;
+    uint32_t* o = gate_out(src, g);
+    if (k >= stride) continue;
+    uint32_t v;
+    if (op == SHE_NOT || op == SHE_COPY) {
+      bool neg;
+      const uint32_t* a = gate_in(src, g, 0, neg);
+      if (op == SHE_NOT) neg = !neg;
+      v = k <= n ? (neg ? 0u - a[k] : a[k]) : 0u;
+    } else {
+      v = k <= n ? acc[q] : 0u;
+    }
+    o[k] = v;
+  }
+}
+
+constexpr int kKsG = 16, kKsCH = 64;
+
+// K6: peak Goldilocks modmul throughput (roofline denominator).  Each thread
+// runs kChains independent chains of the same gl::mul the NTT uses.
+constexpr int kChains = 8;
+__global__ void modmul_peak_kernel(uint64_t* sink, uint32_t iters, uint64_t seed) {
+  uint64_t x[kChains], c[kChains];
+#pragma unroll
+  for (int q = 0; q < kChains; ++q) {
+    x[q] = seed ^ (0x9E3779B97F4A7C15ull * (threadIdx.x + 1 + q * 977 + blockIdx.x * 131));
+    c[q] = x[q] * 0xBF58476D1CE4E5B9ull + q;
+  }
+  for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < kChains; ++q) x[q] = gl::mul(x[q], c[q]);
+  }
+  uint64_t r = 0;
+#pragma unroll
+  for (int q = 0; q < kChains; ++q) r ^= x[q];
+  if (r == 0x12345) sink[0] = r;  // keep the work alive
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct she_ctx {
+  she_params p;
+  int device = 0, rank = 0, world = 1;
+  br::Geometry geo;
+  uint32_t stride = 0, ext_stride = 0;
+  uint64_t* bk = nullptr;
+  size_t bk_bytes = 0;
+  uint32_t* ksk = nullptr;
+  uint64_t* tw = nullptr;
+  uint64_t* itw = nullptr;
+  uint32_t* ext = nullptr;
+  size_t ext_lanes = 0;
+  // staging for the host-buffer API
+  uint8_t* h_ops = nullptr;
+  uint32_t* h_io = nullptr;
+  size_t h_cap = 0;
+  bool persist = false;
+  std::mutex mu;
+  // per-kernel CUDA-event timing (she_ctx_enable_timing / she_ctx_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<cudaEvent_t> ev_marks;  // triples: before BR, after BR, after KS
+  double br_ms = 0, ks_ms = 0;
+  uint64_t br_launches = 0, ks_launches = 0, lanes = 0;
+};
+
+namespace {
+
+she_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(SHE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(call)                                         \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+br::Geometry make_geometry(const she_params& p) {
+  br::Geometry g;
+  g.N = p.N;
+  g.n = p.n;
+  g.l = p.l;
+  g.bg_bits = p.bg_bits;
+  g.lg2N = 0;
+  while ((1u << g.lg2N) < 2 * p.N) g.lg2N++;
+  uint32_t off = 0;
+  for (uint32_t j = 1; j <= p.l; ++j) off += (1u << (p.bg_bits - 1)) << (32 - j * p.bg_bits);
+  off += 1u << (32 - p.l * p.bg_bits - 1);
+  g.dec_offset = off;
+  return g;
+}
+
+template <class S>
+she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
+  const she_params& p = ctx->p;
+  const size_t polys = (size_t)p.n * 2 * p.l * 2;
+  ctx->bk_bytes = polys * p.N * sizeof(uint64_t);
+  CK(cudaMalloc(&ctx->bk, ctx->bk_bytes));
+  CK(cudaMalloc(&ctx->tw, sizeof(uint64_t) * S::L * S::L));
+  CK(cudaMalloc(&ctx->itw, sizeof(uint64_t) * S::L * S::L));
+  std::vector<uint64_t> tw(S::L * S::L), itw(S::L * S::L);
+  ntt::make_twists(S::N, S::L, S::SH, tw.data(), itw.data());
+  CK(cudaMemcpy(ctx->tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->itw, itw.data(), itw.size() * 8, cudaMemcpyHostToDevice));
+  uint32_t* d_bk32 = nullptr;
+  CK(cudaMalloc(&d_bk32, polys * p.N * 4));
+  CK(cudaMemcpy(d_bk32, ck->bk.data(), polys * p.N * 4, cudaMemcpyHostToDevice));
+  const uint64_t ninv = gl::pow(p.N, gl::P - 2);
+  bk_transform_kernel<S><<<(unsigned)polys, 32>>>(d_bk32, ctx->bk, ctx->tw, ninv, (uint32_t)polys);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  cudaFree(d_bk32);
+  CK(cudaFuncSetAttribute(br_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)br_smem_bytes<S>(p.n)));
+  return SHE_OK;
+}
+
+she_status ensure_ext(she_ctx* ctx, size_t lanes) {
+  if (lanes <= ctx->ext_lanes) return SHE_OK;
+  if (ctx->ext) {
+    CK(cudaDeviceSynchronize());
+    cudaFree(ctx->ext);
+    ctx->ext = nullptr;
+  }
+  size_t want = std::max(lanes, (size_t)1024);
+  CK(cudaMalloc(&ctx->ext, want * ctx->ext_stride * 4));
+  ctx->ext_lanes = want;
+  return SHE_OK;
+}
+
+// Gates per BR+KS launch pair (bounds the extracted-sample scratch).
+constexpr size_t kChunk = 1 << 16;
+
+cudaEvent_t mark(she_ctx* ctx, cudaStream_t stream) {
+  cudaEvent_t e;
+  if (!ctx->ev_pool.empty()) {
+    e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+  } else if (cudaEventCreate(&e) != cudaSuccess) {
+    return nullptr;
+  }
+  cudaEventRecord(e, stream);
+  ctx->ev_marks.push_back(e);
+  return e;
+}
+
+template <class S>
+she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
+  const size_t total = src.count;
+  she_status st = ensure_ext(ctx, 2 * std::min(total, kChunk));
+  if (st != SHE_OK) return st;
+  const size_t smem = br_smem_bytes<S>(ctx->p.n);
+  for (size_t g0 = 0; g0 < total; g0 += kChunk) {
+    const size_t cnt = std::min(kChunk, total - g0);
+    GateSrc s = src;
+    // shift the gate window: both modes index gates from 0 within a launch
+    if (s.ops) s.ops += g0;
+    if (s.in_idx) {
+      s.in_idx += 3 * g0;
+      s.out_idx += g0;
+    } else {
+      for (int j = 0; j < 3; ++j)
+        if (s.in[j]) s.in[j] += g0 * s.stride;
+      s.out += g0 * s.stride;
+    }
+    s.count = (uint32_t)cnt;
+    BRArgs a;
+    a.src = s;
+    a.lane_base = 0;
+    a.bk = ctx->bk;
+    a.tw = ctx->tw;
+    a.itw = ctx->itw;
+    a.ext = ctx->ext;
+    a.ext_stride = ctx->ext_stride;
+    a.geo = ctx->geo;
+
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * cnt));
+    cfg.blockDim = dim3(kBRThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    if (ctx->persist) {
+      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[0].val.accessPolicyWindow.base_ptr = ctx->bk;
+      attr[0].val.accessPolicyWindow.num_bytes = ctx->bk_bytes;
+      attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    if (ctx->timing) mark(ctx, stream);
+    CK(cudaLaunchKernelEx(&cfg, br_kernel<S>, a));
+    if (ctx->timing) mark(ctx, stream);
+
+    KSArgs k;
+    k.src = s;
+    k.ext = ctx->ext;
+    k.ext_stride = ctx->ext_stride;
+    k.ksk = ctx->ksk;
+    k.N = ctx->p.N;
+    k.n = ctx->p.n;
+    k.t = ctx->p.ks_t;
+    ks_kernel<kKsG, kKsCH><<<(unsigned)((cnt + kKsG - 1) / kKsG), ctx->stride, 0, stream>>>(k);
+    CK(cudaGetLastError());
+    if (ctx->timing) mark(ctx, stream);
+    ctx->br_launches++;
+    ctx->ks_launches++;
+  }
+  return SHE_OK;
+}
+
+she_status dispatch(she_ctx* ctx, const GateSrc& src, cudaStream_t stream) {
+  if (src.count == 0) return SHE_OK;
+  if (ctx->p.N == 1024) return run_gates<ntt::Shape<1024>>(ctx, src, stream);
+  return run_gates<ntt::Shape<256>>(ctx, src, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int device, int rank,
+                          int world, she_ctx** out) {
+  she_status st = check_params(p);
+  if (st != SHE_OK) return st;
+  if (!ck || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  if (memcmp(&ck->p, p, sizeof(she_params)) != 0)
+    return fail(SHE_ERR_PARAMS, "cloud key was made for other parameters");
+  if (world < 1 || rank < 0 || rank >= world) return fail(SHE_ERR_ARG, "bad rank/world");
+  CK(cudaSetDevice(device));
+  she_ctx* ctx = new (std::nothrow) she_ctx;
+  if (!ctx) return fail(SHE_ERR_OOM, "host allocation failed");
+  ctx->p = *p;
+  ctx->device = device;
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->geo = make_geometry(*p);
+  ctx->stride = (uint32_t)lwe_stride(*p);
+  ctx->ext_stride = (p->N + 1 + 31) / 32 * 32;
+  st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
+  if (st != SHE_OK) {
+    she_ctx_destroy(ctx);
+    return st;
+  }
+  // KSK repacked to [N][t][3][stride] (drop v = 0, pad rows to the slot stride)
+  {
+    const uint32_t N = p->N, n = p->n, t = p->ks_t, base = 1u << p->ks_base_bits;
+    const size_t sz = (size_t)N * t * 3 * ctx->stride;
+    std::vector<uint32_t> h(sz, 0);
+    for (uint32_t i = 0; i < N; ++i)
+      for (uint32_t j = 0; j < t; ++j)
+        for (uint32_t v = 1; v < base; ++v)
+          memcpy(&h[(((size_t)i * t + j) * 3 + (v - 1)) * ctx->stride],
+                 &ck->ksk[(((size_t)i * t + j) * base + v) * (n + 1)], (n + 1) * 4);
+    cudaError_t e = cudaMalloc(&ctx->ksk, sz * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->ksk, h.data(), sz * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      she_ctx_destroy(ctx);
+      return cuda_fail(e, "KSK upload");
+    }
+  }
+  // keep the NTT-domain BK L2-resident (persisting window on the BR launches)
+  {
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
+    if (maxp > 0) {
+      size_t want = std::min((size_t)maxp, ctx->bk_bytes);
+      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+        ctx->persist = true;
+    }
+    cudaGetLastError();
+  }
+  *out = ctx;
+  return SHE_OK;
+}
+
+she_status she_ctx_destroy(she_ctx* ctx) {
+  if (!ctx) return SHE_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  cudaFree(ctx->bk);
+  cudaFree(ctx->ksk);
+  cudaFree(ctx->tw);
+  cudaFree(ctx->itw);
+  cudaFree(ctx->ext);
+  cudaFree(ctx->h_ops);
+  cudaFree(ctx->h_io);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_marks) cudaEventDestroy(e);
+  delete ctx;
+  cudaGetLastError();
+  return SHE_OK;
+}
+
+she_status she_ctx_enable_timing(she_ctx* ctx, int on) {
+  if (!ctx) return fail(SHE_ERR_ARG, "NULL context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ctx->timing = on != 0;
+  return SHE_OK;
+}
+
+she_status she_ctx_timing(she_ctx* ctx, int reset, double* br_ms, double* ks_ms,
+                          uint64_t* br_launches, uint64_t* ks_launches) {
+  if (!ctx) return fail(SHE_ERR_ARG, "NULL context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  for (size_t q = 0; q + 2 < ctx->ev_marks.size(); q += 3) {
+    float a = 0, b = 0;
+    CK(cudaEventSynchronize(ctx->ev_marks[q + 2]));
+    CK(cudaEventElapsedTime(&a, ctx->ev_marks[q], ctx->ev_marks[q + 1]));
+    CK(cudaEventElapsedTime(&b, ctx->ev_marks[q + 1], ctx->ev_marks[q + 2]));
+    ctx->br_ms += a;
+    ctx->ks_ms += b;
+  }
+  for (cudaEvent_t e : ctx->ev_marks) ctx->ev_pool.push_back(e);
+  ctx->ev_marks.clear();
+  if (br_ms) *br_ms = ctx->br_ms;
+  if (ks_ms) *ks_ms = ctx->ks_ms;
+  if (br_launches) *br_launches = ctx->br_launches;
+  if (ks_launches) *ks_launches = ctx->ks_launches;
+  if (reset) {
+    ctx->br_ms = ctx->ks_ms = 0;
+    ctx->br_launches = ctx->ks_launches = 0;
+  }
+  return SHE_OK;
+}
+
+she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms) {
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  uint64_t* sink = nullptr;
+  CK(cudaMalloc(&sink, 8));
+  const unsigned blocks = (unsigned)sms * 8, threads = 256;
+  const uint32_t iters = 4096;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  modmul_peak_kernel<<<blocks, threads>>>(sink, iters, 1);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    CK(cudaEventRecord(e0));
+    modmul_peak_kernel<<<blocks, threads>>>(sink, iters, rep + 2);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    best = std::min(best, t);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  const double total = (double)blocks * threads * kChains * iters;
+  if (modmul_per_s) *modmul_per_s = total / (best * 1e-3);
+  if (ms) *ms = best;
+  return SHE_OK;
+}
+
+she_status she_ctx_synchronize(she_ctx* ctx) {
+  if (!ctx) return fail(SHE_ERR_ARG, "NULL context");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  return SHE_OK;
+}
+
+static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  if (!a || !b) return false;
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + nb && y < x + na;
+}
+
+static she_status gate_batch_common(she_ctx* ctx, const uint8_t* ops, int op, const uint32_t* a,
+                                    const uint32_t* b, const uint32_t* c, uint32_t* out,
+                                    size_t count, void* stream) {
+  if (count == 0) return SHE_OK;
+  if (!ctx || !a || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  if (!ops && (op < 0 || op > SHE_COPY)) return fail(SHE_ERR_ARG, "bad op %d", op);
+  if (!ops && op != SHE_NOT && op != SHE_COPY && !b) return fail(SHE_ERR_ARG, "b is NULL");
+  if (!ops && op == SHE_MUX && !c) return fail(SHE_ERR_ARG, "MUX needs c");
+  if (count > 0x7FFFFFFFull) return fail(SHE_ERR_ARG, "count too large");
+  const size_t bytes = count * ctx->stride * 4;
+  if (overlaps(out, bytes, a, bytes) || overlaps(out, bytes, b, bytes) ||
+      overlaps(out, bytes, c, bytes))
+    return fail(SHE_ERR_ARG, "out overlaps an input");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  GateSrc s = {};
+  s.ops = ops;
+  s.uniform_op = op;
+  s.in[0] = a;
+  s.in[1] = b ? b : a;
+  s.in[2] = c ? c : a;
+  s.out = out;
+  s.stride = ctx->stride;
+  s.count = (uint32_t)count;
+  return dispatch(ctx, s, (cudaStream_t)stream);
+}
+
+she_status she_gate_batch(she_ctx* ctx, int op, const uint32_t* a, const uint32_t* b,
+                          const uint32_t* c, uint32_t* out, size_t count, void* stream) {
+  return gate_batch_common(ctx, nullptr, op, a, b, c, out, count, stream);
+}
+
+she_status she_gate_batch_ops(she_ctx* ctx, const uint8_t* ops, const uint32_t* a,
+                              const uint32_t* b, const uint32_t* c, uint32_t* out, size_t count,
+                              void* stream) {
+  if (count && !ops) return fail(SHE_ERR_ARG, "ops is NULL");
+  if (count && (!b || !c)) return fail(SHE_ERR_ARG, "mixed batches need a, b and c");
+  return gate_batch_common(ctx, ops, 0, a, b, c, out, count, stream);
+}
+
+she_status she_gate_batch_ops_host(she_ctx* ctx, const uint8_t* ops, const uint32_t* a,
+                                   const uint32_t* b, const uint32_t* c, uint32_t* out,
+                                   size_t count, void* stream) {
+  if (count == 0) return SHE_OK;
+  if (!ctx || !ops || !a || !b || !c || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t slots = count * ctx->stride;
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->h_cap < count) {
+      cudaStreamSynchronize(st);
+      cudaFree(ctx->h_ops);
+      cudaFree(ctx->h_io);
+      ctx->h_ops = nullptr;
+      ctx->h_io = nullptr;
+      ctx->h_cap = 0;
+      CK(cudaMalloc(&ctx->h_ops, count));
+      CK(cudaMalloc(&ctx->h_io, 4 * slots * 4));
+      ctx->h_cap = count;
+    }
+    CK(cudaMemcpyAsync(ctx->h_ops, ops, count, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->h_io, a, slots * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->h_io + slots, b, slots * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->h_io + 2 * slots, c, slots * 4, cudaMemcpyHostToDevice, st));
+  }
+  she_status s = she_gate_batch_ops(ctx, ctx->h_ops, ctx->h_io, ctx->h_io + slots,
+                                    ctx->h_io + 2 * slots, ctx->h_io + 3 * slots, count, stream);
+  if (s != SHE_OK) return s;
+  CK(cudaMemcpyAsync(out, ctx->h_io + 3 * slots, slots * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return SHE_OK;
+}
+
+she_status she_gate_level(she_ctx* ctx, uint32_t* wires, const uint8_t* ops, const uint32_t* in,
+                          const uint32_t* out_idx, size_t count, void* stream) {
+  if (count == 0) return SHE_OK;
+  if (!ctx || !wires || !ops || !in || !out_idx) return fail(SHE_ERR_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  GateSrc s = {};
+  s.ops = ops;
+  s.wires = wires;
+  s.out_wires = wires;
+  s.in_idx = in;
+  s.out_idx = out_idx;
+  s.stride = ctx->stride;
+  s.count = (uint32_t)count;
+  return dispatch(ctx, s, (cudaStream_t)stream);
+}
+
+}  // extern "C"

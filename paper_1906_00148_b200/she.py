@@ -1,0 +1,255 @@
+"""Thin Python binding of libshe.so (include/she.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libshe.so; this module
+converts numpy arrays / torch tensors to pointers and raises on error.  There
+is no CPU fallback: if libshe.so is missing or a call fails, it raises.
+
+Device buffers are torch tensors of dtype int32 holding torch-allocated CUDA
+memory (bit patterns of the uint32 torus words); host buffers are numpy
+uint32 / uint8 arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libshe.so")
+
+SHE_AND, SHE_NAND, SHE_OR, SHE_NOR, SHE_XOR, SHE_XNOR, SHE_MUX, SHE_NOT, SHE_COPY = range(9)
+
+_STATUS = {0: "SHE_OK", -1: "SHE_ERR_ARG", -2: "SHE_ERR_PARAMS", -3: "SHE_ERR_SHAPE",
+           -4: "SHE_ERR_CUDA", -5: "SHE_ERR_NCCL", -6: "SHE_ERR_OOM", -7: "SHE_ERR_STATE"}
+
+
+class SheError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class she_params(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_uint32), ("k", ctypes.c_uint32), ("n", ctypes.c_uint32),
+                ("bg_bits", ctypes.c_uint32), ("l", ctypes.c_uint32),
+                ("ks_base_bits", ctypes.c_uint32), ("ks_t", ctypes.c_uint32),
+                ("alpha_lwe", ctypes.c_double), ("alpha_bk", ctypes.c_double)]
+
+    @classmethod
+    def of(cls, p) -> "she_params":
+        return cls(p.N, p.k, p.n, p.bg_bits, p.l, p.ks_base_bits, p.ks_t, p.alpha_lwe, p.alpha_bk)
+
+
+_lib = None
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree libshe.so; raise (never fall back) if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run paper_1906_00148_b200.build (no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER(she_params)
+        sig = {
+            "she_lwe_stride": ([P], _sz),
+            "she_last_error": ([], ctypes.c_char_p),
+            "she_keygen": ([P, ctypes.c_uint64, ctypes.POINTER(_vp), ctypes.POINTER(_vp)], ctypes.c_int),
+            "she_secret_key_free": ([_vp], None),
+            "she_cloud_key_free": ([_vp], None),
+            "she_secret_key_export": ([_vp, _vp, ctypes.POINTER(_sz)], ctypes.c_int),
+            "she_cloud_key_export": ([_vp, _vp, ctypes.POINTER(_sz)], ctypes.c_int),
+            "she_cloud_key_import": ([P, _vp, _sz, ctypes.POINTER(_vp)], ctypes.c_int),
+            "she_encrypt_bits": ([_vp, _vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
+            "she_decrypt_bits": ([_vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_ctx_create": ([P, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)],
+                               ctypes.c_int),
+            "she_ctx_destroy": ([_vp], ctypes.c_int),
+            "she_ctx_synchronize": ([_vp], ctypes.c_int),
+            "she_gate_batch": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_gate_batch_ops": ([_vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_gate_batch_ops_host": ([_vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_gate_level": ([_vp, _vp, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_ctx_enable_timing": ([_vp, ctypes.c_int], ctypes.c_int),
+            "she_ctx_timing": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64),
+                                ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
+            "she_bench_modmul_peak": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise SheError(status, lib().she_last_error().decode(errors="replace"))
+
+
+def _np_ptr(a: np.ndarray) -> int:
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data
+
+
+def _dev_ptr(t) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("device buffers must be contiguous CUDA tensors")
+    return t.data_ptr()
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def stride(params) -> int:
+    return int(lib().she_lwe_stride(ctypes.byref(she_params.of(params))))
+
+
+# ---- client side -------------------------------------------------------------
+
+class SecretKey:
+    def __init__(self, handle: int, params):
+        self.handle, self.params = handle, params
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.she_secret_key_free(self.handle)
+            self.handle = None
+
+    def export(self) -> bytes:
+        n = _sz(0)
+        _check(lib().she_secret_key_export(self.handle, None, ctypes.byref(n)))
+        buf = np.zeros(n.value, dtype=np.uint8)
+        _check(lib().she_secret_key_export(self.handle, _np_ptr(buf), ctypes.byref(n)))
+        return buf.tobytes()
+
+
+class CloudKey:
+    def __init__(self, handle: int, params):
+        self.handle, self.params = handle, params
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.she_cloud_key_free(self.handle)
+            self.handle = None
+
+    def export(self) -> np.ndarray:
+        n = _sz(0)
+        _check(lib().she_cloud_key_export(self.handle, None, ctypes.byref(n)))
+        buf = np.zeros(n.value // 4, dtype=np.uint32)
+        _check(lib().she_cloud_key_export(self.handle, _np_ptr(buf), ctypes.byref(n)))
+        return buf
+
+    @classmethod
+    def import_(cls, params, words: np.ndarray) -> "CloudKey":
+        words = np.ascontiguousarray(words, dtype=np.uint32)
+        h = _vp()
+        _check(lib().she_cloud_key_import(ctypes.byref(she_params.of(params)), _np_ptr(words),
+                                          words.nbytes, ctypes.byref(h)))
+        return cls(h.value, params)
+
+
+def she_keygen(params, seed: int):
+    sk, ck = _vp(), _vp()
+    _check(lib().she_keygen(ctypes.byref(she_params.of(params)), seed, ctypes.byref(sk),
+                            ctypes.byref(ck)))
+    return SecretKey(sk.value, params), CloudKey(ck.value, params)
+
+
+def she_encrypt_bits(sk: SecretKey, bits, seed: int, first_index: int = 0) -> np.ndarray:
+    bits = np.ascontiguousarray(bits, dtype=np.uint8).ravel()
+    out = np.zeros((len(bits), stride(sk.params)), dtype=np.uint32)
+    if len(bits):
+        _check(lib().she_encrypt_bits(sk.handle, _np_ptr(bits), len(bits), seed, first_index,
+                                      _np_ptr(out)))
+    return out
+
+
+def she_decrypt_bits(sk: SecretKey, cts) -> np.ndarray:
+    cts = np.ascontiguousarray(cts, dtype=np.uint32)
+    cts2 = cts.reshape(-1, cts.shape[-1])
+    assert cts2.shape[-1] == stride(sk.params)
+    bits = np.zeros(cts2.shape[0], dtype=np.uint8)
+    if len(bits):
+        _check(lib().she_decrypt_bits(sk.handle, _np_ptr(cts2), cts2.shape[0], _np_ptr(bits)))
+    return bits.reshape(cts.shape[:-1])
+
+
+# ---- server side -------------------------------------------------------------
+
+class Context:
+    """she_ctx: device keys (BK in the NTT domain, KSK) on one CUDA device."""
+
+    def __init__(self, params, ck: CloudKey, device: int = 0, rank: int = 0, world: int = 1):
+        h = _vp()
+        _check(lib().she_ctx_create(ctypes.byref(she_params.of(params)), ck.handle, device, rank,
+                                    world, ctypes.byref(h)))
+        self.handle, self.params, self.device = h.value, params, device
+        self.stride = stride(params)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().she_ctx_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def synchronize(self):
+        _check(lib().she_ctx_synchronize(self.handle))
+
+    def enable_timing(self, on: bool = True):
+        _check(lib().she_ctx_enable_timing(self.handle, int(on)))
+
+    def timing(self, reset: bool = False) -> dict:
+        br, ks = ctypes.c_double(), ctypes.c_double()
+        nb, nk = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().she_ctx_timing(self.handle, int(reset), ctypes.byref(br), ctypes.byref(ks),
+                                    ctypes.byref(nb), ctypes.byref(nk)))
+        return {"br_ms": br.value, "ks_ms": ks.value, "br_launches": nb.value,
+                "ks_launches": nk.value}
+
+
+def modmul_peak(device: int = 0) -> tuple[float, float]:
+    """K6: measured Goldilocks modmul/s on all SMs (and the kernel's ms)."""
+    r, ms = ctypes.c_double(), ctypes.c_double()
+    _check(lib().she_bench_modmul_peak(device, ctypes.byref(r), ctypes.byref(ms)))
+    return r.value, ms.value
+
+
+def she_gate_batch(ctx: Context, op: int, a, b, c, out, stream=None) -> None:
+    count = a.shape[0]
+    _check(lib().she_gate_batch(ctx.handle, op, _dev_ptr(a), _dev_ptr(b), _dev_ptr(c),
+                                _dev_ptr(out), count, _stream_ptr(stream)))
+
+
+def she_gate_batch_ops(ctx: Context, ops, a, b, c, out, stream=None) -> None:
+    count = a.shape[0]
+    _check(lib().she_gate_batch_ops(ctx.handle, _dev_ptr(ops), _dev_ptr(a), _dev_ptr(b),
+                                    _dev_ptr(c), _dev_ptr(out), count, _stream_ptr(stream)))
+
+
+def she_gate_batch_ops_host(ctx: Context, ops: np.ndarray, a: np.ndarray, b: np.ndarray,
+                            c: np.ndarray, out: np.ndarray, stream=None) -> None:
+    """Host buffers (ideally pinned): copy in, evaluate, copy out, synchronise."""
+    count = a.shape[0]
+    _check(lib().she_gate_batch_ops_host(ctx.handle, ops.ctypes.data, a.ctypes.data,
+                                         b.ctypes.data, c.ctypes.data, out.ctypes.data, count,
+                                         _stream_ptr(stream)))
+
+
+def she_gate_level(ctx: Context, wires, ops, ins, out_idx, stream=None) -> None:
+    count = ops.shape[0]
+    _check(lib().she_gate_level(ctx.handle, _dev_ptr(wires), _dev_ptr(ops), _dev_ptr(ins),
+                                _dev_ptr(out_idx), count, _stream_ptr(stream)))

@@ -1,0 +1,137 @@
+"""CPU tests of the product library's host side (no GPU needed).
+
+  * libshe.so loads and exports every function include/she.h declares;
+  * the product client (keygen / encrypt / decrypt, csrc/client.cpp) produces
+    byte-identical keys and ciphertexts to the oracle's independent client
+    (oracle/oracle.c) from the same seeds — so the GPU path and the oracle
+    consume identical inputs;
+  * the device arithmetic, compiled for the host (csrc/host_emu.cpp runs the
+    same __host__ __device__ step functions as the sm_100a kernel), is
+    bit-exact with the oracle's schoolbook: the negacyclic NTT product
+    (random and extreme inputs) and a whole blind rotation at C0 and C1.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import she_inputs as si
+from paper_1906_00148_b200 import build, she
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    build.build()
+
+
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "she.h")).read()
+    header = re.sub(r"/\*.*?\*/", "", header, flags=re.S)
+    names = sorted(set(re.findall(r"\b(she_[a-z0-9_]+)\s*\(", header)))
+    assert len(names) >= 20
+    lib = ctypes.CDLL(build.LIB)
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+@pytest.mark.parametrize("params", [si.C0, si.C1], ids=["C0", "C1"])
+def test_client_keys_match_oracle_bytes(params):
+    sk, ck = she.she_keygen(params, 4321)
+    K = oracle.keygen(params, 4321)
+    skb = np.frombuffer(sk.export(), dtype=np.uint8)
+    assert np.array_equal(skb[: params.n], K.s) and np.array_equal(skb[params.n:], K.S)
+    w = ck.export()
+    assert np.array_equal(w[: len(K.bk)], K.bk)
+    assert np.array_equal(w[len(K.bk):], K.ksk)
+    ck2 = she.CloudKey.import_(params, w)
+    assert np.array_equal(ck2.export(), w)
+
+
+@pytest.mark.parametrize("params", [si.C0, si.C1], ids=["C0", "C1"])
+def test_client_encrypt_decrypt_matches_oracle(params):
+    sk, _ = she.she_keygen(params, 99)
+    K = oracle.keygen(params, 99)
+    bits = np.random.default_rng(1).integers(0, 2, 500).astype(np.uint8)
+    c1 = she.she_encrypt_bits(sk, bits, seed=7, first_index=123)
+    c2 = oracle.encrypt(params, K.s, bits, 7, 123)
+    assert np.array_equal(c1, c2)
+    assert np.array_equal(she.she_decrypt_bits(sk, c1), bits)
+    assert np.array_equal(she.she_decrypt_bits(sk, c2), oracle.decrypt(params, K.s, c2))
+
+
+def test_bad_params_rejected():
+    from dataclasses import replace
+    for bad in (replace(si.C1, N=512), replace(si.C1, l=3), replace(si.C1, k=2),
+                replace(si.C1, ks_base_bits=3)):
+        with pytest.raises(she.SheError):
+            she.she_keygen(bad, 1)
+
+
+# ---- host emulation of the device arithmetic --------------------------------
+
+def emu():
+    L = ctypes.CDLL(build.build_emu())
+    L.she_emu_gl_mul.restype = ctypes.c_uint64
+    L.she_emu_gl_mul.argtypes = [ctypes.c_uint64] * 2
+    L.she_emu_gl_mul_pow2.restype = ctypes.c_uint64
+    L.she_emu_gl_mul_pow2.argtypes = [ctypes.c_uint64, ctypes.c_int]
+    for f in ("she_emu_gl_add", "she_emu_gl_sub"):
+        getattr(L, f).restype = ctypes.c_uint64
+        getattr(L, f).argtypes = [ctypes.c_uint64] * 2
+    return L
+
+
+P64 = 2 ** 64 - 2 ** 32 + 1
+
+
+def test_goldilocks_field_ops():
+    L = emu()
+    rng = np.random.default_rng(0)
+    edge = [0, 1, 2, P64 - 1, P64, P64 + 1, 2 ** 64 - 1, 2 ** 63, 2 ** 32 - 1, 2 ** 32]
+    vals = edge + [int(v) for v in rng.integers(0, 2 ** 63, 200, dtype=np.uint64) * 2 + 1]
+    for a in vals[:40]:
+        for b in vals[:40]:
+            assert L.she_emu_gl_mul(a, b) == a * b % P64
+            assert L.she_emu_gl_add(a, b) == (a + b) % P64
+            assert L.she_emu_gl_sub(a, b) == (a - b) % P64
+    for s in range(192):
+        for x in vals[:16]:
+            assert L.she_emu_gl_mul_pow2(x, s) == x * pow(2, s, P64) % P64, (s, x)
+
+
+@pytest.mark.parametrize("N", [256, 1024])
+def test_device_ntt_product_matches_schoolbook(N):
+    L = emu()
+    rng = np.random.default_rng(N)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    half = 512 if N == 1024 else 128
+    cases = [(rng.integers(-half, half, N), rng.integers(0, 2 ** 32, N, dtype=np.uint64))]
+    for dv in (-half, half - 1):
+        for bv in (0, 2 ** 31, 2 ** 32 - 1):
+            cases.append((np.full(N, dv), np.full(N, bv, dtype=np.uint64)))
+    for d, b in cases:
+        d = np.ascontiguousarray(d, dtype=np.int32)
+        b = np.ascontiguousarray(b.astype(np.uint32))
+        out = np.zeros(N, dtype=np.uint32)
+        assert L.she_emu_negacyclic_mul(N, d.ctypes.data_as(i32p), b.ctypes.data_as(u32p),
+                                        out.ctypes.data_as(u32p)) == 0
+        assert np.array_equal(out, oracle.negacyclic_mul(d, b))
+
+
+@pytest.mark.parametrize("params", [si.C0, si.C1], ids=["C0", "C1"])
+def test_device_blind_rotation_matches_oracle(params):
+    L = emu()
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    K = oracle.keygen(params, 1000)
+    ct = oracle.encrypt(params, K.s, [1], 5)[0]
+    acc = np.zeros(2 * params.N, dtype=np.uint32)
+    assert L.she_emu_blind_rotate(params.N, params.n, params.l, params.bg_bits,
+                                  K.bk.ctypes.data_as(u32p), ct.ctypes.data_as(u32p),
+                                  acc.ctypes.data_as(u32p)) == 0
+    assert np.array_equal(acc, oracle.blind_rotate(K, ct))
