@@ -158,29 +158,64 @@ she_status she_gate_level(she_ctx* ctx, uint32_t* wires, const uint8_t* ops,
                           void* stream);
 
 /* ---- layer calls (§3; scheduled by the library) ------------------ */
-/* Weight codes (host int8): 0 = zero weight; w = +-(e+1) means sign * 2^-e,
- * e in 0..7 (PAPER.md:118 weightQ; the term is sign * (x >> e), R12).
- * Encrypted words in/out are device slot arrays in the layouts given. */
+/* Each call builds the layer's gate circuit on the host from the PLAINTEXT
+ * weights (shifts = rewiring, negations = literal flags, constants folded),
+ * levelises it ASAP and runs one she_gate_level per level on the device.
+ *
+ * Weight codes (host int8): 0 = zero weight; w = +-(e+1) means sign * 2^-e,
+ * e in 0..7 (PAPER.md:118 weightQ); a term is sign * (x >> e) (R12).
+ * Words: [..][width][stride] device slot arrays, LSB first.  in_signed = 0:
+ * unsigned words of w_in value bits (e.g. 8-bit pixels, ReLU outputs; the
+ * constant-0 sign bit is implicit); in_signed = 1: two's complement words.
+ * Accumulators widen one bit per tree level up to acc_cap bits and wrap at
+ * the cap (R13).
+ * Output width: *w_out (in: capacity of `out` per word; out: width used).
+ * Call with out == NULL to query *w_out only (host only, no device work).
+ * relu != 0 fuses the sign-bit ReLU: outputs are UNSIGNED words of width w-1.
+ * Multi-GPU: a context with world > 1 computes only its rank's contiguous
+ * share of the output words (neurons [r*ceil(M/W), ...)); the caller
+ * all-gathers `out` across ranks. */
+typedef struct {
+  uint64_t gates, br_lanes, levels, max_level_width, min_level_width, tiles;
+} she_circuit_stats;
 
-/* conv (no bias) + shift-accumulate: in [H][W][C][w_in][stride], wq [Co][K][K][C],
- * out [Ho][Wo][Co][*w_out][stride]; accumulators widen 1 bit per tree level up
- * to acc_cap (16) bits, wrapping at the cap (R13).  relu != 0 applies the
- * sign-bit ReLU to the outputs (out width then excludes nothing: same w_out). */
+/* conv (no bias): in [H][W][C][w_in][stride], wq [Co][K][K][C],
+ * out [Ho][Wo][Co][*w_out][stride], Ho = (H + 2 pad - K)/stride + 1 ("same"
+ * zero padding when pad > 0, R14/R15). */
 she_status she_conv_shift_acc(she_ctx* ctx, const uint32_t* in, int H, int W, int C, int w_in,
-                              const int8_t* wq, int Co, int K, int stride, int pad, int acc_cap,
-                              int relu, uint32_t* out, int* w_out, void* stream);
-/* fully connected: in [K][w_in][stride], wq [M][K], out [M][*w_out][stride]. */
-she_status she_fc_shift_acc(she_ctx* ctx, const uint32_t* in, int K, int w_in, const int8_t* wq,
-                            int M, int acc_cap, int relu, uint32_t* out, int* w_out,
-                            void* stream);
-/* ReLU on `words` encrypted two's-complement words of `width` bits:
- * R_i = AND(X_i, NOT sign) (SPEC.md:193-201 reading of PAPER.md F2). */
+                              int in_signed, const int8_t* wq, int Co, int K, int stride, int pad,
+                              int acc_cap, int relu, uint32_t* out, int* w_out, void* stream);
+/* fully connected: in [K][w_in][stride] (HWC-flattened, R16), wq [M][K],
+ * out [M][*w_out][stride]. */
+she_status she_fc_shift_acc(she_ctx* ctx, const uint32_t* in, int K, int w_in, int in_signed,
+                            const int8_t* wq, int M, int acc_cap, int relu, uint32_t* out,
+                            int* w_out, void* stream);
+/* ReLU on `words` signed words of `width` bits: R_i = AND(X_i, NOT sign)
+ * (SPEC.md:193-201 reading of PAPER.md F2); out: words x (width-1) unsigned. */
 she_status she_relu(she_ctx* ctx, const uint32_t* in, size_t words, int width, uint32_t* out,
                     void* stream);
-/* 2x2 stride-2 max-pool on [H][W][C][w][stride] signed words: each max is a
- * subtract-comparator sign driving per-bit MUXes (PAPER.md F2). */
+/* 2x2 stride-2 max-pool on [H][W][C][w][stride]: max = subtract-comparator
+ * sign driving per-bit MUXes (PAPER.md F2); out [H/2][W/2][C][w][stride],
+ * same signedness as the input. */
 she_status she_maxpool2x2(she_ctx* ctx, const uint32_t* in, int H, int W, int C, int w,
-                          uint32_t* out, void* stream);
+                          int in_signed, uint32_t* out, void* stream);
+/* Gate / lane / level counters of the context's last layer call. */
+she_status she_ctx_layer_stats(she_ctx* ctx, she_circuit_stats* stats);
+
+/* Clear-bit backend: the same circuits evaluated on plaintext bits (uint8 per
+ * bit, layouts as above without the stride axis), host only.  For testing the
+ * scheduler and counting gates; stats may be NULL. */
+she_status she_clear_conv_shift_acc(const uint8_t* in, int H, int W, int C, int w_in,
+                                    int in_signed, const int8_t* wq, int Co, int K, int stride,
+                                    int pad, int acc_cap, int relu, uint8_t* out, int* w_out,
+                                    she_circuit_stats* stats);
+she_status she_clear_fc_shift_acc(const uint8_t* in, int K, int w_in, int in_signed,
+                                  const int8_t* wq, int M, int acc_cap, int relu, uint8_t* out,
+                                  int* w_out, she_circuit_stats* stats);
+she_status she_clear_relu(const uint8_t* in, size_t words, int width, uint8_t* out,
+                          she_circuit_stats* stats);
+she_status she_clear_maxpool2x2(const uint8_t* in, int H, int W, int C, int w, int in_signed,
+                                uint8_t* out, she_circuit_stats* stats);
 
 #ifdef __cplusplus
 }

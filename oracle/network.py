@@ -1,0 +1,124 @@
+"""Plaintext integer shift-accumulate network — TEST INFRASTRUCTURE ONLY (see
+oracle/__init__.py).  The decrypted outputs of the encrypted layers must equal
+these values exactly.
+
+Semantics (PAPER.md:118 log quantisation, :142 shifts, :147-149 accumulator;
+readings R11-R16 of SURVEY.md §8(c)):
+  * R11 pixels are unsigned 8-bit values (zero-extended, non-negative);
+  * R12 a weight code +-(e+1) contributes sign * floor(x / 2^e), i.e. the
+    shift happens before the sign (-(x >> e), not (-x) >> e); code 0 nothing;
+  * R13 neuron = the exact integer sum reduced to `cap`-bit two's complement
+    (wrap-around, not saturation);
+  * ReLU = max(v, 0); max-pool 2x2 stride 2 = max of the four;
+  * R14 valid convolution unless `pad` > 0 (zero padding, "same" for 3x3 pad 1);
+  * R16 flatten order HWC.
+Written as the definitions, with plain loops over the kernel window.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def wrap(v, cap: int):
+    """Reduce integers to cap-bit two's complement (R13)."""
+    v = np.asarray(v, dtype=np.int64)
+    m = 1 << cap
+    return ((v + (m >> 1)) % m) - (m >> 1)
+
+
+def wrap_events(v, cap: int) -> int:
+    v = np.asarray(v, dtype=np.int64)
+    return int(np.sum((v < -(1 << (cap - 1))) | (v >= (1 << (cap - 1)))))
+
+
+def term(x, code):
+    """sign * (x >> e) for code = +-(e+1); 0 for code 0 (R12)."""
+    x = np.asarray(x, dtype=np.int64)
+    code = np.asarray(code, dtype=np.int64)
+    e = np.abs(code) - 1
+    t = np.right_shift(x, np.maximum(e, 0))  # floor division by 2^e
+    return np.where(code == 0, 0, np.sign(code) * t)
+
+
+def conv_exact(x, wq, stride: int, pad: int):
+    """Exact (unwrapped) sums of a conv layer: x (H,W,C) ints, wq (Co,K,K,C) codes."""
+    x = np.asarray(x, dtype=np.int64)
+    H, W, C = x.shape
+    Co, K, _, _ = wq.shape
+    xp = np.zeros((H + 2 * pad, W + 2 * pad, C), dtype=np.int64)
+    xp[pad:pad + H, pad:pad + W] = x
+    Ho = (H + 2 * pad - K) // stride + 1
+    Wo = (W + 2 * pad - K) // stride + 1
+    out = np.zeros((Ho, Wo, Co), dtype=np.int64)
+    for kh in range(K):
+        for kw in range(K):
+            patch = xp[kh:kh + stride * (Ho - 1) + 1:stride, kw:kw + stride * (Wo - 1) + 1:stride]
+            # patch (Ho, Wo, C); weight codes (Co, C) for this tap
+            for co in range(Co):
+                out[:, :, co] += term(patch, wq[co, kh, kw][None, None, :]).sum(axis=-1)
+    return out
+
+
+def conv(x, wq, stride: int, pad: int, cap: int):
+    return wrap(conv_exact(x, wq, stride, pad), cap)
+
+
+def fc_exact(x, wq):
+    x = np.asarray(x, dtype=np.int64).ravel()
+    return term(x[None, :], wq).sum(axis=-1)
+
+
+def fc(x, wq, cap: int):
+    return wrap(fc_exact(x, wq), cap)
+
+
+def relu(v):
+    return np.maximum(np.asarray(v, dtype=np.int64), 0)
+
+
+def maxpool2x2(v):
+    v = np.asarray(v, dtype=np.int64)
+    H, W = v.shape[0] // 2 * 2, v.shape[1] // 2 * 2
+    v = v[:H, :W]
+    return np.maximum(np.maximum(v[0::2, 0::2], v[0::2, 1::2]),
+                      np.maximum(v[1::2, 0::2], v[1::2, 1::2]))
+
+
+def bits_of(v, width: int) -> np.ndarray:
+    """Two's-complement bits, LSB first: (..., width) uint8."""
+    v = np.asarray(v, dtype=np.int64)
+    return ((v[..., None] >> np.arange(width)) & 1).astype(np.uint8)
+
+
+def value_of(bits, signed: bool) -> np.ndarray:
+    bits = np.asarray(bits, dtype=np.int64)
+    w = bits.shape[-1]
+    v = (bits << np.arange(w)).sum(axis=-1)
+    if signed:
+        v = np.where(bits[..., -1] == 1, v - (1 << w), v)
+    return v
+
+
+# ---- the configs' networks (BASELINE.json configs 2-4) ----------------------
+
+def config2(px, w1, cap=16):
+    """conv 5x5 s2 1->5 (valid) + ReLU."""
+    return relu(conv(px, w1, 2, 0, cap))
+
+
+def config3(px, w1, w2, w3, cap=16):
+    """conv 5x5 s2 1->5 + ReLU; FC 720->100 + ReLU; FC 100->10 (logits)."""
+    h = config2(px, w1, cap)
+    h = relu(fc(h.ravel(), w2, cap))
+    return fc(h, w3, cap)
+
+
+def config4(px, w1, w2, w3, w4, cap=16):
+    """conv3x3 3->32 + ReLU, conv3x3 32->32 + ReLU, maxpool, conv3x3 32->64 + ReLU,
+    maxpool, FC 4096->10 ('same' padding for the 3x3 convs, R15)."""
+    h = relu(conv(px, w1, 1, 1, cap))
+    h = relu(conv(h, w2, 1, 1, cap))
+    h = maxpool2x2(h)
+    h = relu(conv(h, w3, 1, 1, cap))
+    h = maxpool2x2(h)
+    return fc(h.ravel(), w4, cap)

@@ -19,6 +19,7 @@
 
 #include "bootstrap_core.cuh"
 #include "common.h"
+#include "engine.h"
 #include "keys.h"
 
 using namespace she;
@@ -296,6 +297,25 @@ __global__ void __launch_bounds__(512) ks_kernel(KSArgs args) {
 
 constexpr int kKsG = 16, kKsCH = 64;
 
+// Slot gather: dst[dst_first + o] = +-src[lit_o & 0x7fffffff] (bit 31 negates
+// the n+1 live words; padding stays zero).  One CTA per slot.
+__global__ void gather_kernel(uint32_t* dst, size_t dst_first, const uint32_t* src,
+                              const uint32_t* lits, uint32_t stride, uint32_t n) {
+  const uint32_t lit = lits[blockIdx.x];
+  const uint32_t* s = src + (size_t)(lit & 0x7FFFFFFFu) * stride;
+  uint32_t* d = dst + (dst_first + blockIdx.x) * stride;
+  const bool neg = (lit >> 31) != 0;
+  for (uint32_t k = threadIdx.x; k < stride; k += blockDim.x) {
+    const uint32_t v = s[k];
+    d[k] = (neg && k <= n) ? 0u - v : v;
+  }
+}
+
+// Slot 0 of a wire table: the constant FALSE, trivial ciphertext (0, -1/8).
+__global__ void const_slot_kernel(uint32_t* table, uint32_t stride, uint32_t n) {
+  for (uint32_t k = threadIdx.x; k < stride; k += blockDim.x) table[k] = k == n ? 0u - kMu : 0u;
+}
+
 // K6: peak Goldilocks modmul throughput (roofline denominator).  Each thread
 // runs kChains independent chains of the same gl::mul the NTT uses.
 constexpr int kChains = 8;
@@ -339,6 +359,14 @@ struct she_ctx {
   size_t h_cap = 0;
   bool persist = false;
   std::mutex mu;
+  // wire table + program buffers of the layer scheduler
+  uint32_t* table = nullptr;
+  size_t table_slots = 0;
+  uint8_t* prog_dev = nullptr;
+  size_t prog_cap = 0;
+  uint8_t* prog_host = nullptr;  // pinned staging
+  size_t prog_host_cap = 0;
+  she_circuit_stats stats = {};
   // per-kernel CUDA-event timing (she_ctx_enable_timing / she_ctx_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -570,6 +598,9 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaFree(ctx->ext);
   cudaFree(ctx->h_ops);
   cudaFree(ctx->h_io);
+  cudaFree(ctx->table);
+  cudaFree(ctx->prog_dev);
+  cudaFreeHost(ctx->prog_host);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev_marks) cudaEventDestroy(e);
   delete ctx;
@@ -747,3 +778,87 @@ she_status she_gate_level(she_ctx* ctx, uint32_t* wires, const uint8_t* ops, con
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// scheduler -> engine
+// ---------------------------------------------------------------------------
+namespace she {
+
+int engine_rank(const she_ctx* ctx) { return ctx->rank; }
+int engine_world(const she_ctx* ctx) { return ctx->world; }
+
+she_circuit_stats* engine_stats(she_ctx* ctx, bool reset) {
+  if (reset) ctx->stats = she_circuit_stats{};
+  return &ctx->stats;
+}
+
+she_status engine_run_program(she_ctx* ctx, const sched::Program& p, const uint32_t* in,
+                              const std::vector<uint32_t>& input_bits, uint32_t* out,
+                              size_t out_first, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  const size_t G = p.ops.size(), I = input_bits.size(), O = p.out_lits.size();
+  // program image: [ins 3G u32][outs G u32][in lits I u32][out lits O u32][ops G u8]
+  const size_t bytes = (3 * G + G + I + O) * 4 + G;
+  if (ctx->prog_host_cap < bytes || ctx->prog_cap < bytes) {
+    CK(cudaStreamSynchronize(stream));
+    cudaFreeHost(ctx->prog_host);
+    cudaFree(ctx->prog_dev);
+    ctx->prog_host = nullptr;
+    ctx->prog_dev = nullptr;
+    ctx->prog_host_cap = ctx->prog_cap = 0;
+    const size_t cap = bytes + bytes / 4 + 4096;
+    CK(cudaMallocHost(&ctx->prog_host, cap));
+    CK(cudaMalloc(&ctx->prog_dev, cap));
+    ctx->prog_host_cap = ctx->prog_cap = cap;
+  } else {
+    CK(cudaStreamSynchronize(stream));  // the staging buffer may still be in flight
+  }
+  uint32_t* h32 = reinterpret_cast<uint32_t*>(ctx->prog_host);
+  memcpy(h32, p.ins.data(), 3 * G * 4);
+  memcpy(h32 + 3 * G, p.outs.data(), G * 4);
+  memcpy(h32 + 4 * G, input_bits.data(), I * 4);
+  memcpy(h32 + 4 * G + I, p.out_lits.data(), O * 4);
+  memcpy(ctx->prog_host + (4 * G + I + O) * 4, p.ops.data(), G);
+  CK(cudaMemcpyAsync(ctx->prog_dev, ctx->prog_host, bytes, cudaMemcpyHostToDevice, stream));
+  const uint32_t* d_ins = reinterpret_cast<const uint32_t*>(ctx->prog_dev);
+  const uint32_t* d_outs = d_ins + 3 * G;
+  const uint32_t* d_inl = d_ins + 4 * G;
+  const uint32_t* d_outl = d_inl + I;
+  const uint8_t* d_ops = ctx->prog_dev + (4 * G + I + O) * 4;
+
+  if (ctx->table_slots < p.num_slots) {
+    CK(cudaStreamSynchronize(stream));
+    cudaFree(ctx->table);
+    ctx->table = nullptr;
+    ctx->table_slots = 0;
+    const size_t want = p.num_slots + p.num_slots / 4 + 64;
+    CK(cudaMalloc(&ctx->table, want * ctx->stride * 4));
+    ctx->table_slots = want;
+  }
+  const uint32_t n = ctx->p.n;
+  const_slot_kernel<<<1, 256, 0, stream>>>(ctx->table, ctx->stride, n);
+  if (I) gather_kernel<<<(unsigned)I, 128, 0, stream>>>(ctx->table, 1, in, d_inl, ctx->stride, n);
+  CK(cudaGetLastError());
+  for (size_t lv = 1; lv + 1 < p.level_begin.size(); ++lv) {
+    const uint32_t b = p.level_begin[lv], e = p.level_begin[lv + 1];
+    if (e == b) continue;
+    GateSrc s = {};
+    s.ops = d_ops + b;
+    s.wires = ctx->table;
+    s.out_wires = ctx->table;
+    s.in_idx = d_ins + 3 * (size_t)b;
+    s.out_idx = d_outs + b;
+    s.stride = ctx->stride;
+    s.count = e - b;
+    she_status st = dispatch(ctx, s, stream);
+    if (st != SHE_OK) return st;
+  }
+  if (O) gather_kernel<<<(unsigned)O, 128, 0, stream>>>(out, out_first, ctx->table, d_outl,
+                                                        ctx->stride, n);
+  CK(cudaGetLastError());
+  return SHE_OK;
+}
+
+}  // namespace she

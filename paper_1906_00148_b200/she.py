@@ -41,6 +41,14 @@ class she_params(ctypes.Structure):
         return cls(p.N, p.k, p.n, p.bg_bits, p.l, p.ks_base_bits, p.ks_t, p.alpha_lwe, p.alpha_bk)
 
 
+class she_circuit_stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint64) for k in
+                ("gates", "br_lanes", "levels", "max_level_width", "min_level_width", "tiles")]
+
+    def as_dict(self) -> dict:
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
 _lib = None
 _vp = ctypes.c_void_p
 _sz = ctypes.c_size_t
@@ -79,6 +87,25 @@ def lib() -> ctypes.CDLL:
                                 ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
             "she_bench_modmul_peak": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+            "she_conv_shift_acc": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
+                                   + [_vp, ctypes.POINTER(ctypes.c_int), _vp], ctypes.c_int),
+            "she_fc_shift_acc": ([_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                  ctypes.POINTER(ctypes.c_int), _vp], ctypes.c_int),
+            "she_relu": ([_vp, _vp, _sz, ctypes.c_int, _vp, _vp], ctypes.c_int),
+            "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
+            "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
+            "she_clear_conv_shift_acc": ([_vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
+                                         + [_vp, ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
+            "she_clear_fc_shift_acc": ([_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                        ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
+            "she_clear_relu": ([_vp, _sz, ctypes.c_int, _vp, ctypes.POINTER(she_circuit_stats)],
+                               ctypes.c_int),
+            "she_clear_maxpool2x2": ([_vp] + [ctypes.c_int] * 5 + [_vp,
+                                     ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -250,6 +277,130 @@ def she_gate_batch_ops_host(ctx: Context, ops: np.ndarray, a: np.ndarray, b: np.
 
 
 def she_gate_level(ctx: Context, wires, ops, ins, out_idx, stream=None) -> None:
-    count = ops.shape[0]
+    """ops: uint8 codes (any dtype view of the bytes); ins: 3 x uint32 per gate;
+    out_idx: one uint32 slot index per gate (its length is the gate count)."""
+    count = out_idx.numel()
     _check(lib().she_gate_level(ctx.handle, _dev_ptr(wires), _dev_ptr(ops), _dev_ptr(ins),
                                 _dev_ptr(out_idx), count, _stream_ptr(stream)))
+
+
+# ---- layer calls (device) ------------------------------------------------------
+
+def _codes(wq) -> np.ndarray:
+    return np.ascontiguousarray(wq, dtype=np.int8)
+
+
+def conv_width(H, W, C, w_in, in_signed, wq, stride, pad, cap=16, relu=False) -> int:
+    wq = _codes(wq)
+    Co, K = wq.shape[0], wq.shape[1]
+    w = ctypes.c_int(0)
+    _check(lib().she_conv_shift_acc(None, None, H, W, C, w_in, int(in_signed), _np_ptr(wq), Co, K,
+                                    stride, pad, cap, int(relu), None, ctypes.byref(w), None))
+    return w.value
+
+
+def fc_width(K, w_in, in_signed, wq, cap=16, relu=False) -> int:
+    wq = _codes(wq)
+    w = ctypes.c_int(0)
+    _check(lib().she_fc_shift_acc(None, None, K, w_in, int(in_signed), _np_ptr(wq), wq.shape[0],
+                                  cap, int(relu), None, ctypes.byref(w), None))
+    return w.value
+
+
+def she_conv_shift_acc(ctx: Context, x, H, W, C, w_in, in_signed, wq, stride, pad, cap=16,
+                       relu=False, out=None, stream=None):
+    """x: device slots [H][W][C][w_in][stride]; returns (out [Ho][Wo][Co][w][stride], w)."""
+    import torch
+    wq = _codes(wq)
+    Co, K = wq.shape[0], wq.shape[1]
+    Ho, Wo = (H + 2 * pad - K) // stride + 1, (W + 2 * pad - K) // stride + 1
+    w = ctypes.c_int(conv_width(H, W, C, w_in, in_signed, wq, stride, pad, cap, relu))
+    if out is None:
+        out = torch.zeros((Ho, Wo, Co, w.value, ctx.stride), dtype=torch.int32, device=x.device)
+    _check(lib().she_conv_shift_acc(ctx.handle, _dev_ptr(x), H, W, C, w_in, int(in_signed),
+                                    _np_ptr(wq), Co, K, stride, pad, cap, int(relu), _dev_ptr(out),
+                                    ctypes.byref(w), _stream_ptr(stream)))
+    return out, w.value
+
+
+def she_fc_shift_acc(ctx: Context, x, K, w_in, in_signed, wq, cap=16, relu=False, out=None,
+                     stream=None):
+    import torch
+    wq = _codes(wq)
+    M = wq.shape[0]
+    w = ctypes.c_int(fc_width(K, w_in, in_signed, wq, cap, relu))
+    if out is None:
+        out = torch.zeros((M, w.value, ctx.stride), dtype=torch.int32, device=x.device)
+    _check(lib().she_fc_shift_acc(ctx.handle, _dev_ptr(x), K, w_in, int(in_signed), _np_ptr(wq), M,
+                                  cap, int(relu), _dev_ptr(out), ctypes.byref(w),
+                                  _stream_ptr(stream)))
+    return out, w.value
+
+
+def she_relu(ctx: Context, x, words, width, out=None, stream=None):
+    import torch
+    if out is None:
+        out = torch.zeros((words, width - 1, ctx.stride), dtype=torch.int32, device=x.device)
+    _check(lib().she_relu(ctx.handle, _dev_ptr(x), words, width, _dev_ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def she_maxpool2x2(ctx: Context, x, H, W, C, w, in_signed, out=None, stream=None):
+    import torch
+    if out is None:
+        out = torch.zeros((H // 2, W // 2, C, w, ctx.stride), dtype=torch.int32, device=x.device)
+    _check(lib().she_maxpool2x2(ctx.handle, _dev_ptr(x), H, W, C, w, int(in_signed), _dev_ptr(out),
+                                _stream_ptr(stream)))
+    return out
+
+
+def layer_stats(ctx: Context) -> dict:
+    st = she_circuit_stats()
+    _check(lib().she_ctx_layer_stats(ctx.handle, ctypes.byref(st)))
+    return st.as_dict()
+
+
+# ---- clear-bit backend (host bits; scheduler tests and gate counts) -------------
+
+def clear_conv_shift_acc(bits, H, W, C, w_in, in_signed, wq, stride, pad, cap=16, relu=False):
+    """bits: uint8 [H][W][C][w_in]; returns (bits [Ho][Wo][Co][w], w, stats)."""
+    wq = _codes(wq)
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    Co, K = wq.shape[0], wq.shape[1]
+    Ho, Wo = (H + 2 * pad - K) // stride + 1, (W + 2 * pad - K) // stride + 1
+    w = ctypes.c_int(conv_width(H, W, C, w_in, in_signed, wq, stride, pad, cap, relu))
+    out = np.zeros((Ho, Wo, Co, w.value), dtype=np.uint8)
+    st = she_circuit_stats()
+    _check(lib().she_clear_conv_shift_acc(_np_ptr(bits), H, W, C, w_in, int(in_signed), _np_ptr(wq),
+                                          Co, K, stride, pad, cap, int(relu), _np_ptr(out),
+                                          ctypes.byref(w), ctypes.byref(st)))
+    return out, w.value, st.as_dict()
+
+
+def clear_fc_shift_acc(bits, K, w_in, in_signed, wq, cap=16, relu=False):
+    wq = _codes(wq)
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    M = wq.shape[0]
+    w = ctypes.c_int(fc_width(K, w_in, in_signed, wq, cap, relu))
+    out = np.zeros((M, w.value), dtype=np.uint8)
+    st = she_circuit_stats()
+    _check(lib().she_clear_fc_shift_acc(_np_ptr(bits), K, w_in, int(in_signed), _np_ptr(wq), M, cap,
+                                        int(relu), _np_ptr(out), ctypes.byref(w), ctypes.byref(st)))
+    return out, w.value, st.as_dict()
+
+
+def clear_relu(bits, words, width):
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    out = np.zeros((words, width - 1), dtype=np.uint8)
+    st = she_circuit_stats()
+    _check(lib().she_clear_relu(_np_ptr(bits), words, width, _np_ptr(out), ctypes.byref(st)))
+    return out, st.as_dict()
+
+
+def clear_maxpool2x2(bits, H, W, C, w, in_signed):
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    out = np.zeros((H // 2, W // 2, C, w), dtype=np.uint8)
+    st = she_circuit_stats()
+    _check(lib().she_clear_maxpool2x2(_np_ptr(bits), H, W, C, w, int(in_signed), _np_ptr(out),
+                                      ctypes.byref(st)))
+    return out, st.as_dict()
