@@ -1,20 +1,26 @@
 // bootstrap_core.cuh — the per-thread steps of one CMux iteration of the blind
 // rotation, written as __host__ __device__ functions of
-// (warp, lane, shared-memory pointers, registers).  The sm_100a kernel
-// (bootstrap.cu) calls them between __syncwarp/__syncthreads; the host
-// emulation (host_emu.cpp, tests only) calls them in loops over threads, so
-// the exact device arithmetic is checked against the oracle on the CPU too.
+// (lane index, shared-memory pointers, registers).  The sm_100a kernel
+// (engine.cu) calls them between barriers; the host emulation (host_emu.cpp,
+// tests only) calls them in loops over threads, so the exact device
+// arithmetic is checked against the oracle on the CPU as well.
 //
-// One blind-rotation lane (one bootstrapped LWE sample) is one CTA of 4 warps.
-// Warp w owns row r = w of the gadget decomposition, r = c*l + j (c = 0 for
-// the accumulator's A polynomial, 1 for B; j = digit level) — DESIGN.md R2.
+// One blind-rotation lane (one bootstrapped LWE sample) is served by 4 warps:
+//   forward   warp w computes row r = w of the gadget decomposition (r = c*l+j,
+//             c = 0 for the accumulator's A polynomial, 1 for B; R2)
+//             and its full forward NTT (32 threads x 32 registers);
+//   pointwise all threads of the CTA, BK_i read once per CTA for all lanes;
+//   inverse   warps (2c, 2c+1) split the inverse NTT of output component c:
+//             thread (H, lane) holds half of a 32-point column, the last
+//             butterfly stage exchanges L/4 values through shared memory.
 //
 // Shared memory of one lane:
-//   acc  : uint32[2][N]           the TRLWE accumulator (A, B), torus32
-//   buf  : uint64[4][L][L+1]      per-row NTT scratch; storage order q*L + i
-//                                  in the first N words, transposed pass-1
-//                                  output at i*(L+1) + j1 (padded: no bank
-//                                  conflicts for the column reads)
+//   acc  : uint32[2][N]          the TRLWE accumulator (A, B), torus32
+//   buf  : uint64[4][L][L+1]     per-row NTT storage (order q*L + i in the first
+//                                N words) / transposition scratch (i*(L+1) + j1,
+//                                padded: conflict-free column access); rows 2, 3
+//                                double as the inverse's exchange buffers
+//   abar : uint16[n+1]           modulus-switched input sample
 #pragma once
 #include "ntt.cuh"
 
@@ -24,8 +30,8 @@ constexpr uint32_t MU = 1u << 29;  // 1/8
 
 struct Geometry {
   uint32_t N, n, l, bg_bits;
-  uint32_t lg2N;       // log2(2N)
-  uint32_t dec_offset; // sum_j (Bg/2) 2^{32-j bg} + 2^{32-l bg-1}   (R8)
+  uint32_t lg2N;        // log2(2N)
+  uint32_t dec_offset;  // sum_j (Bg/2) 2^{32-j bg} + 2^{32-l bg-1}   (R8)
 };
 
 __host__ __device__ inline uint32_t modswitch(uint32_t x, uint32_t lg2N) {
@@ -33,9 +39,21 @@ __host__ __device__ inline uint32_t modswitch(uint32_t x, uint32_t lg2N) {
 }
 
 template <class S>
-__host__ __device__ __forceinline__ uint64_t* buf_row(uint64_t* buf, int w) {
-  return buf + (size_t)w * S::L * (S::L + 1);
-}
+struct Lane {
+  static constexpr int L = S::L, N = S::N;
+  static constexpr int RS = L * (L + 1);  // words per buf row
+  static constexpr size_t bytes(uint32_t n) {
+    return (size_t)2 * N * 4 + (size_t)4 * RS * 8 + ((n + 1) * 2 + 15) / 16 * 16;
+  }
+  uint32_t* acc;
+  uint64_t* buf;
+  uint16_t* abar;
+  __host__ __device__ explicit Lane(uint8_t* base)
+      : acc(reinterpret_cast<uint32_t*>(base)),
+        buf(reinterpret_cast<uint64_t*>(base + 2 * N * 4)),
+        abar(reinterpret_cast<uint16_t*>(base + 2 * N * 4 + 4 * RS * 8)) {}
+  __host__ __device__ uint64_t* row(int r) const { return buf + (size_t)r * RS; }
+};
 
 // ---- forward path of row w ------------------------------------------------
 
@@ -61,12 +79,12 @@ __host__ __device__ __forceinline__ void load_digits(const Geometry& g, int w, i
   }
 }
 
-// Pass 1 + transposed store: x (coefficients j2 of column j1=lane) -> scratch.
+// Pass 1 (negacyclic, shift twiddles) + transposed store.
 template <class S>
 __host__ __device__ __forceinline__ void fwd_pass1_store(int lane, uint64_t (&x)[S::L],
                                                          uint64_t* row) {
   constexpr int L = S::L;
-  ntt::nega_fwd<L, S::SH>(x);
+  ntt::fwd<L, S::SH, true>(x);
 #pragma unroll
   for (int q = 0; q < L; ++q) row[ntt::brev(q, ntt::ilog2(L)) * (L + 1) + lane] = x[q];
 }
@@ -81,75 +99,109 @@ __host__ __device__ __forceinline__ void fwd_pass2_load(int i, const uint64_t* r
   for (int j1 = 1; j1 < L; ++j1) y[j1] = gl::mul(row[i * (L + 1) + j1], tw[j1 * L + i]);
 }
 
-// Pass 2 + store in NTT storage order (position q*L + i).
+// Pass 2 (cyclic, shift twiddles) + store in NTT storage order (q*L + i).
 template <class S>
 __host__ __device__ __forceinline__ void fwd_pass2_store(int i, uint64_t (&y)[S::L], uint64_t* row) {
   constexpr int L = S::L;
-  ntt::cyc_fwd<L, S::SH2>(y);
+  ntt::fwd<L, S::SH2, false>(y);
 #pragma unroll
   for (int q = 0; q < L; ++q) row[q * L + i] = y[q];
 }
 
-// ---- pointwise multiply-accumulate with BK_i --------------------------------
-// out_c[p] = sum_r D_r[p] * BK_i[r][c][p] for p = t, t + T, ...; results go to
-// rows 0 (c = A) and 1 (c = B) of buf.  bki: uint64[2l][2][N] storage order.
+// ---- pointwise multiply-accumulate with BK_i (lazy: one reduction per output)
+// out_c[p] = sum_r D_r[p] * BK_i[r][c][p]; b[r*2 + c] = BK_i[r][c][p].
 template <class S>
-__host__ __device__ __forceinline__ void pointwise(int t, int T, int rows, uint64_t* buf,
-                                                   const uint64_t* bki) {
-  constexpr int L = S::L, N = S::N;
-  constexpr int RS = L * (L + 1);
-  for (int p = t; p < N; p += T) {
-    uint64_t d[4];
+__host__ __device__ __forceinline__ void pointwise_pos(uint64_t* buf, int p, const uint64_t (&b)[8]) {
+  constexpr int RS = Lane<S>::RS;
+  uint64_t d[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) d[r] = r < rows ? buf[r * RS + p] : 0;
-    uint64_t oa = 0, ob = 0;
+  for (int r = 0; r < 4; ++r) d[r] = buf[r * RS + p];
+  gl::Acc3 oa, ob;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (r < rows) {
-        oa = gl::add(oa, gl::mul(d[r], bki[(size_t)(r * 2 + 0) * N + p]));
-        ob = gl::add(ob, gl::mul(d[r], bki[(size_t)(r * 2 + 1) * N + p]));
-      }
+  for (int r = 0; r < 4; ++r) {
+    gl::mac(oa, d[r], b[2 * r + 0]);
+    gl::mac(ob, d[r], b[2 * r + 1]);
+  }
+  buf[0 * RS + p] = gl::reduce_acc(oa);
+  buf[1 * RS + p] = gl::reduce_acc(ob);
+}
+
+// ---- inverse path: output component c, thread (H, lane) ----------------------
+// Exchange buffer: row 2 + c of buf, xbuf[(H*L/4 + m)*L + lane].
+
+template <class S, int H>
+__host__ __device__ __forceinline__ void inv_a_load(int i, const uint64_t* row, uint64_t (&y)[S::L / 2]) {
+  constexpr int L = S::L;
+#pragma unroll
+  for (int m = 0; m < L / 2; ++m) y[m] = row[(H * (L / 2) + m) * L + i];
+}
+
+template <class S, int H, bool NEGA>
+__host__ __device__ __forceinline__ void inv_stages_send(int lane, uint64_t (&y)[S::L / 2], uint64_t* xbuf) {
+  constexpr int L = S::L;
+  ntt::inv_half<L, (NEGA ? S::SH : S::SH2), NEGA, H>(y);
+  // H = 0 sends its lo values for j in [L/4, L/2); H = 1 its hi values for j < L/4
+#pragma unroll
+  for (int m = 0; m < L / 4; ++m) xbuf[(H * (L / 4) + m) * L + lane] = y[(H == 0 ? L / 4 : 0) + m];
+}
+
+template <class S, int H, bool NEGA>
+__host__ __device__ __forceinline__ void inv_recv_cross(int lane, const uint64_t (&y)[S::L / 2],
+                                                        const uint64_t* xbuf, uint64_t (&lo)[S::L / 4],
+                                                        uint64_t (&hi)[S::L / 4]) {
+  constexpr int L = S::L;
+  const int P = 1 - H;  // partner
+#pragma unroll
+  for (int m = 0; m < L / 4; ++m) {
+    const uint64_t other = xbuf[(P * (L / 4) + m) * L + lane];
+    if (H == 0) {
+      lo[m] = y[m];
+      hi[m] = other;
+    } else {
+      lo[m] = other;
+      hi[m] = y[L / 4 + m];
     }
-    buf[0 * RS + p] = oa;
-    buf[1 * RS + p] = ob;
+  }
+  ntt::inv_cross<L, (NEGA ? S::SH : S::SH2), NEGA>(lo, hi);
+}
+
+// After pass A: untwist and store transposed (thread row i; outputs j1 =
+// H*L/4 + m and H*L/4 + m + L/2).
+template <class S, int H>
+__host__ __device__ __forceinline__ void inv_a_store(int i, const uint64_t (&lo)[S::L / 4],
+                                                     const uint64_t (&hi)[S::L / 4],
+                                                     const uint64_t* itw, uint64_t* row) {
+  constexpr int L = S::L;
+#pragma unroll
+  for (int m = 0; m < L / 4; ++m) {
+    const int j1 = H * (L / 4) + m, j1h = j1 + L / 2;
+    row[i * (L + 1) + j1] = j1 == 0 ? lo[m] : gl::mul(lo[m], itw[j1 * L + i]);
+    row[i * (L + 1) + j1h] = gl::mul(hi[m], itw[j1h * L + i]);
   }
 }
 
-// ---- inverse path of output component c = w ---------------------------------
-
-template <class S>
-__host__ __device__ __forceinline__ void inv_pass2_load(int i, const uint64_t* row,
-                                                        uint64_t (&y)[S::L]) {
+// Pass B load: column j1 = lane in the nega_fwd output order (register q <-> row brev(q)).
+template <class S, int H>
+__host__ __device__ __forceinline__ void inv_b_load(int j1, const uint64_t* row, uint64_t (&y)[S::L / 2]) {
   constexpr int L = S::L;
 #pragma unroll
-  for (int q = 0; q < L; ++q) y[q] = row[q * L + i];
+  for (int m = 0; m < L / 2; ++m) y[m] = row[ntt::brev(H * (L / 2) + m, ntt::ilog2(L)) * (L + 1) + j1];
 }
 
-template <class S>
-__host__ __device__ __forceinline__ void inv_pass2_store(int i, uint64_t (&y)[S::L],
-                                                         const uint64_t* itw, uint64_t* row) {
+// After pass B: lift mod 2^32 and ACC_c += result (coefficients j1 + L j2).
+template <class S, int H>
+__host__ __device__ __forceinline__ void inv_b_acc(int j1, const uint64_t (&lo)[S::L / 4],
+                                                   const uint64_t (&hi)[S::L / 4], uint32_t* accc) {
   constexpr int L = S::L;
-  ntt::cyc_inv<L, S::SH2>(y);
-  row[i * (L + 1)] = y[0];
 #pragma unroll
-  for (int j1 = 1; j1 < L; ++j1) row[i * (L + 1) + j1] = gl::mul(y[j1], itw[j1 * L + i]);
-}
-
-// Pass 1 inverse for column j1 = lane, then lift mod 2^32 and ACC_c += result.
-template <class S>
-__host__ __device__ __forceinline__ void inv_pass1_acc(int lane, const uint64_t* row,
-                                                       uint32_t* accc) {
-  constexpr int L = S::L;
-  uint64_t x[L];
-#pragma unroll
-  for (int q = 0; q < L; ++q) x[q] = row[ntt::brev(q, ntt::ilog2(L)) * (L + 1) + lane];
-  ntt::nega_inv<L, S::SH>(x);
-#pragma unroll
-  for (int j2 = 0; j2 < L; ++j2) accc[lane + L * j2] += gl::lift32(x[j2]);
+  for (int m = 0; m < L / 4; ++m) {
+    const int j2 = H * (L / 4) + m;
+    accc[j1 + L * j2] += gl::lift32(lo[m]);
+    accc[j1 + L * (j2 + L / 2)] += gl::lift32(hi[m]);
+  }
 }
 
 // ---- BK transform (setup, K1) ----------------------------------------------
-// Load column j1 = lane of a torus32 polynomial with the signed lift.
 template <class S>
 __host__ __device__ __forceinline__ void load_poly_signed(int lane, const uint32_t* poly,
                                                           uint64_t (&x)[S::L]) {
@@ -158,21 +210,19 @@ __host__ __device__ __forceinline__ void load_poly_signed(int lane, const uint32
   for (int j2 = 0; j2 < L; ++j2) x[j2] = gl::from_i64((int32_t)poly[lane + L * j2]);
 }
 
-// Pass 2 + N^-1 scaling + store to a global NTT-domain polynomial.
 template <class S>
 __host__ __device__ __forceinline__ void fwd_pass2_store_scaled(int i, uint64_t (&y)[S::L],
                                                                 uint64_t ninv, uint64_t* out) {
   constexpr int L = S::L;
-  ntt::cyc_fwd<L, S::SH2>(y);
+  ntt::fwd<L, S::SH2, false>(y);
 #pragma unroll
   for (int q = 0; q < L; ++q) out[q * L + i] = gl::canon(gl::mul(y[q], ninv));
 }
 
-// ---- test vector and sample extraction ---------------------------------------
-// ACC = (0, X^{-bbar} v), v = mu sum_j X^j: coefficient m of X^{-bbar} v is
-// +mu if m + bbar lands in [0, N) of the 2N cycle, -mu otherwise.
+// ---- test vector ---------------------------------------------------------------
+// ACC = (0, X^{-bbar} v), v = mu sum_j X^j: coefficient m collects j = m + bbar
+// (mod 2N); +mu if that j is in [0, N), -mu otherwise.
 __host__ __device__ inline uint32_t testvec_coeff(uint32_t m, uint32_t bbar, uint32_t N) {
-  // X^{-bbar} X^j = X^{j - bbar}; coefficient m collects j = m + bbar (mod 2N)
   const uint32_t j = (m + bbar) & (2 * N - 1);
   return j < N ? MU : 0u - MU;
 }

@@ -26,8 +26,6 @@ using namespace she;
 
 namespace {
 
-constexpr int kWarps = 4;            // 2l rows (l = 2)
-constexpr int kBRThreads = 32 * kWarps;
 constexpr uint32_t kMu = 1u << 29;
 
 // ---------------------------------------------------------------------------
@@ -88,103 +86,194 @@ __device__ __forceinline__ LaneForm lane_form(int op, int h) {
 
 struct BRArgs {
   GateSrc src;
-  uint32_t lane_base;        // first lane of this launch (lane = 2 g + h)
+  const uint32_t* lanes;     // compact lane list: gate | h << 31
+  const uint32_t* nlanes;    // device: number of lanes
   const uint64_t* bk;        // [n][2l][2][N] NTT storage order
   const uint64_t* tw;        // [L][L]
   const uint64_t* itw;       // [L][L]
-  uint32_t* ext;             // [lanes][ext_stride] extracted samples (N+1 words)
+  uint32_t* ext;             // [2 count][ext_stride] extracted samples (N+1 words)
   uint32_t ext_stride;
   br::Geometry geo;
 };
 
-template <class S>
-constexpr size_t br_smem_bytes(uint32_t n) {
-  return (size_t)2 * S::N * 4 + (size_t)kWarps * S::L * (S::L + 1) * 8 + ((n + 1) * 2 + 15) / 16 * 16;
+__device__ __forceinline__ void pair_sync(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 
-// K2 + K3: gate prologue, blind rotation, sample extraction for one lane.
-template <class S>
-__global__ void __launch_bounds__(kBRThreads) br_kernel(BRArgs args) {
+// K2 + K3: gate prologue, blind rotation, sample extraction.  A persistent CTA
+// serves G lanes at a time in lock step (all 4G warps run the same phase, so
+// they share the instruction stream and each BK_i load); warp roles per lane
+// as described in bootstrap_core.cuh.  No iteration is skipped (a~_i = 0
+// gives digits 0 and an exactly-zero update, R9), so all lanes stay in step.
+template <class S, int G>
+__global__ void __launch_bounds__(128 * G, 1) br_kernel(BRArgs args) {
   constexpr int N = S::N, L = S::L;
+  constexpr int T = 128 * G;
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* acc = reinterpret_cast<uint32_t*>(smem);
-  uint64_t* buf = reinterpret_cast<uint64_t*>(smem + 2 * N * 4);
-  uint16_t* abar = reinterpret_cast<uint16_t*>(buf + kWarps * L * (L + 1));
-
   const GateSrc& src = args.src;
   const br::Geometry& geo = args.geo;
-  const uint32_t lane_id = args.lane_base + blockIdx.x;
-  const uint32_t g = lane_id >> 1, h = lane_id & 1;
-  if (g >= src.count) return;
-  const LaneForm f = lane_form(gate_op(src, g), (int)h);
-  if (!f.valid) return;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t n = geo.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp >> 2, w = warp & 3, lt = tid & 127;  // lane slot, role, thread in slot
+  const size_t lane_bytes = br::Lane<S>::bytes(n);
+  br::Lane<S> me(smem + (size_t)g * lane_bytes);
+  const uint32_t total = *args.nlanes;
+  const bool active_lane = lane < L;
 
-  // K2: gate linear form and modulus switch to Z_2N (R7).
-  {
-    bool n0, n1;
-    const uint32_t* x0 = gate_in(src, g, 0, n0);
-    const uint32_t* x1 = gate_in(src, g, f.j1, n1);
-    const uint32_t k0 = (uint32_t)(n0 ? -f.k0 : f.k0), k1 = (uint32_t)(n1 ? -f.k1 : f.k1);
-    for (uint32_t k = tid; k <= n; k += kBRThreads) {
-      uint32_t v = k0 * x0[k] + k1 * x1[k];
-      if (k == n) v += f.kappa;
-      abar[k] = (uint16_t)br::modswitch(v, geo.lg2N);
-    }
-  }
-  __syncthreads();
-  // ACC = (0, X^{-bbar} v)
-  {
-    const uint32_t bbar = abar[n];
-    for (int m = tid; m < N; m += kBRThreads) {
-      acc[m] = 0;
-      acc[N + m] = br::testvec_coeff(m, bbar, N);
-    }
-  }
-  __syncthreads();
-
-  uint64_t* row = br::buf_row<S>(buf, warp);
-  const bool active = lane < L;
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint32_t a = abar[i];
-    if (a == 0) continue;  // R9 (uniform across the CTA)
-    // forward: decompose row `warp`, pass 1, transpose, twist, pass 2
-    {
-      uint64_t x[L];
-      if (active) {
-        br::load_digits<S>(geo, warp, lane, acc, a, x);
-        br::fwd_pass1_store<S>(lane, x, row);
+  for (uint32_t base = blockIdx.x * G; base < total; base += gridDim.x * G) {
+    const uint32_t L_id = base + g;
+    const bool on = L_id < total;
+    uint32_t gate = 0, h = 0;
+    if (on) {
+      const uint32_t e = args.lanes[L_id];
+      gate = e & 0x7FFFFFFFu;
+      h = e >> 31;
+      // K2: gate linear form and modulus switch to Z_2N (R7)
+      const LaneForm f = lane_form(gate_op(src, gate), (int)h);
+      bool n0, n1;
+      const uint32_t* x0 = gate_in(src, gate, 0, n0);
+      const uint32_t* x1 = gate_in(src, gate, f.j1, n1);
+      const uint32_t k0 = (uint32_t)(n0 ? -f.k0 : f.k0), k1 = (uint32_t)(n1 ? -f.k1 : f.k1);
+      for (uint32_t k = lt; k <= n; k += 128) {
+        uint32_t v = k0 * x0[k] + k1 * x1[k];
+        if (k == n) v += f.kappa;
+        me.abar[k] = (uint16_t)br::modswitch(v, geo.lg2N);
       }
-      __syncwarp();
-      if (active) br::fwd_pass2_load<S>(lane, row, args.tw, x);
-      __syncwarp();
-      if (active) br::fwd_pass2_store<S>(lane, x, row);
     }
     __syncthreads();
-    br::pointwise<S>(tid, kBRThreads, kWarps, buf, args.bk + (size_t)i * kWarps * 2 * N);
-    __syncthreads();
-    if (warp < 2) {  // inverse of output component c = warp, ACC_c += result
-      uint64_t y[L];
-      if (active) br::inv_pass2_load<S>(lane, row, y);
-      __syncwarp();
-      if (active) br::inv_pass2_store<S>(lane, y, args.itw, row);
-      __syncwarp();
-      if (active) br::inv_pass1_acc<S>(lane, row, acc + warp * N);
+    if (on) {  // ACC = (0, X^{-bbar} v)
+      const uint32_t bbar = me.abar[n];
+      for (int m = lt; m < N; m += 128) {
+        me.acc[m] = 0;
+        me.acc[N + m] = br::testvec_coeff(m, bbar, N);
+      }
     }
     __syncthreads();
-  }
 
-  // sample extract: a'_0 = A_0, a'_j = -A_{N-j}, b' = B_0
-  uint32_t* e = args.ext + (size_t)lane_id * args.ext_stride;
-  for (int m = tid; m <= N; m += kBRThreads) {
-    uint32_t v;
-    if (m == 0) v = acc[0];
-    else if (m < N) v = 0u - acc[N - m];
-    else v = acc[N];
-    e[m] = v;
+    for (uint32_t i = 0; i < n; ++i) {
+      // ---- forward: row w of lane g ----
+      if (on) {
+        uint64_t* row = me.row(w);
+        uint64_t x[L];
+        if (active_lane) {
+          br::load_digits<S>(geo, w, lane, me.acc, me.abar[i], x);
+          br::fwd_pass1_store<S>(lane, x, row);
+        }
+        __syncwarp();
+        if (active_lane) br::fwd_pass2_load<S>(lane, row, args.tw, x);
+        __syncwarp();
+        if (active_lane) br::fwd_pass2_store<S>(lane, x, row);
+      }
+      __syncthreads();
+      // ---- pointwise: BK_i read once per CTA for all G lanes ----
+      {
+        const uint64_t* bki = args.bk + (size_t)i * 8 * N;
+        for (int p = tid; p < N; p += T) {
+          uint64_t b[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) b[q] = __ldg(bki + (size_t)q * N + p);
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg)
+            if (base + gg < total) {
+              br::Lane<S> other(smem + (size_t)gg * lane_bytes);
+              br::pointwise_pos<S>(other.buf, p, b);
+            }
+        }
+      }
+      __syncthreads();
+      // ---- inverse of component c = w >> 1 by warps (2c, 2c+1) ----
+      if (on) {
+        const int c = w >> 1, H = w & 1;
+        const int bar = 1 + 2 * g + c;
+        uint64_t* row = me.row(c);
+        uint64_t* xb = me.row(2 + c);
+        uint64_t y[L / 2], lo[L / 4], hi[L / 4];
+        if (H == 0) {
+          if (active_lane) {
+            br::inv_a_load<S, 0>(lane, row, y);
+            br::inv_stages_send<S, 0, false>(lane, y, xb);
+          }
+          pair_sync(bar);
+          if (active_lane) {
+            br::inv_recv_cross<S, 0, false>(lane, y, xb, lo, hi);
+            br::inv_a_store<S, 0>(lane, lo, hi, args.itw, row);
+          }
+          pair_sync(bar);
+          if (active_lane) {
+            br::inv_b_load<S, 0>(lane, row, y);
+            br::inv_stages_send<S, 0, true>(lane, y, xb);
+          }
+          pair_sync(bar);
+          if (active_lane) {
+            br::inv_recv_cross<S, 0, true>(lane, y, xb, lo, hi);
+            br::inv_b_acc<S, 0>(lane, lo, hi, me.acc + c * N);
+          }
+        } else {
+          if (active_lane) {
+            br::inv_a_load<S, 1>(lane, row, y);
+            br::inv_stages_send<S, 1, false>(lane, y, xb);
+          }
+          pair_sync(bar);
+          if (active_lane) {
+            br::inv_recv_cross<S, 1, false>(lane, y, xb, lo, hi);
+            br::inv_a_store<S, 1>(lane, lo, hi, args.itw, row);
+          }
+          pair_sync(bar);
+          if (active_lane) {
+            br::inv_b_load<S, 1>(lane, row, y);
+            br::inv_stages_send<S, 1, true>(lane, y, xb);
+          }
+          pair_sync(bar);
+          if (active_lane) {
+            br::inv_recv_cross<S, 1, true>(lane, y, xb, lo, hi);
+            br::inv_b_acc<S, 1>(lane, lo, hi, me.acc + c * N);
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    // sample extract: a'_0 = A_0, a'_j = -A_{N-j}, b' = B_0
+    if (on) {
+      uint32_t* e = args.ext + (size_t)(2 * gate + h) * args.ext_stride;
+      for (int m = lt; m <= N; m += 128) {
+        uint32_t v;
+        if (m == 0) v = me.acc[0];
+        else if (m < N) v = 0u - me.acc[N - m];
+        else v = me.acc[N];
+        e[m] = v;
+      }
+    }
+    __syncthreads();
   }
+}
+
+// Compact lane list of a gate batch: gate g contributes lane (g, 0) if it is
+// bootstrapped and (g, 1) too if it is a MUX.  One CTA, block-wide scan.
+__global__ void lane_list_kernel(GateSrc src, uint32_t* lanes, uint32_t* nlanes) {
+  __shared__ uint32_t part[1024];
+  const uint32_t tid = threadIdx.x, T = blockDim.x, count = src.count;
+  const uint32_t per = (count + T - 1) / T, g0 = tid * per, g1 = min(count, g0 + per);
+  uint32_t cnt = 0;
+  for (uint32_t g = g0; g < g1; ++g) {
+    const int op = gate_op(src, g);
+    cnt += op == SHE_MUX ? 2 : (op >= 0 && op < SHE_NOT ? 1 : 0);
+  }
+  part[tid] = cnt;
+  __syncthreads();
+  for (uint32_t off = 1; off < T; off <<= 1) {  // inclusive Hillis-Steele scan
+    const uint32_t v = tid >= off ? part[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  uint32_t pos = part[tid] - cnt;
+  for (uint32_t g = g0; g < g1; ++g) {
+    const int op = gate_op(src, g);
+    if (op >= 0 && op < SHE_NOT) lanes[pos++] = g;
+    if (op == SHE_MUX) lanes[pos++] = g | 0x80000000u;
+  }
+  if (tid == T - 1) *nlanes = part[tid];
 }
 
 // K1: BK -> NTT domain (signed lift, N^-1 folded).  One warp per polynomial.
@@ -352,7 +441,10 @@ struct she_ctx {
   uint64_t* tw = nullptr;
   uint64_t* itw = nullptr;
   uint32_t* ext = nullptr;
+  uint32_t* lane_buf = nullptr;  // compact lane list (+ count at [ext_lanes])
   size_t ext_lanes = 0;
+  int sms = 148;
+  int br_lanes_per_cta = 4;  // G: lanes served in lock step by one persistent CTA
   // staging for the host-buffer API
   uint8_t* h_ops = nullptr;
   uint32_t* h_io = nullptr;
@@ -372,7 +464,7 @@ struct she_ctx {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<cudaEvent_t> ev_marks;  // triples: before BR, after BR, after KS
   double br_ms = 0, ks_ms = 0;
-  uint64_t br_launches = 0, ks_launches = 0, lanes = 0;
+  uint64_t br_launches = 0, ks_launches = 0;
 };
 
 namespace {
@@ -421,8 +513,10 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   cudaFree(d_bk32);
-  CK(cudaFuncSetAttribute(br_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)br_smem_bytes<S>(p.n)));
+  CK(cudaFuncSetAttribute(br_kernel<S, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(4 * br::Lane<S>::bytes(p.n))));
+  CK(cudaFuncSetAttribute(br_kernel<S, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(5 * br::Lane<S>::bytes(p.n))));
   return SHE_OK;
 }
 
@@ -431,10 +525,13 @@ she_status ensure_ext(she_ctx* ctx, size_t lanes) {
   if (ctx->ext) {
     CK(cudaDeviceSynchronize());
     cudaFree(ctx->ext);
+    cudaFree(ctx->lane_buf);
     ctx->ext = nullptr;
+    ctx->lane_buf = nullptr;
   }
   size_t want = std::max(lanes, (size_t)1024);
   CK(cudaMalloc(&ctx->ext, want * ctx->ext_stride * 4));
+  CK(cudaMalloc(&ctx->lane_buf, (want + 1) * 4));  // list + count
   ctx->ext_lanes = want;
   return SHE_OK;
 }
@@ -455,12 +552,35 @@ cudaEvent_t mark(she_ctx* ctx, cudaStream_t stream) {
   return e;
 }
 
+template <class S, int G>
+she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
+  const size_t smem = G * br::Lane<S>::bytes(ctx->p.n);
+  const size_t groups = (max_lanes + G - 1) / G;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(groups, ctx->sms)));
+  cfg.blockDim = dim3(128 * G);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (ctx->persist) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = ctx->bk;
+    attr[0].val.accessPolicyWindow.num_bytes = ctx->bk_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  CK(cudaLaunchKernelEx(&cfg, br_kernel<S, G>, a));
+  return SHE_OK;
+}
+
 template <class S>
 she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
   const size_t total = src.count;
   she_status st = ensure_ext(ctx, 2 * std::min(total, kChunk));
   if (st != SHE_OK) return st;
-  const size_t smem = br_smem_bytes<S>(ctx->p.n);
   for (size_t g0 = 0; g0 < total; g0 += kChunk) {
     const size_t cnt = std::min(kChunk, total - g0);
     GateSrc s = src;
@@ -475,34 +595,23 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
       s.out += g0 * s.stride;
     }
     s.count = (uint32_t)cnt;
+    uint32_t* nl = ctx->lane_buf + ctx->ext_lanes;
+    lane_list_kernel<<<1, 1024, 0, stream>>>(s, ctx->lane_buf, nl);
+    CK(cudaGetLastError());
     BRArgs a;
     a.src = s;
-    a.lane_base = 0;
+    a.lanes = ctx->lane_buf;
+    a.nlanes = nl;
     a.bk = ctx->bk;
     a.tw = ctx->tw;
     a.itw = ctx->itw;
     a.ext = ctx->ext;
     a.ext_stride = ctx->ext_stride;
     a.geo = ctx->geo;
-
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * cnt));
-    cfg.blockDim = dim3(kBRThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    if (ctx->persist) {
-      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      attr[0].val.accessPolicyWindow.base_ptr = ctx->bk;
-      attr[0].val.accessPolicyWindow.num_bytes = ctx->bk_bytes;
-      attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-    }
     if (ctx->timing) mark(ctx, stream);
-    CK(cudaLaunchKernelEx(&cfg, br_kernel<S>, a));
+    st = ctx->br_lanes_per_cta == 5 ? launch_br<S, 5>(ctx, a, 2 * cnt, stream)
+                                    : launch_br<S, 4>(ctx, a, 2 * cnt, stream);
+    if (st != SHE_OK) return st;
     if (ctx->timing) mark(ctx, stream);
 
     KSArgs k;
@@ -550,6 +659,8 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
   ctx->geo = make_geometry(*p);
   ctx->stride = (uint32_t)lwe_stride(*p);
   ctx->ext_stride = (p->N + 1 + 31) / 32 * 32;
+  cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char* e = getenv("SHE_BR_LANES_PER_CTA")) ctx->br_lanes_per_cta = atoi(e) == 5 ? 5 : 4;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
     she_ctx_destroy(ctx);
@@ -596,6 +707,7 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaFree(ctx->tw);
   cudaFree(ctx->itw);
   cudaFree(ctx->ext);
+  cudaFree(ctx->lane_buf);
   cudaFree(ctx->h_ops);
   cudaFree(ctx->h_io);
   cudaFree(ctx->table);

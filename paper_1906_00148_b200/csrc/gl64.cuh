@@ -88,32 +88,54 @@ __host__ __device__ __forceinline__ uint64_t mul_2_32(uint64_t x) {
   return reduce96(x << 32, x >> 32);
 }
 
-// x * 2^s mod p for 0 <= s < 192 (s is a compile-time constant at every call
-// site of the NTT, so the branches fold away).
+// x * 2^s mod p for 0 <= s < 96, as a non-negative lazy value.
+// Write y = x * 2^(s mod 32) exactly as 96 bits (w2:w1:w0), w2 < 2^31, then
+// fold the powers 2^64 = 2^32 - 1, 2^96 = -1, 2^128 = -2^32:
+//   s in [0, 32):   y              = (w1:w0) + w2 EPS
+//   s in [32, 64):  y 2^32         = (w0 << 32) + w1 EPS - w2
+//   s in [64, 96):  y 2^64         = w0 EPS - (w2:w1)
+// Each case needs at most one carry and one borrow fold (bounds in DESIGN.md).
+__host__ __device__ __forceinline__ uint64_t mul_pow2_pos(uint64_t x, int s) {
+  if (s == 0) return x;
+  const int r = s & 31;
+  const uint32_t x0 = (uint32_t)x, x1 = (uint32_t)(x >> 32);
+  uint32_t w0, w1, w2;
+  if (r == 0) {
+    w0 = x0;
+    w1 = x1;
+    w2 = 0;
+  } else {
+    const uint64_t P = (uint64_t)x0 << r;                  // x0 2^r
+    const uint64_t W = ((uint64_t)x1 << r) + (P >> 32);    // (w2:w1), < 2^63
+    w0 = (uint32_t)P;
+    w1 = (uint32_t)W;
+    w2 = (uint32_t)(W >> 32);
+  }
+  if (s < 32) {
+    const uint64_t m = ((uint64_t)w2 << 32) - w2;  // w2 EPS
+    uint64_t v = (((uint64_t)w1 << 32) | w0) + m;
+    if (v < m) v += EPS;  // carry (no second carry: v < m < 2^63 after the wrap)
+    return v;
+  }
+  if (s < 64) {
+    const uint64_t m = ((uint64_t)w1 << 32) - w1;  // w1 EPS
+    uint64_t v = ((uint64_t)w0 << 32) + m;
+    if (v < m) v += EPS;
+    uint64_t d = v - w2;
+    if (v < w2) d -= EPS;  // borrow: + p (no second borrow)
+    return d;
+  }
+  // 64 <= s < 96
+  const uint64_t a = ((uint64_t)w0 << 32) - w0;  // w0 EPS
+  const uint64_t b = ((uint64_t)w2 << 32) | w1;  // (w2:w1) < 2^63
+  uint64_t d = a - b;
+  if (a < b) d -= EPS;  // + p
+  return d;
+}
+
+// x * 2^s mod p for 0 <= s < 192 (2^96 = -1).
 __host__ __device__ __forceinline__ uint64_t mul_pow2(uint64_t x, int s) {
-  bool negate = false;
-  if (s >= 96) {  // 2^96 = -1
-    s -= 96;
-    negate = true;
-  }
-  uint64_t r;
-  if (s == 0) {
-    r = x;
-  } else if (s < 32) {
-    r = reduce96(x << s, x >> (64 - s));
-  } else if (s == 32) {
-    r = mul_2_32(x);
-  } else if (s < 64) {
-    r = reduce128(x << s, x >> (64 - s));
-  } else if (s == 64) {
-    r = reduce128(0, x);
-  } else {  // 64 < s < 96: (x 2^(s-64)) 2^64, the 2^128 part = -2^32
-    uint64_t lo = x << (s - 64), top = x >> (128 - s);  // x 2^(s-64) = top 2^64 + lo
-    // value = lo 2^64 + top 2^128 = lo (2^32 - 1) - top 2^32  (top < 2^32)
-    uint64_t a = reduce128(0, lo);
-    r = sub(a, top << 32);
-  }
-  return negate ? neg(r) : r;
+  return s >= 96 ? neg(mul_pow2_pos(x, s - 96)) : mul_pow2_pos(x, s);
 }
 
 __host__ __device__ inline uint64_t pow(uint64_t b, uint64_t e) {
@@ -124,6 +146,38 @@ __host__ __device__ inline uint64_t pow(uint64_t b, uint64_t e) {
     e >>= 1;
   }
   return canon(r);
+}
+
+// Lazy multiply-accumulate of up to 4 products (< 2^130) with one reduction:
+// value = lo + hi 2^64 + top 2^128, and 2^128 = -2^32 (mod p).
+struct Acc3 {
+  uint64_t lo = 0, hi = 0;
+  uint32_t top = 0;
+};
+
+__host__ __device__ __forceinline__ void mac(Acc3& A, uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  const uint64_t l = a * b, h = __umul64hi(a, b);
+  asm("add.cc.u64 %0, %0, %3;\n\t"
+      "addc.cc.u64 %1, %1, %4;\n\t"
+      "addc.u32 %2, %2, 0;"
+      : "+l"(A.lo), "+l"(A.hi), "+r"(A.top)
+      : "l"(l), "l"(h));
+#else
+  const unsigned __int128 pr = (unsigned __int128)a * b;
+  const unsigned __int128 s = (((unsigned __int128)A.hi << 64) | A.lo) + pr;
+  if (s < pr) A.top += 1;
+  A.lo = (uint64_t)s;
+  A.hi = (uint64_t)(s >> 64);
+#endif
+}
+
+__host__ __device__ __forceinline__ uint64_t reduce_acc(const Acc3& A) {
+  const uint64_t r = reduce128(A.lo, A.hi);
+  const uint64_t t = (uint64_t)A.top << 32;  // top <= 3
+  uint64_t d = r - t;
+  if (r < t) d -= EPS;  // + p (single borrow: r - t >= -2^34)
+  return d;
 }
 
 // Signed small integer -> F_p.

@@ -39,57 +39,108 @@ struct Emu {
   }
 };
 
+// The inverse of output component c by the warp pair (2c, 2c+1), phase by
+// phase (the device separates the phases with named barriers).
+template <class S>
+void inverse_component(Emu<S>& E, br::Lane<S>& ln, int c, uint32_t* accc) {
+  constexpr int L = S::L;
+  uint64_t* row = ln.row(c);
+  uint64_t* xb = ln.row(2 + c);
+  std::vector<uint64_t> y(2 * L * (L / 2)), lo(2 * L * (L / 4)), hi(2 * L * (L / 4));
+  auto Y = [&](int H, int t) { return reinterpret_cast<uint64_t(*)[L / 2]>(&y[(H * L + t) * (L / 2)]); };
+  auto LO = [&](int H, int t) { return reinterpret_cast<uint64_t(*)[L / 4]>(&lo[(H * L + t) * (L / 4)]); };
+  auto HI = [&](int H, int t) { return reinterpret_cast<uint64_t(*)[L / 4]>(&hi[(H * L + t) * (L / 4)]); };
+  // pass A (cyclic inverse over rows)
+  for (int t = 0; t < L; ++t) {
+    br::inv_a_load<S, 0>(t, row, *Y(0, t));
+    br::inv_a_load<S, 1>(t, row, *Y(1, t));
+  }
+  for (int t = 0; t < L; ++t) {
+    br::inv_stages_send<S, 0, false>(t, *Y(0, t), xb);
+    br::inv_stages_send<S, 1, false>(t, *Y(1, t), xb);
+  }
+  for (int t = 0; t < L; ++t) {
+    br::inv_recv_cross<S, 0, false>(t, *Y(0, t), xb, *LO(0, t), *HI(0, t));
+    br::inv_recv_cross<S, 1, false>(t, *Y(1, t), xb, *LO(1, t), *HI(1, t));
+  }
+  for (int t = 0; t < L; ++t) {
+    br::inv_a_store<S, 0>(t, *LO(0, t), *HI(0, t), E.itw.data(), row);
+    br::inv_a_store<S, 1>(t, *LO(1, t), *HI(1, t), E.itw.data(), row);
+  }
+  // pass B (negacyclic inverse over columns)
+  for (int t = 0; t < L; ++t) {
+    br::inv_b_load<S, 0>(t, row, *Y(0, t));
+    br::inv_b_load<S, 1>(t, row, *Y(1, t));
+  }
+  for (int t = 0; t < L; ++t) {
+    br::inv_stages_send<S, 0, true>(t, *Y(0, t), xb);
+    br::inv_stages_send<S, 1, true>(t, *Y(1, t), xb);
+  }
+  for (int t = 0; t < L; ++t) {
+    br::inv_recv_cross<S, 0, true>(t, *Y(0, t), xb, *LO(0, t), *HI(0, t));
+    br::inv_recv_cross<S, 1, true>(t, *Y(1, t), xb, *LO(1, t), *HI(1, t));
+  }
+  for (int t = 0; t < L; ++t) {
+    br::inv_b_acc<S, 0>(t, *LO(0, t), *HI(0, t), accc);
+    br::inv_b_acc<S, 1>(t, *LO(1, t), *HI(1, t), accc);
+  }
+}
+
+template <class S>
+void forward_row(Emu<S>& E, br::Lane<S>& ln, int w, const uint64_t (*xs)[S::L]) {
+  constexpr int L = S::L;
+  uint64_t* row = ln.row(w);
+  for (int lane = 0; lane < L; ++lane) {
+    uint64_t x[L];
+    memcpy(x, xs[lane], sizeof(x));
+    br::fwd_pass1_store<S>(lane, x, row);
+  }
+  std::vector<uint64_t> regs((size_t)L * L);
+  for (int lane = 0; lane < L; ++lane) {
+    uint64_t y[L];
+    br::fwd_pass2_load<S>(lane, row, E.tw.data(), y);
+    memcpy(&regs[lane * L], y, sizeof(y));
+  }
+  for (int lane = 0; lane < L; ++lane) {
+    uint64_t y[L];
+    memcpy(y, &regs[lane * L], sizeof(y));
+    br::fwd_pass2_store<S>(lane, y, row);
+  }
+}
+
 template <class S>
 void blind_rotate(const br::Geometry& g, const uint64_t* bk_ntt, const uint32_t* ct,
-                  uint32_t* acc) {
+                  uint32_t* acc_out) {
   constexpr int L = S::L, N = S::N;
   static Emu<S> E;
-  const int rows = 2 * g.l;
-  std::vector<uint64_t> buf((size_t)4 * L * (L + 1));
-  std::vector<uint64_t> regs((size_t)4 * L * L);
-  const uint32_t bbar = br::modswitch(ct[g.n], g.lg2N);
+  std::vector<uint8_t> smem(br::Lane<S>::bytes(g.n) + 64, 0);
+  br::Lane<S> ln(smem.data());
+  for (uint32_t k = 0; k <= g.n; ++k) ln.abar[k] = (uint16_t)br::modswitch(ct[k], g.lg2N);
+  const uint32_t bbar = ln.abar[g.n];
   for (uint32_t m = 0; m < (uint32_t)N; ++m) {
-    acc[m] = 0;
-    acc[N + m] = br::testvec_coeff(m, bbar, N);
+    ln.acc[m] = 0;
+    ln.acc[N + m] = br::testvec_coeff(m, bbar, N);
   }
+  std::vector<uint64_t> xs((size_t)L * L);
   for (uint32_t i = 0; i < g.n; ++i) {
-    const uint32_t a = br::modswitch(ct[i], g.lg2N);
-    if (a == 0) continue;  // R9: digits of X^0 ACC - ACC = 0 are all 0
-    for (int w = 0; w < rows; ++w)
+    const uint32_t a = ln.abar[i];  // no skip: the device runs a = 0 as well
+    for (int w = 0; w < 4; ++w) {
       for (int lane = 0; lane < L; ++lane) {
         uint64_t x[L];
-        br::load_digits<S>(g, w, lane, acc, a, x);
-        br::fwd_pass1_store<S>(lane, x, br::buf_row<S>(buf.data(), w));
+        br::load_digits<S>(g, w, lane, ln.acc, a, x);
+        memcpy(&xs[lane * L], x, sizeof(x));
       }
-    for (int w = 0; w < rows; ++w) {
-      for (int lane = 0; lane < L; ++lane) {
-        uint64_t y[L];
-        br::fwd_pass2_load<S>(lane, br::buf_row<S>(buf.data(), w), E.tw.data(), y);
-        memcpy(&regs[(w * L + lane) * L], y, sizeof(y));
-      }
-      for (int lane = 0; lane < L; ++lane) {
-        uint64_t y[L];
-        memcpy(y, &regs[(w * L + lane) * L], sizeof(y));
-        br::fwd_pass2_store<S>(lane, y, br::buf_row<S>(buf.data(), w));
-      }
+      forward_row<S>(E, ln, w, reinterpret_cast<const uint64_t(*)[L]>(xs.data()));
     }
-    const uint64_t* bki = bk_ntt + (size_t)i * rows * 2 * N;
-    for (int t = 0; t < 128; ++t) br::pointwise<S>(t, 128, rows, buf.data(), bki);
-    for (int w = 0; w < 2; ++w) {
-      for (int lane = 0; lane < L; ++lane) {
-        uint64_t y[L];
-        br::inv_pass2_load<S>(lane, br::buf_row<S>(buf.data(), w), y);
-        memcpy(&regs[(w * L + lane) * L], y, sizeof(y));
-      }
-      for (int lane = 0; lane < L; ++lane) {
-        uint64_t y[L];
-        memcpy(y, &regs[(w * L + lane) * L], sizeof(y));
-        br::inv_pass2_store<S>(lane, y, E.itw.data(), br::buf_row<S>(buf.data(), w));
-      }
-      for (int lane = 0; lane < L; ++lane)
-        br::inv_pass1_acc<S>(lane, br::buf_row<S>(buf.data(), w), acc + w * N);
+    const uint64_t* bki = bk_ntt + (size_t)i * 8 * N;
+    for (int p = 0; p < N; ++p) {
+      uint64_t b[8];
+      for (int q = 0; q < 8; ++q) b[q] = bki[(size_t)q * N + p];
+      br::pointwise_pos<S>(ln.buf, p, b);
     }
+    for (int c = 0; c < 2; ++c) inverse_component<S>(E, ln, c, ln.acc + c * N);
   }
+  memcpy(acc_out, ln.acc, sizeof(uint32_t) * 2 * N);
 }
 
 br::Geometry geometry(uint32_t N, uint32_t n, uint32_t l, uint32_t bg_bits) {
@@ -111,45 +162,28 @@ br::Geometry geometry(uint32_t N, uint32_t n, uint32_t l, uint32_t bg_bits) {
 
 extern "C" {
 
-// out = d * b in Z_{2^32}[X]/(X^N+1) through the device NTT path.
+// out = d * b in Z_{2^32}[X]/(X^N+1) through the device NTT path (row 0 of
+// the pointwise with BK row [0][0] = NTT(b), all other rows and outputs 0).
 int she_emu_negacyclic_mul(uint32_t N, const int32_t* d, const uint32_t* b, uint32_t* out) {
   auto run = [&](auto shape) {
     using S = decltype(shape);
     constexpr int L = S::L, NN = S::N;
     static Emu<S> E;
-    std::vector<uint64_t> bki((size_t)4 * 2 * NN, 0);  // rows x 2 outputs; only [0][0] used
+    std::vector<uint64_t> bki((size_t)8 * NN, 0);
     E.bk_transform(b, bki.data());
-    std::vector<uint64_t> buf((size_t)4 * L * (L + 1), 0);
-    uint64_t* row = buf.data();
-    for (int lane = 0; lane < L; ++lane) {
-      uint64_t x[L];
-      for (int j2 = 0; j2 < L; ++j2) x[j2] = gl::from_i64(d[lane + L * j2]);
-      br::fwd_pass1_store<S>(lane, x, row);
-    }
-    std::vector<uint64_t> regs((size_t)L * L);
-    for (int lane = 0; lane < L; ++lane) {
-      uint64_t y[L];
-      br::fwd_pass2_load<S>(lane, row, E.tw.data(), y);
-      memcpy(&regs[lane * L], y, sizeof(y));
-    }
-    for (int lane = 0; lane < L; ++lane) {
-      uint64_t y[L];
-      memcpy(y, &regs[lane * L], sizeof(y));
-      br::fwd_pass2_store<S>(lane, y, row);
-    }
-    for (int t = 0; t < 128; ++t) br::pointwise<S>(t, 128, 1, buf.data(), bki.data());
-    for (int lane = 0; lane < L; ++lane) {
-      uint64_t y[L];
-      br::inv_pass2_load<S>(lane, row, y);
-      memcpy(&regs[lane * L], y, sizeof(y));
-    }
-    for (int lane = 0; lane < L; ++lane) {
-      uint64_t y[L];
-      memcpy(y, &regs[lane * L], sizeof(y));
-      br::inv_pass2_store<S>(lane, y, E.itw.data(), row);
+    std::vector<uint8_t> smem(br::Lane<S>::bytes(0) + 64, 0);
+    br::Lane<S> ln(smem.data());
+    std::vector<uint64_t> xs((size_t)L * L);
+    for (int lane = 0; lane < L; ++lane)
+      for (int j2 = 0; j2 < L; ++j2) xs[lane * L + j2] = gl::from_i64(d[lane + L * j2]);
+    forward_row<S>(E, ln, 0, reinterpret_cast<const uint64_t(*)[L]>(xs.data()));
+    for (int p = 0; p < NN; ++p) {
+      uint64_t bb[8];
+      for (int q = 0; q < 8; ++q) bb[q] = bki[(size_t)q * NN + p];
+      br::pointwise_pos<S>(ln.buf, p, bb);
     }
     memset(out, 0, sizeof(uint32_t) * NN);
-    for (int lane = 0; lane < L; ++lane) br::inv_pass1_acc<S>(lane, row, out);
+    inverse_component<S>(E, ln, 0, out);
     return 0;
   };
   if (N == 1024) return run(ntt::Shape<1024>{});

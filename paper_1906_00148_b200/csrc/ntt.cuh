@@ -29,95 +29,102 @@ __host__ __device__ constexpr int brev(int x, int bits) {
 }
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 
-// Forward negacyclic length-L NTT in registers; theta = 2^SH has order 2L.
-// Out: a[q] = sum_j a_j theta^((2 brev(q) + 1) j).
-template <int L, int SH>
-__host__ __device__ __forceinline__ void nega_fwd(uint64_t (&a)[L]) {
+// t = x * 2^s for a compile-time shift s in [0, 192): returns x * 2^(s mod 96)
+// and reports the sign (2^96 = -1) so butterflies swap add/sub instead of
+// negating.
+__host__ __device__ __forceinline__ uint64_t shift_twiddle(uint64_t x, int s, bool& negative) {
+  negative = s >= 96;
+  return gl::mul_pow2_pos(x, negative ? s - 96 : s);
+}
+
+// CT butterfly (lo, hi) <- (lo + w hi, lo - w hi), w = 2^s.
+__host__ __device__ __forceinline__ void ct_bfly(uint64_t& lo, uint64_t& hi, int s) {
+  bool ng;
+  const uint64_t t = shift_twiddle(hi, s, ng);
+  const uint64_t u = lo;
+  lo = ng ? gl::sub(u, t) : gl::add(u, t);
+  hi = ng ? gl::add(u, t) : gl::sub(u, t);
+}
+
+// GS butterfly (lo, hi) <- (lo + hi, (lo - hi) w), w = 2^s; for w = -2^(s-96)
+// the difference is taken the other way round instead of negating.
+__host__ __device__ __forceinline__ void gs_bfly(uint64_t& lo, uint64_t& hi, int s) {
+  const uint64_t u = lo, v = hi;
+  lo = gl::add(u, v);
+  hi = s >= 96 ? gl::mul_pow2_pos(gl::sub(v, u), s - 96) : gl::mul_pow2_pos(gl::sub(u, v), s);
+}
+
+// Twiddle shift of block b at stage k of a length-L transform.
+//   negacyclic (theta = 2^SH, order 2L): theta^((2 brev_k(b) + 1) L / 2^(k+1))
+//   cyclic     (omega = 2^SH, order L) : omega^(brev_k(b) L / 2^(k+1))
+template <bool NEGA>
+__host__ __device__ constexpr int stage_shift(int L, int SH, int k, int b) {
+  return NEGA ? (SH * (2 * brev(b, k) + 1) * (L >> (k + 1))) % 192
+              : (SH * brev(b, k) * (L >> (k + 1))) % 192;
+}
+__host__ __device__ constexpr int inv_shift(int s) { return (192 - s) % 192; }
+
+// Forward length-L transform in registers (CT, natural in, bit-reversed out).
+//   NEGA: a[q] = sum_j a_j theta^((2 brev(q) + 1) j)
+//   cyc : a[q] = sum_j a_j omega^(brev(q) j)
+template <int L, int SH, bool NEGA>
+__host__ __device__ __forceinline__ void fwd(uint64_t (&a)[L]) {
   constexpr int LG = ilog2(L);
 #pragma unroll
   for (int k = 0; k < LG; ++k) {
     const int len = L >> (k + 1);
 #pragma unroll
     for (int b = 0; b < (1 << k); ++b) {
-      const int x = (2 * brev(b, k) + 1) * len;  // twiddle theta^x
-      const int s = (SH * x) % 192;
+      const int s = stage_shift<NEGA>(L, SH, k, b);
 #pragma unroll
-      for (int j = 0; j < len; ++j) {
-        const int lo = b * 2 * len + j, hi = lo + len;
-        uint64_t t = gl::mul_pow2(a[hi], s);
-        uint64_t u = a[lo];
-        a[lo] = gl::add(u, t);
-        a[hi] = gl::sub(u, t);
-      }
+      for (int j = 0; j < len; ++j) ct_bfly(a[b * 2 * len + j], a[b * 2 * len + j + len], s);
     }
   }
 }
 
-// Exact inverse of nega_fwd up to the factor L.
-template <int L, int SH>
-__host__ __device__ __forceinline__ void nega_inv(uint64_t (&a)[L]) {
+// Exact inverse of fwd up to the factor L (GS, bit-reversed in, natural out).
+template <int L, int SH, bool NEGA>
+__host__ __device__ __forceinline__ void inv(uint64_t (&a)[L]) {
   constexpr int LG = ilog2(L);
 #pragma unroll
   for (int k = LG - 1; k >= 0; --k) {
     const int len = L >> (k + 1);
 #pragma unroll
     for (int b = 0; b < (1 << k); ++b) {
-      const int x = (2 * brev(b, k) + 1) * len;
-      const int s = (192 - (SH * x) % 192) % 192;  // theta^-x
+      const int s = inv_shift(stage_shift<NEGA>(L, SH, k, b));
 #pragma unroll
-      for (int j = 0; j < len; ++j) {
-        const int lo = b * 2 * len + j, hi = lo + len;
-        uint64_t u = a[lo], v = a[hi];
-        a[lo] = gl::add(u, v);
-        a[hi] = gl::mul_pow2(gl::sub(u, v), s);
-      }
+      for (int j = 0; j < len; ++j) gs_bfly(a[b * 2 * len + j], a[b * 2 * len + j + len], s);
     }
   }
 }
 
-// Forward cyclic length-L NTT in registers; omega = 2^SH2 has order L.
-// Out: a[q] = sum_j a_j omega^(brev(q) j).
-template <int L, int SH2>
-__host__ __device__ __forceinline__ void cyc_fwd(uint64_t (&a)[L]) {
+// The inverse split over two threads H = 0, 1 holding halves a[H L/2 + m]:
+// stages k = LG-1 .. 1 never cross the halves ...
+template <int L, int SH, bool NEGA, int H>
+__host__ __device__ __forceinline__ void inv_half(uint64_t (&a)[L / 2]) {
   constexpr int LG = ilog2(L);
 #pragma unroll
-  for (int k = 0; k < LG; ++k) {
+  for (int k = LG - 1; k >= 1; --k) {
     const int len = L >> (k + 1);
+    const int nb = 1 << (k - 1);  // blocks per half
 #pragma unroll
-    for (int b = 0; b < (1 << k); ++b) {
-      const int x = brev(b, k) * len;  // omega^x
-      const int s = (SH2 * x) % 192;
+    for (int bb = 0; bb < nb; ++bb) {
+      const int b = H * nb + bb;
+      const int s = inv_shift(stage_shift<NEGA>(L, SH, k, b));
 #pragma unroll
-      for (int j = 0; j < len; ++j) {
-        const int lo = b * 2 * len + j, hi = lo + len;
-        uint64_t t = gl::mul_pow2(a[hi], s);
-        uint64_t u = a[lo];
-        a[lo] = gl::add(u, t);
-        a[hi] = gl::sub(u, t);
-      }
+      for (int j = 0; j < len; ++j) gs_bfly(a[bb * 2 * len + j], a[bb * 2 * len + j + len], s);
     }
   }
 }
-
-template <int L, int SH2>
-__host__ __device__ __forceinline__ void cyc_inv(uint64_t (&a)[L]) {
-  constexpr int LG = ilog2(L);
+// ... and stage 0 pairs element j with j + L/2 (one twiddle for all j).
+// Thread H computes the butterflies j in [H L/4, (H+1) L/4): it keeps u (H=0)
+// or v (H=1) for those j and receives the other operand from its partner.
+// On return lo[m] = out[H L/4 + m], hi[m] = out[H L/4 + m + L/2].
+template <int L, int SH, bool NEGA>
+__host__ __device__ __forceinline__ void inv_cross(uint64_t (&lo)[L / 4], uint64_t (&hi)[L / 4]) {
+  const int s = inv_shift(stage_shift<NEGA>(L, SH, 0, 0));
 #pragma unroll
-  for (int k = LG - 1; k >= 0; --k) {
-    const int len = L >> (k + 1);
-#pragma unroll
-    for (int b = 0; b < (1 << k); ++b) {
-      const int x = brev(b, k) * len;
-      const int s = (192 - (SH2 * x) % 192) % 192;
-#pragma unroll
-      for (int j = 0; j < len; ++j) {
-        const int lo = b * 2 * len + j, hi = lo + len;
-        uint64_t u = a[lo], v = a[hi];
-        a[lo] = gl::add(u, v);
-        a[hi] = gl::mul_pow2(gl::sub(u, v), s);
-      }
-    }
-  }
+  for (int m = 0; m < L / 4; ++m) gs_bfly(lo[m], hi[m], s);
 }
 
 // Compile-time description of the transform for a ring dimension N = L^2.
