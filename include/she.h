@@ -204,18 +204,20 @@ she_status she_ctx_layer_stats(she_ctx* ctx, she_circuit_stats* stats);
 
 /* Clear-bit backend: the same circuits evaluated on plaintext bits (uint8 per
  * bit, layouts as above without the stride axis), host only.  For testing the
- * scheduler and counting gates; stats may be NULL. */
+ * scheduler and counting gates; stats may be NULL.  rank/world select the
+ * same output shard a context with that rank/world computes (only those
+ * output words are written). */
 she_status she_clear_conv_shift_acc(const uint8_t* in, int H, int W, int C, int w_in,
                                     int in_signed, const int8_t* wq, int Co, int K, int stride,
                                     int pad, int acc_cap, int relu, uint8_t* out, int* w_out,
-                                    she_circuit_stats* stats);
+                                    int rank, int world, she_circuit_stats* stats);
 she_status she_clear_fc_shift_acc(const uint8_t* in, int K, int w_in, int in_signed,
                                   const int8_t* wq, int M, int acc_cap, int relu, uint8_t* out,
-                                  int* w_out, she_circuit_stats* stats);
-she_status she_clear_relu(const uint8_t* in, size_t words, int width, uint8_t* out,
-                          she_circuit_stats* stats);
+                                  int* w_out, int rank, int world, she_circuit_stats* stats);
+she_status she_clear_relu(const uint8_t* in, size_t words, int width, uint8_t* out, int rank,
+                          int world, she_circuit_stats* stats);
 she_status she_clear_maxpool2x2(const uint8_t* in, int H, int W, int C, int w, int in_signed,
-                                uint8_t* out, she_circuit_stats* stats);
+                                uint8_t* out, int rank, int world, she_circuit_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ HEADERS = ["gl64.cuh", "ntt.cuh", "bootstrap_core.cuh", "common.h", "keys.h", "s
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_FLAGS = "-fPIC,-fopenmp,-ffp-contract=off,-march=x86-64-v3"
-NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-DGL_ADDSUB_PTX",
               "-Xcompiler", HOST_FLAGS]
 
 

@@ -36,6 +36,39 @@ __host__ __device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) {
 
 __host__ __device__ __forceinline__ uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
 
+#if defined(__CUDA_ARCH__) && defined(GL_ADDSUB_PTX)
+// a + b mod p (lazy in, lazy out): 64-bit add, fold each carry as +EPS with
+// IMAD carry chains (FMA pipe) instead of 64-bit compares and selects.
+__device__ __forceinline__ uint64_t add(uint64_t a, uint64_t b) {
+  uint32_t s0, s1, c;
+  asm("add.cc.u32 %0, %3, %5;\n\t"
+      "addc.cc.u32 %1, %4, %6;\n\t"
+      "addc.u32 %2, 0, 0;\n\t"
+      "mad.lo.cc.u32 %0, %2, 0xFFFFFFFF, %0;\n\t"
+      "madc.hi.cc.u32 %1, %2, 0xFFFFFFFF, %1;\n\t"
+      "addc.u32 %2, 0, 0;\n\t"
+      "mad.lo.cc.u32 %0, %2, 0xFFFFFFFF, %0;\n\t"
+      "madc.hi.u32 %1, %2, 0xFFFFFFFF, %1;"
+      : "=&r"(s0), "=&r"(s1), "=&r"(c)
+      : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)));
+  return ((uint64_t)s1 << 32) | s0;
+}
+// a - b mod p: borrow chains; each borrow subtracts EPS (= adds p).
+__device__ __forceinline__ uint64_t sub(uint64_t a, uint64_t b) {
+  uint32_t d0, d1, bw;
+  asm("sub.cc.u32 %0, %3, %5;\n\t"
+      "subc.cc.u32 %1, %4, %6;\n\t"
+      "subc.u32 %2, 0, 0;\n\t"
+      "sub.cc.u32 %0, %0, %2;\n\t"
+      "subc.cc.u32 %1, %1, 0;\n\t"
+      "subc.u32 %2, 0, 0;\n\t"
+      "sub.cc.u32 %0, %0, %2;\n\t"
+      "subc.u32 %1, %1, 0;"
+      : "=&r"(d0), "=&r"(d1), "=&r"(bw)
+      : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)));
+  return ((uint64_t)d1 << 32) | d0;
+}
+#else
 // a + b mod p (lazy in, lazy out).
 __host__ __device__ __forceinline__ uint64_t add(uint64_t a, uint64_t b) {
   uint64_t s = a + b;
@@ -57,6 +90,7 @@ __host__ __device__ __forceinline__ uint64_t sub(uint64_t a, uint64_t b) {
   }
   return d;
 }
+#endif
 
 __host__ __device__ __forceinline__ uint64_t neg(uint64_t a) { return sub(0, a); }
 
@@ -95,6 +129,44 @@ __host__ __device__ __forceinline__ uint64_t mul_2_32(uint64_t x) {
 //   s in [32, 64):  y 2^32         = (w0 << 32) + w1 EPS - w2
 //   s in [64, 96):  y 2^64         = w0 EPS - (w2:w1)
 // Each case needs at most one carry and one borrow fold (bounds in DESIGN.md).
+// x + y with ONE carry fold (callers guarantee no second wrap).
+__host__ __device__ __forceinline__ uint64_t add_fold1(uint64_t x, uint64_t y) {
+#if defined(__CUDA_ARCH__) && defined(GL_ADDSUB_PTX)
+  uint32_t s0, s1, c;
+  asm("add.cc.u32 %0, %3, %5;\n\t"
+      "addc.cc.u32 %1, %4, %6;\n\t"
+      "addc.u32 %2, 0, 0;\n\t"
+      "mad.lo.cc.u32 %0, %2, 0xFFFFFFFF, %0;\n\t"
+      "madc.hi.u32 %1, %2, 0xFFFFFFFF, %1;"
+      : "=&r"(s0), "=&r"(s1), "=&r"(c)
+      : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32)));
+  return ((uint64_t)s1 << 32) | s0;
+#else
+  uint64_t v = x + y;
+  if (v < y) v += EPS;
+  return v;
+#endif
+}
+
+// x - y with ONE borrow fold (+p; callers guarantee no second borrow).
+__host__ __device__ __forceinline__ uint64_t sub_fold1(uint64_t x, uint64_t y) {
+#if defined(__CUDA_ARCH__) && defined(GL_ADDSUB_PTX)
+  uint32_t d0, d1, bw;
+  asm("sub.cc.u32 %0, %3, %5;\n\t"
+      "subc.cc.u32 %1, %4, %6;\n\t"
+      "subc.u32 %2, 0, 0;\n\t"
+      "sub.cc.u32 %0, %0, %2;\n\t"
+      "subc.u32 %1, %1, 0;"
+      : "=&r"(d0), "=&r"(d1), "=&r"(bw)
+      : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32)));
+  return ((uint64_t)d1 << 32) | d0;
+#else
+  uint64_t d = x - y;
+  if (x < y) d -= EPS;
+  return d;
+#endif
+}
+
 __host__ __device__ __forceinline__ uint64_t mul_pow2_pos(uint64_t x, int s) {
   if (s == 0) return x;
   const int r = s & 31;
@@ -105,32 +177,29 @@ __host__ __device__ __forceinline__ uint64_t mul_pow2_pos(uint64_t x, int s) {
     w1 = x1;
     w2 = 0;
   } else {
+#if defined(__CUDA_ARCH__) && defined(GL_ADDSUB_PTX)
+    // x * 2^r as two IMAD.WIDE on the FMA pipe (instead of funnel shifts)
+    uint64_t P, W;
+    const uint32_t m = 1u << r;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(P) : "r"(x0), "r"(m));
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(W) : "r"(x1), "r"(m), "l"(P >> 32));
+#else
     const uint64_t P = (uint64_t)x0 << r;                  // x0 2^r
     const uint64_t W = ((uint64_t)x1 << r) + (P >> 32);    // (w2:w1), < 2^63
+#endif
     w0 = (uint32_t)P;
     w1 = (uint32_t)W;
     w2 = (uint32_t)(W >> 32);
   }
-  if (s < 32) {
-    const uint64_t m = ((uint64_t)w2 << 32) - w2;  // w2 EPS
-    uint64_t v = (((uint64_t)w1 << 32) | w0) + m;
-    if (v < m) v += EPS;  // carry (no second carry: v < m < 2^63 after the wrap)
-    return v;
+  if (s < 32) {  // (w1:w0) + w2 EPS; after a carry the sum is < w2 EPS < 2^63
+    return add_fold1(((uint64_t)w1 << 32) | w0, ((uint64_t)w2 << 32) - w2);
   }
-  if (s < 64) {
-    const uint64_t m = ((uint64_t)w1 << 32) - w1;  // w1 EPS
-    uint64_t v = ((uint64_t)w0 << 32) + m;
-    if (v < m) v += EPS;
-    uint64_t d = v - w2;
-    if (v < w2) d -= EPS;  // borrow: + p (no second borrow)
-    return d;
+  if (s < 64) {  // (w0 << 32) + w1 EPS - w2; after the carry fold v < 2^64 - 2^32
+    const uint64_t v = add_fold1((uint64_t)w0 << 32, ((uint64_t)w1 << 32) - w1);
+    return sub_fold1(v, w2);  // v - w2 >= -2^31: one borrow at most
   }
-  // 64 <= s < 96
-  const uint64_t a = ((uint64_t)w0 << 32) - w0;  // w0 EPS
-  const uint64_t b = ((uint64_t)w2 << 32) | w1;  // (w2:w1) < 2^63
-  uint64_t d = a - b;
-  if (a < b) d -= EPS;  // + p
-  return d;
+  // 64 <= s < 96: w0 EPS - (w2:w1); w0 EPS < p, (w2:w1) < 2^63
+  return sub_fold1(((uint64_t)w0 << 32) - w0, ((uint64_t)w2 << 32) | w1);
 }
 
 // x * 2^s mod p for 0 <= s < 192 (2^96 = -1).

@@ -716,49 +716,53 @@ she_status she_ctx_layer_stats(she_ctx* ctx, she_circuit_stats* st) {
 she_status she_clear_conv_shift_acc(const uint8_t* in, int H, int W, int C, int w_in,
                                     int in_signed, const int8_t* wq, int Co, int K, int stride,
                                     int pad, int acc_cap, int relu_, uint8_t* out, int* w_out,
-                                    she_circuit_stats* st) {
+                                    int rank, int world, she_circuit_stats* st) {
   ConvGeom g{H, W, C, w_in, in_signed, Co, K, stride, pad, acc_cap, relu_, wq};
   if (st) *st = she_circuit_stats{};
   if (!out) return conv_common(g, w_out, 0, 1, nullptr, nullptr);
   if (!in) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return she::fail(SHE_ERR_ARG, "bad rank/world");
   ClearExec ex;
   ex.in = in;
   ex.out = out;
-  return conv_common(g, w_out, 0, 1, &ex, st);
+  return conv_common(g, w_out, rank, world, &ex, st);
 }
 
 she_status she_clear_fc_shift_acc(const uint8_t* in, int K, int w_in, int in_signed,
                                   const int8_t* wq, int M, int acc_cap, int relu_, uint8_t* out,
-                                  int* w_out, she_circuit_stats* st) {
+                                  int* w_out, int rank, int world, she_circuit_stats* st) {
   FcGeom g{K, w_in, in_signed, M, acc_cap, relu_, wq};
   if (st) *st = she_circuit_stats{};
   if (!out) return fc_common(g, w_out, 0, 1, nullptr, nullptr);
   if (!in) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return she::fail(SHE_ERR_ARG, "bad rank/world");
   ClearExec ex;
   ex.in = in;
   ex.out = out;
-  return fc_common(g, w_out, 0, 1, &ex, st);
+  return fc_common(g, w_out, rank, world, &ex, st);
 }
 
-she_status she_clear_relu(const uint8_t* in, size_t words, int width, uint8_t* out,
-                          she_circuit_stats* st) {
+she_status she_clear_relu(const uint8_t* in, size_t words, int width, uint8_t* out, int rank,
+                          int world, she_circuit_stats* st) {
   if (st) *st = she_circuit_stats{};
   if (words == 0) return SHE_OK;
   if (!in || !out) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return she::fail(SHE_ERR_ARG, "bad rank/world");
   ClearExec ex;
   ex.in = in;
   ex.out = out;
-  return relu_common(words, width, 0, 1, ex, st);
+  return relu_common(words, width, rank, world, ex, st);
 }
 
 she_status she_clear_maxpool2x2(const uint8_t* in, int H, int W, int C, int w, int in_signed,
-                                uint8_t* out, she_circuit_stats* st) {
+                                uint8_t* out, int rank, int world, she_circuit_stats* st) {
   if (st) *st = she_circuit_stats{};
   if (!in || !out) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return she::fail(SHE_ERR_ARG, "bad rank/world");
   ClearExec ex;
   ex.in = in;
   ex.out = out;
-  return maxpool_common(H, W, C, w, in_signed, 0, 1, ex, st);
+  return maxpool_common(H, W, C, w, in_signed, rank, world, ex, st);
 }
 
 }  // extern "C"

@@ -96,15 +96,16 @@ def lib() -> ctypes.CDLL:
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_clear_conv_shift_acc": ([_vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
-                                         + [_vp, ctypes.POINTER(ctypes.c_int),
-                                            ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
+                                         + [_vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                            ctypes.c_int, ctypes.POINTER(she_circuit_stats)],
+                                         ctypes.c_int),
             "she_clear_fc_shift_acc": ([_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
-                                        ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
-            "she_clear_relu": ([_vp, _sz, ctypes.c_int, _vp, ctypes.POINTER(she_circuit_stats)],
-                               ctypes.c_int),
-            "she_clear_maxpool2x2": ([_vp] + [ctypes.c_int] * 5 + [_vp,
+            "she_clear_relu": ([_vp, _sz, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int,
+                                ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
+            "she_clear_maxpool2x2": ([_vp] + [ctypes.c_int] * 5 + [_vp, ctypes.c_int, ctypes.c_int,
                                      ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -362,7 +363,8 @@ def layer_stats(ctx: Context) -> dict:
 
 # ---- clear-bit backend (host bits; scheduler tests and gate counts) -------------
 
-def clear_conv_shift_acc(bits, H, W, C, w_in, in_signed, wq, stride, pad, cap=16, relu=False):
+def clear_conv_shift_acc(bits, H, W, C, w_in, in_signed, wq, stride, pad, cap=16, relu=False,
+                         rank=0, world=1):
     """bits: uint8 [H][W][C][w_in]; returns (bits [Ho][Wo][Co][w], w, stats)."""
     wq = _codes(wq)
     bits = np.ascontiguousarray(bits, dtype=np.uint8)
@@ -373,11 +375,11 @@ def clear_conv_shift_acc(bits, H, W, C, w_in, in_signed, wq, stride, pad, cap=16
     st = she_circuit_stats()
     _check(lib().she_clear_conv_shift_acc(_np_ptr(bits), H, W, C, w_in, int(in_signed), _np_ptr(wq),
                                           Co, K, stride, pad, cap, int(relu), _np_ptr(out),
-                                          ctypes.byref(w), ctypes.byref(st)))
+                                          ctypes.byref(w), rank, world, ctypes.byref(st)))
     return out, w.value, st.as_dict()
 
 
-def clear_fc_shift_acc(bits, K, w_in, in_signed, wq, cap=16, relu=False):
+def clear_fc_shift_acc(bits, K, w_in, in_signed, wq, cap=16, relu=False, rank=0, world=1):
     wq = _codes(wq)
     bits = np.ascontiguousarray(bits, dtype=np.uint8)
     M = wq.shape[0]
@@ -385,22 +387,24 @@ def clear_fc_shift_acc(bits, K, w_in, in_signed, wq, cap=16, relu=False):
     out = np.zeros((M, w.value), dtype=np.uint8)
     st = she_circuit_stats()
     _check(lib().she_clear_fc_shift_acc(_np_ptr(bits), K, w_in, int(in_signed), _np_ptr(wq), M, cap,
-                                        int(relu), _np_ptr(out), ctypes.byref(w), ctypes.byref(st)))
+                                        int(relu), _np_ptr(out), ctypes.byref(w), rank, world,
+                                        ctypes.byref(st)))
     return out, w.value, st.as_dict()
 
 
-def clear_relu(bits, words, width):
+def clear_relu(bits, words, width, rank=0, world=1):
     bits = np.ascontiguousarray(bits, dtype=np.uint8)
     out = np.zeros((words, width - 1), dtype=np.uint8)
     st = she_circuit_stats()
-    _check(lib().she_clear_relu(_np_ptr(bits), words, width, _np_ptr(out), ctypes.byref(st)))
+    _check(lib().she_clear_relu(_np_ptr(bits), words, width, _np_ptr(out), rank, world,
+                                ctypes.byref(st)))
     return out, st.as_dict()
 
 
-def clear_maxpool2x2(bits, H, W, C, w, in_signed):
+def clear_maxpool2x2(bits, H, W, C, w, in_signed, rank=0, world=1):
     bits = np.ascontiguousarray(bits, dtype=np.uint8)
     out = np.zeros((H // 2, W // 2, C, w), dtype=np.uint8)
     st = she_circuit_stats()
     _check(lib().she_clear_maxpool2x2(_np_ptr(bits), H, W, C, w, int(in_signed), _np_ptr(out),
-                                      ctypes.byref(st)))
+                                      rank, world, ctypes.byref(st)))
     return out, st.as_dict()
