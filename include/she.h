@@ -202,6 +202,21 @@ she_status she_maxpool2x2(she_ctx* ctx, const uint32_t* in, int H, int W, int C,
 /* Gate / lane / level counters of the context's last layer call. */
 she_status she_ctx_layer_stats(she_ctx* ctx, she_circuit_stats* stats);
 
+/* Gate capture, for the seed-sampled ciphertext parity of the layer calls
+ * ("the oracle recomputes sampled gates from the exact input
+ * ciphertexts captured from the GPU's wire table").  While enabled (every > 0)
+ * each bootstrapped layer gate whose ordinal o (counted over every level of
+ * every layer call since this call) satisfies mix64(seed + o) % every == 0 is
+ * recorded, up to max_gates: its op, its three input slots exactly as the gate
+ * reads them (negation flags applied to the n+1 live words) and its output
+ * slot.  every == 0 disables capture and frees the buffer.  Capture makes the
+ * layer calls synchronous.  Test instrumentation, not part of the hot path. */
+she_status she_ctx_capture(she_ctx* ctx, uint64_t seed, uint32_t every, size_t max_gates);
+/* Copy the captured gates out (HOST buffers): ops[cap], slots[cap][4][stride]
+ * (a, b, c, out); *count = number recorded (<= cap copied). */
+she_status she_ctx_capture_read(she_ctx* ctx, uint8_t* ops, uint32_t* slots, size_t cap,
+                                size_t* count);
+
 /* Clear-bit backend: the same circuits evaluated on plaintext bits (uint8 per
  * bit, layouts as above without the stride axis), host only.  For testing the
  * scheduler and counting gates; stats may be NULL.  rank/world select the

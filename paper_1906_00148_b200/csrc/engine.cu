@@ -10,6 +10,7 @@
 // PAPER.md:31 (bootstrapping), :110 (gates), :188 (TFHE setting, key switching).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
@@ -84,6 +85,9 @@ __device__ __forceinline__ LaneForm lane_form(int op, int h) {
   return f;
 }
 
+// Instantiated blind-rotation launch shapes (G lanes per CTA, B CTAs per SM).
+#define SHE_BR_CONFIGS(X) X(5, 1) X(4, 1) X(3, 1) X(2, 2) X(1, 4)
+
 struct BRArgs {
   GateSrc src;
   const uint32_t* lanes;     // compact lane list: gate | h << 31
@@ -105,8 +109,8 @@ __device__ __forceinline__ void pair_sync(int id) {
 // they share the instruction stream and each BK_i load); warp roles per lane
 // as described in bootstrap_core.cuh.  No iteration is skipped (a~_i = 0
 // gives digits 0 and an exactly-zero update, R9), so all lanes stay in step.
-template <class S, int G>
-__global__ void __launch_bounds__(128 * G, 1) br_kernel(BRArgs args) {
+template <class S, int G, int B>
+__global__ void __launch_bounds__(128 * G, B) br_kernel(BRArgs args) {
   constexpr int N = S::N, L = S::L;
   constexpr int T = 128 * G;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -444,7 +448,10 @@ struct she_ctx {
   uint32_t* lane_buf = nullptr;  // compact lane list (+ count at [ext_lanes])
   size_t ext_lanes = 0;
   int sms = 148;
-  int br_lanes_per_cta = 4;  // G: lanes served in lock step by one persistent CTA
+  // blind-rotation launch shape: G lanes served in lock step by one persistent
+  // CTA of 128 G threads, B CTAs per SM (SHE_BR_CFG="GxB" selects another
+  // instantiated shape, see SHE_BR_CONFIGS)
+  int br_g = 5, br_b = 1;
   // staging for the host-buffer API
   uint8_t* h_ops = nullptr;
   uint32_t* h_io = nullptr;
@@ -465,6 +472,13 @@ struct she_ctx {
   std::vector<cudaEvent_t> ev_marks;  // triples: before BR, after BR, after KS
   double br_ms = 0, ks_ms = 0;
   uint64_t br_launches = 0, ks_launches = 0;
+  // gate capture (she_ctx_capture; test instrumentation)
+  uint32_t cap_every = 0;
+  uint64_t cap_seed = 0, cap_ordinal = 0;
+  size_t cap_max = 0, cap_count = 0;
+  uint32_t* cap_slots = nullptr;  // [cap_max][4][stride]
+  uint32_t* cap_lits = nullptr;   // device staging of the gather literals
+  std::vector<uint8_t> cap_ops;
 };
 
 namespace {
@@ -513,10 +527,11 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   cudaFree(d_bk32);
-  CK(cudaFuncSetAttribute(br_kernel<S, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)(4 * br::Lane<S>::bytes(p.n))));
-  CK(cudaFuncSetAttribute(br_kernel<S, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)(5 * br::Lane<S>::bytes(p.n))));
+#define SHE_BR_SMEM(G, B)                                                            \
+  CK(cudaFuncSetAttribute(br_kernel<S, G, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                          (int)(G * br::Lane<S>::bytes(p.n))));
+  SHE_BR_CONFIGS(SHE_BR_SMEM)
+#undef SHE_BR_SMEM
   return SHE_OK;
 }
 
@@ -552,12 +567,12 @@ cudaEvent_t mark(she_ctx* ctx, cudaStream_t stream) {
   return e;
 }
 
-template <class S, int G>
+template <class S, int G, int B>
 she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
   const size_t smem = G * br::Lane<S>::bytes(ctx->p.n);
   const size_t groups = (max_lanes + G - 1) / G;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(groups, ctx->sms)));
+  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(groups, (size_t)ctx->sms * B)));
   cfg.blockDim = dim3(128 * G);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -572,7 +587,7 @@ she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  CK(cudaLaunchKernelEx(&cfg, br_kernel<S, G>, a));
+  CK(cudaLaunchKernelEx(&cfg, br_kernel<S, G, B>, a));
   return SHE_OK;
 }
 
@@ -609,8 +624,11 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     a.ext_stride = ctx->ext_stride;
     a.geo = ctx->geo;
     if (ctx->timing) mark(ctx, stream);
-    st = ctx->br_lanes_per_cta == 5 ? launch_br<S, 5>(ctx, a, 2 * cnt, stream)
-                                    : launch_br<S, 4>(ctx, a, 2 * cnt, stream);
+    st = fail(SHE_ERR_STATE, "no blind-rotation kernel for config %dx%d", ctx->br_g, ctx->br_b);
+#define SHE_BR_LAUNCH(G, B) \
+    if (ctx->br_g == G && ctx->br_b == B) st = launch_br<S, G, B>(ctx, a, 2 * cnt, stream);
+    SHE_BR_CONFIGS(SHE_BR_LAUNCH)
+#undef SHE_BR_LAUNCH
     if (st != SHE_OK) return st;
     if (ctx->timing) mark(ctx, stream);
 
@@ -660,7 +678,20 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
   ctx->stride = (uint32_t)lwe_stride(*p);
   ctx->ext_stride = (p->N + 1 + 31) / 32 * 32;
   cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
-  if (const char* e = getenv("SHE_BR_LANES_PER_CTA")) ctx->br_lanes_per_cta = atoi(e) == 5 ? 5 : 4;
+  if (const char* e = getenv("SHE_BR_CFG")) {
+    int g = 0, b = 0;
+    bool ok = sscanf(e, "%dx%d", &g, &b) == 2;
+    bool known = false;
+#define SHE_BR_KNOWN(G, B) known = known || (g == G && b == B);
+    SHE_BR_CONFIGS(SHE_BR_KNOWN)
+#undef SHE_BR_KNOWN
+    if (!ok || !known) {
+      delete ctx;
+      return fail(SHE_ERR_ARG, "SHE_BR_CFG=%s is not an instantiated GxB shape", e);
+    }
+    ctx->br_g = g;
+    ctx->br_b = b;
+  }
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
     she_ctx_destroy(ctx);
@@ -713,6 +744,8 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaFree(ctx->table);
   cudaFree(ctx->prog_dev);
   cudaFreeHost(ctx->prog_host);
+  cudaFree(ctx->cap_slots);
+  cudaFree(ctx->cap_lits);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev_marks) cudaEventDestroy(e);
   delete ctx;
@@ -872,6 +905,44 @@ she_status she_gate_batch_ops_host(she_ctx* ctx, const uint8_t* ops, const uint3
   return SHE_OK;
 }
 
+she_status she_ctx_capture(she_ctx* ctx, uint64_t seed, uint32_t every, size_t max_gates) {
+  if (!ctx) return fail(SHE_ERR_ARG, "NULL context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  cudaFree(ctx->cap_slots);
+  cudaFree(ctx->cap_lits);
+  ctx->cap_slots = ctx->cap_lits = nullptr;
+  ctx->cap_every = 0;
+  ctx->cap_max = ctx->cap_count = 0;
+  ctx->cap_ordinal = 0;
+  ctx->cap_ops.clear();
+  if (every == 0 || max_gates == 0) return SHE_OK;
+  CK(cudaMalloc(&ctx->cap_slots, max_gates * 4 * ctx->stride * 4));
+  CK(cudaMemset(ctx->cap_slots, 0, max_gates * 4 * ctx->stride * 4));
+  CK(cudaMalloc(&ctx->cap_lits, max_gates * 3 * 4));
+  ctx->cap_every = every;
+  ctx->cap_seed = seed;
+  ctx->cap_max = max_gates;
+  return SHE_OK;
+}
+
+she_status she_ctx_capture_read(she_ctx* ctx, uint8_t* ops, uint32_t* slots, size_t cap,
+                                size_t* count) {
+  if (!ctx || !count) return fail(SHE_ERR_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  *count = ctx->cap_count;
+  const size_t m = std::min(cap, ctx->cap_count);
+  if (m && (!ops || !slots)) return fail(SHE_ERR_ARG, "NULL buffer");
+  if (m) {
+    memcpy(ops, ctx->cap_ops.data(), m);
+    CK(cudaMemcpy(slots, ctx->cap_slots, m * 4 * ctx->stride * 4, cudaMemcpyDeviceToHost));
+  }
+  return SHE_OK;
+}
+
 she_status she_gate_level(she_ctx* ctx, uint32_t* wires, const uint8_t* ops, const uint32_t* in,
                           const uint32_t* out_idx, size_t count, void* stream) {
   if (count == 0) return SHE_OK;
@@ -902,6 +973,43 @@ int engine_world(const she_ctx* ctx) { return ctx->world; }
 she_circuit_stats* engine_stats(she_ctx* ctx, bool reset) {
   if (reset) ctx->stats = she_circuit_stats{};
   return &ctx->stats;
+}
+
+// Test instrumentation (she_ctx_capture): SplitMix64 finaliser for sampling.
+static uint64_t capture_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Copy the input slots (before = true: a, b, c with negation applied, as the
+// gate reads them) or the output slot of the picked gates into the capture
+// buffer.  Synchronous: the literal staging vector is host memory.
+static she_status capture_slots(she_ctx* ctx, const sched::Program& p,
+                                const std::vector<uint32_t>& pick, bool before,
+                                cudaStream_t stream) {
+  const size_t base = ctx->cap_count;
+  std::vector<uint32_t> lits;
+  for (uint32_t q : pick)
+    for (int j = 0; j < (before ? 3 : 1); ++j) lits.push_back(before ? p.ins[3 * (size_t)q + j] : p.outs[q]);
+  CK(cudaMemcpyAsync(ctx->cap_lits, lits.data(), lits.size() * 4, cudaMemcpyHostToDevice, stream));
+  // gather_kernel writes slot o at dst[(dst_first + o) * stride]; one launch per role j
+  for (size_t k = 0; k < pick.size(); ++k) {
+    const int roles = before ? 3 : 1;
+    for (int j = 0; j < roles; ++j) {
+      const size_t dst_slot = (base + k) * 4 + (before ? j : 3);
+      gather_kernel<<<1, 128, 0, stream>>>(ctx->cap_slots, dst_slot, ctx->table,
+                                           ctx->cap_lits + k * roles + j, ctx->stride, ctx->p.n);
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(stream));
+  if (before)
+    for (uint32_t q : pick) ctx->cap_ops.push_back(p.ops[q]);
+  else
+    ctx->cap_count += pick.size();
+  return SHE_OK;
 }
 
 she_status engine_run_program(she_ctx* ctx, const sched::Program& p, const uint32_t* in,
@@ -964,8 +1072,23 @@ she_status engine_run_program(she_ctx* ctx, const sched::Program& p, const uint3
     s.out_idx = d_outs + b;
     s.stride = ctx->stride;
     s.count = e - b;
+    std::vector<uint32_t> pick;  // captured gates of this level: index in the level
+    if (ctx->cap_every) {
+      for (uint32_t q = b; q < e && ctx->cap_count + pick.size() < ctx->cap_max; ++q)
+        if (capture_mix(ctx->cap_seed + ctx->cap_ordinal + (q - b)) % ctx->cap_every == 0)
+          pick.push_back(q);
+      ctx->cap_ordinal += e - b;
+      if (!pick.empty()) {
+        she_status cs = capture_slots(ctx, p, pick, true, stream);
+        if (cs != SHE_OK) return cs;
+      }
+    }
     she_status st = dispatch(ctx, s, stream);
     if (st != SHE_OK) return st;
+    if (!pick.empty()) {
+      she_status cs = capture_slots(ctx, p, pick, false, stream);
+      if (cs != SHE_OK) return cs;
+    }
   }
   if (O) gather_kernel<<<(unsigned)O, 128, 0, stream>>>(out, out_first, ctx->table, d_outl,
                                                         ctx->stride, n);

@@ -95,6 +95,8 @@ def lib() -> ctypes.CDLL:
             "she_relu": ([_vp, _vp, _sz, ctypes.c_int, _vp, _vp], ctypes.c_int),
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
+            "she_ctx_capture": ([_vp, ctypes.c_uint64, ctypes.c_uint32, _sz], ctypes.c_int),
+            "she_ctx_capture_read": ([_vp, _vp, _vp, _sz, ctypes.POINTER(_sz)], ctypes.c_int),
             "she_clear_conv_shift_acc": ([_vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
                                          + [_vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int,
                                             ctypes.c_int, ctypes.POINTER(she_circuit_stats)],
@@ -359,6 +361,21 @@ def layer_stats(ctx: Context) -> dict:
     st = she_circuit_stats()
     _check(lib().she_ctx_layer_stats(ctx.handle, ctypes.byref(st)))
     return st.as_dict()
+
+
+def capture(ctx: Context, seed: int, every: int, max_gates: int) -> None:
+    """Sample layer gates for ciphertext parity (test instrumentation, she.h)."""
+    _check(lib().she_ctx_capture(ctx.handle, seed, every, max_gates))
+
+
+def capture_read(ctx: Context, cap: int):
+    """-> (ops uint8[k], slots uint32[k][4][stride]: a, b, c as read, out)."""
+    ops = np.zeros(max(cap, 1), np.uint8)
+    slots = np.zeros((max(cap, 1), 4, ctx.stride), np.uint32)
+    n = ctypes.c_size_t(0)
+    _check(lib().she_ctx_capture_read(ctx.handle, _np_ptr(ops), _np_ptr(slots), cap, ctypes.byref(n)))
+    k = min(n.value, cap)
+    return ops[:k], slots[:k]
 
 
 # ---- clear-bit backend (host bits; scheduler tests and gate counts) -------------
