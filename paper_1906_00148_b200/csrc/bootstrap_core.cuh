@@ -12,7 +12,8 @@
 //   pointwise all threads of the CTA, BK_i read once per CTA for all lanes;
 //   inverse   warps (2c, 2c+1) split the inverse NTT of output component c:
 //             thread (H, lane) holds half of a 32-point column, the last
-//             butterfly stage exchanges L/4 values through shared memory.
+//             butterfly stage exchanges L/4 values through shared memory
+//             (decimation-in-time CT butterflies, ntt.cuh).
 //
 // Shared memory of one lane:
 //   acc  : uint32[2][N]          the TRLWE accumulator (A, B), torus32
@@ -57,11 +58,12 @@ struct Lane {
 
 // ---- forward path of row w ------------------------------------------------
 
-// Load: digit polynomial of row w of D = X^a ACC - ACC, column j1 = lane.
+// Load: digit polynomial of row w of D = X^a ACC - ACC, column j1 = lane, as
+// small signed integers (|digit| <= Bg/2).
 template <class S>
 __host__ __device__ __forceinline__ void load_digits(const Geometry& g, int w, int lane,
                                                      const uint32_t* acc, uint32_t a,
-                                                     uint64_t (&x)[S::L]) {
+                                                     int32_t (&d)[S::L]) {
   constexpr int L = S::L, N = S::N;
   const int c = w / g.l, j = w % g.l;
   const uint32_t* P = acc + c * N;
@@ -74,8 +76,7 @@ __host__ __device__ __forceinline__ void load_digits(const Geometry& g, int w, i
     uint32_t v = P[idx & (N - 1)];
     if (idx >= (uint32_t)N) v = 0u - v;
     const uint32_t y = v - P[m] + g.dec_offset;
-    const int32_t d = (int32_t)((y >> shift) & mask) - (int32_t)half;
-    x[j2] = gl::from_i64(d);
+    d[j2] = (int32_t)((y >> shift) & mask) - (int32_t)half;
   }
 }
 
@@ -85,6 +86,26 @@ __host__ __device__ __forceinline__ void fwd_pass1_store(int lane, uint64_t (&x)
                                                          uint64_t* row) {
   constexpr int L = S::L;
   ntt::fwd<L, S::SH, true>(x);
+#pragma unroll
+  for (int q = 0; q < L; ++q) row[ntt::brev(q, ntt::ilog2(L)) * (L + 1) + lane] = x[q];
+}
+
+// Pass 1 of a digit polynomial: stage 0 (pairs j, j + L/2, twiddle theta^(L/2)
+// = 2^48) is exact in int64 because the digits are small (|d| 2^48 < 2^57), so
+// it needs no modular reduction; the field elements enter at stage 1.
+template <class S>
+__host__ __device__ __forceinline__ void fwd_pass1_digits_store(int lane, const int32_t (&d)[S::L],
+                                                                uint64_t* row) {
+  constexpr int L = S::L;
+  static_assert(ntt::stage_shift<true>(L, S::SH, 0, 0) == 48, "stage-0 twiddle is 2^48");
+  uint64_t x[L];
+#pragma unroll
+  for (int j = 0; j < L / 2; ++j) {
+    const int64_t u = d[j], t = (int64_t)d[j + L / 2] * (int64_t(1) << 48);
+    x[j] = gl::from_i64(u + t);
+    x[j + L / 2] = gl::from_i64(u - t);
+  }
+  ntt::fwd<L, S::SH, true, 1>(x);
 #pragma unroll
   for (int q = 0; q < L; ++q) row[ntt::brev(q, ntt::ilog2(L)) * (L + 1) + lane] = x[q];
 }
@@ -139,7 +160,7 @@ __host__ __device__ __forceinline__ void inv_a_load(int i, const uint64_t* row, 
 template <class S, int H, bool NEGA>
 __host__ __device__ __forceinline__ void inv_stages_send(int lane, uint64_t (&y)[S::L / 2], uint64_t* xbuf) {
   constexpr int L = S::L;
-  ntt::inv_half<L, (NEGA ? S::SH : S::SH2), NEGA, H>(y);
+  ntt::inv_dit_half<L, S::SH2>(y);  // both passes: inverse cyclic, omega = theta^2 = 2^SH2
   // H = 0 sends its lo values for j in [L/4, L/2); H = 1 its hi values for j < L/4
 #pragma unroll
   for (int m = 0; m < L / 4; ++m) xbuf[(H * (L / 4) + m) * L + lane] = y[(H == 0 ? L / 4 : 0) + m];
@@ -162,7 +183,7 @@ __host__ __device__ __forceinline__ void inv_recv_cross(int lane, const uint64_t
       hi[m] = y[L / 4 + m];
     }
   }
-  ntt::inv_cross<L, (NEGA ? S::SH : S::SH2), NEGA>(lo, hi);
+  ntt::inv_dit_cross<L, S::SH2, H>(lo, hi);
 }
 
 // After pass A: untwist and store transposed (thread row i; outputs j1 =
@@ -188,7 +209,14 @@ __host__ __device__ __forceinline__ void inv_b_load(int j1, const uint64_t* row,
   for (int m = 0; m < L / 2; ++m) y[m] = row[ntt::brev(H * (L / 2) + m, ntt::ilog2(L)) * (L + 1) + j1];
 }
 
-// After pass B: lift mod 2^32 and ACC_c += result (coefficients j1 + L j2).
+// After pass B: the negacyclic post-twist theta^(-j2) = -2^(96 - SH j2) (a
+// shift, j2 > 0), the centred lift mod 2^32 and ACC_c += result (coefficients
+// j1 + L j2).
+template <class S>
+__host__ __device__ __forceinline__ uint32_t twist_lift(uint64_t x, int j2) {
+  if (j2 == 0) return gl::lift32(x);
+  return gl::lift32_neg(gl::shl_le(x, 96 - S::SH * j2));
+}
 template <class S, int H>
 __host__ __device__ __forceinline__ void inv_b_acc(int j1, const uint64_t (&lo)[S::L / 4],
                                                    const uint64_t (&hi)[S::L / 4], uint32_t* accc) {
@@ -196,8 +224,8 @@ __host__ __device__ __forceinline__ void inv_b_acc(int j1, const uint64_t (&lo)[
 #pragma unroll
   for (int m = 0; m < L / 4; ++m) {
     const int j2 = H * (L / 4) + m;
-    accc[j1 + L * j2] += gl::lift32(lo[m]);
-    accc[j1 + L * (j2 + L / 2)] += gl::lift32(hi[m]);
+    accc[j1 + L * j2] += twist_lift<S>(lo[m], j2);
+    accc[j1 + L * (j2 + L / 2)] += twist_lift<S>(hi[m], j2 + L / 2);
   }
 }
 

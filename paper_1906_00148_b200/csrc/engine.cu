@@ -160,8 +160,9 @@ __global__ void __launch_bounds__(128 * G, B) br_kernel(BRArgs args) {
         uint64_t* row = me.row(w);
         uint64_t x[L];
         if (active_lane) {
-          br::load_digits<S>(geo, w, lane, me.acc, me.abar[i], x);
-          br::fwd_pass1_store<S>(lane, x, row);
+          int32_t d[L];
+          br::load_digits<S>(geo, w, lane, me.acc, me.abar[i], d);
+          br::fwd_pass1_digits_store<S>(lane, d, row);
         }
         __syncwarp();
         if (active_lane) br::fwd_pass2_load<S>(lane, row, args.tw, x);

@@ -207,6 +207,141 @@ __host__ __device__ __forceinline__ uint64_t mul_pow2(uint64_t x, int s) {
   return s >= 96 ? neg(mul_pow2_pos(x, s - 96)) : mul_pow2_pos(x, s);
 }
 
+// ---- butterfly primitives with a bounded twiddle product ----
+// The NTT butterflies compute u +- t with t = v 2^s.  If the twiddle product
+// is kept <= p (not merely < 2^64), one carry (borrow) fold is always enough:
+//   u + t <= 2^64 - 1 + p: after a carry, u + t - 2^64 <= p - 1, + EPS < 2^64;
+//   u - t >= -p:           after a borrow, u - t + 2^64 >= EPS, - EPS >= 0.
+// shl_le() produces such a product from any 64-bit v.
+
+// x + y for any x and y <= p (lazy result).
+__host__ __device__ __forceinline__ uint64_t add_le(uint64_t x, uint64_t y) {
+#if defined(__CUDA_ARCH__)
+  uint32_t s0, s1, c;
+  asm("add.cc.u32 %0, %3, %5;\n\t"
+      "addc.cc.u32 %1, %4, %6;\n\t"
+      "addc.u32 %2, 0, 0;\n\t"
+      "mad.lo.cc.u32 %0, %2, 0xFFFFFFFF, %0;\n\t"
+      "madc.hi.u32 %1, %2, 0xFFFFFFFF, %1;"
+      : "=&r"(s0), "=&r"(s1), "=&r"(c)
+      : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32)));
+  return ((uint64_t)s1 << 32) | s0;
+#else
+  const uint64_t s = x + y;
+  return s < y ? s + EPS : s;
+#endif
+}
+
+// x - y for any x and y <= p (lazy result).
+__host__ __device__ __forceinline__ uint64_t sub_le(uint64_t x, uint64_t y) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d0, d1, bw;
+  asm("sub.cc.u32 %0, %3, %5;\n\t"
+      "subc.cc.u32 %1, %4, %6;\n\t"
+      "subc.u32 %2, 0, 0;\n\t"
+      "sub.cc.u32 %0, %0, %2;\n\t"
+      "subc.u32 %1, %1, 0;"
+      : "=&r"(d0), "=&r"(d1), "=&r"(bw)
+      : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32)));
+  return ((uint64_t)d1 << 32) | d0;
+#else
+  const uint64_t d = x - y;
+  return x < y ? d - EPS : d;
+#endif
+}
+
+// v 2^s mod p for a compile-time 0 <= s < 96 and any 64-bit v; result <= p.
+// With r = s mod 32, T = v 2^r = (T2:T1:T0) (T2 < 2^r) and 2^64 = 2^32 - 1,
+// 2^96 = -1 (mod p):
+//   s <  32: T            = (T1:T0) + T2 EPS.  w = (T1:T0) + (T2+1) EPS with
+//            carry c; result c ? w : w - EPS  (c: w < 2^31 EPS < p; !c: w - EPS
+//            < 2^64 - EPS = p).
+//   s <  64: T 2^32       = (T0 + T1) 2^32 - (T1 + T2).  With T0 + T1 = s1 2^32
+//            + s0: = (s0 + s1) 2^32 - (T1 + T2 + s1), H = s0 + s1 < 2^32; R =
+//            (H:0) - E lies in [-2^33, 2^64 - 2^32]: add p once if negative.
+//   s <  96: T 2^64       = (T0 - T2) 2^32 - (T0 + T1) in (-2^64, 2^64 - 2^32]:
+//            add p once if negative (borrow of T0 - T2 or of the 64-bit sub;
+//            never both).
+// Verified exhaustively on edge values and randomly in tests (host build).
+__host__ __device__ __forceinline__ uint64_t shl_le(uint64_t v, const int s) {
+  const int q = s >> 5, r = s & 31;
+  const uint32_t v0 = (uint32_t)v, v1 = (uint32_t)(v >> 32);
+  uint32_t T0, T1, T2;
+  if (r == 0) {
+    T0 = v0;
+    T1 = v1;
+    T2 = 0;
+  } else {
+    T0 = v0 << r;
+#if defined(__CUDA_ARCH__)
+    T1 = __funnelshift_l(v0, v1, r);
+#else
+    T1 = (v1 << r) | (v0 >> (32 - r));
+#endif
+    T2 = v1 >> (32 - r);
+  }
+#if defined(__CUDA_ARCH__)
+  uint32_t o0, o1;
+  if (q == 0) {
+    uint32_t w0, w1, c, e0, e1;
+    asm("mad.lo.cc.u32 %0, %5, 0xFFFFFFFF, %6;\n\t"
+        "madc.hi.cc.u32 %1, %5, 0xFFFFFFFF, %7;\n\t"
+        "addc.u32 %2, 0, 0;\n\t"
+        "add.cc.u32 %3, %0, 1;\n\t"
+        "addc.u32 %4, %1, 0xFFFFFFFF;"
+        : "=&r"(w0), "=&r"(w1), "=&r"(c), "=&r"(e0), "=&r"(e1)
+        : "r"(T2 + 1), "r"(T0), "r"(T1));
+    o0 = c ? w0 : e0;
+    o1 = c ? w1 : e1;
+  } else if (q == 1) {
+    uint32_t s0, H, e0, e1;
+    asm("add.cc.u32 %1, %5, %6;\n\t"     // s0 = T0 + T1, CF = s1
+        "addc.u32 %2, %1, 0;\n\t"        // H = s0 + s1
+        "addc.cc.u32 %3, %6, %7;\n\t"    // e0 = T1 + T2 + s1, CF = e1
+        "addc.u32 %4, 0, 0;\n\t"         // e1
+        "sub.cc.u32 %0, 0, %3;\n\t"      // R = (H:0) - (e1:e0)
+        "subc.cc.u32 %1, %2, %4;\n\t"
+        "subc.u32 %4, 0, 0;\n\t"         // -borrow
+        "sub.cc.u32 %0, %0, %4;\n\t"     // R + p if negative (- EPS mod 2^64)
+        "subc.u32 %1, %1, 0;"
+        : "=&r"(o0), "=&r"(s0), "=&r"(H), "=&r"(e0), "=&r"(e1)
+        : "r"(T0), "r"(T1), "r"(T2));
+    o1 = s0;
+  } else {
+    uint32_t F, fn, g0, g1;
+    asm("sub.cc.u32 %2, %6, %8;\n\t"     // F = T0 - T2, CF = borrow
+        "subc.u32 %3, 0, 0;\n\t"         // fn = -borrow
+        "add.cc.u32 %4, %6, %7;\n\t"     // G = T0 + T1
+        "addc.u32 %5, 0, 0;\n\t"
+        "sub.cc.u32 %0, 0, %4;\n\t"      // L = (F:0) - G
+        "subc.cc.u32 %1, %2, %5;\n\t"
+        "subc.u32 %3, %3, 0;\n\t"        // -(borrow_F + borrow_L), at most one is set
+        "sub.cc.u32 %0, %0, %3;\n\t"
+        "subc.u32 %1, %1, 0;"
+        : "=&r"(o0), "=&r"(o1), "=&r"(F), "=&r"(fn), "=&r"(g0), "=&r"(g1)
+        : "r"(T0), "r"(T1), "r"(T2));
+  }
+  return ((uint64_t)o1 << 32) | o0;
+#else
+  if (q == 0) {
+    const uint64_t m = (uint64_t)(T2 + 1) * EPS;
+    const uint64_t w = (((uint64_t)T1 << 32) | T0) + m;
+    return w < m ? w : w - EPS;
+  }
+  if (q == 1) {
+    const uint64_t S = (uint64_t)T0 + T1;
+    const uint32_t s0 = (uint32_t)S, s1 = (uint32_t)(S >> 32);
+    const uint64_t H = (uint64_t)(s0 + s1) << 32;
+    const uint64_t E = (uint64_t)T1 + T2 + s1;
+    return H < E ? H - E - EPS : H - E;
+  }
+  const uint64_t Hh = (uint64_t)(uint32_t)(T0 - T2) << 32;
+  const uint64_t G = (uint64_t)T0 + T1;
+  const uint64_t Lv = Hh - G;
+  return (T0 < T2 || Hh < G) ? Lv - EPS : Lv;
+#endif
+}
+
 __host__ __device__ inline uint64_t pow(uint64_t b, uint64_t e) {
   uint64_t r = 1;
   while (e) {
@@ -259,6 +394,12 @@ __host__ __device__ __forceinline__ uint64_t from_i64(int64_t v) {
 __host__ __device__ __forceinline__ uint32_t lift32(uint64_t x) {
   x = canon(x);
   return (uint32_t)x - (x > (P - 1) / 2 ? 1u : 0u);
+}
+
+// lift32(-t) for t <= p: (p - t) centred and reduced mod 2^32.  p = 1 mod 2^32,
+// and p - t > (p-1)/2 exactly when t < (p+1)/2 (t = 0 and t = p both give 0).
+__host__ __device__ __forceinline__ uint32_t lift32_neg(uint64_t t) {
+  return (0u - (uint32_t)t) + (t >= (P + 1) / 2 ? 1u : 0u);
 }
 
 }  // namespace gl

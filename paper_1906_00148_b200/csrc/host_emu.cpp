@@ -87,6 +87,9 @@ void inverse_component(Emu<S>& E, br::Lane<S>& ln, int c, uint32_t* accc) {
 }
 
 template <class S>
+void pass2_row(Emu<S>& E, uint64_t* row);
+
+template <class S>
 void forward_row(Emu<S>& E, br::Lane<S>& ln, int w, const uint64_t (*xs)[S::L]) {
   constexpr int L = S::L;
   uint64_t* row = ln.row(w);
@@ -95,6 +98,13 @@ void forward_row(Emu<S>& E, br::Lane<S>& ln, int w, const uint64_t (*xs)[S::L]) 
     memcpy(x, xs[lane], sizeof(x));
     br::fwd_pass1_store<S>(lane, x, row);
   }
+  pass2_row<S>(E, row);
+}
+
+// Pass 2 of a row: every thread loads (with the twist) before any stores.
+template <class S>
+void pass2_row(Emu<S>& E, uint64_t* row) {
+  constexpr int L = S::L;
   std::vector<uint64_t> regs((size_t)L * L);
   for (int lane = 0; lane < L; ++lane) {
     uint64_t y[L];
@@ -125,12 +135,13 @@ void blind_rotate(const br::Geometry& g, const uint64_t* bk_ntt, const uint32_t*
   for (uint32_t i = 0; i < g.n; ++i) {
     const uint32_t a = ln.abar[i];  // no skip: the device runs a = 0 as well
     for (int w = 0; w < 4; ++w) {
-      for (int lane = 0; lane < L; ++lane) {
-        uint64_t x[L];
-        br::load_digits<S>(g, w, lane, ln.acc, a, x);
-        memcpy(&xs[lane * L], x, sizeof(x));
+      uint64_t* row = ln.row(w);
+      for (int lane = 0; lane < L; ++lane) {  // digits + exact stage 0, as on the device
+        int32_t d[L];
+        br::load_digits<S>(g, w, lane, ln.acc, a, d);
+        br::fwd_pass1_digits_store<S>(lane, d, row);
       }
-      forward_row<S>(E, ln, w, reinterpret_cast<const uint64_t(*)[L]>(xs.data()));
+      pass2_row<S>(E, row);
     }
     const uint64_t* bki = bk_ntt + (size_t)i * 8 * N;
     for (int p = 0; p < N; ++p) {
@@ -216,4 +227,10 @@ uint64_t she_emu_gl_mul(uint64_t a, uint64_t b) { return gl::canon(gl::mul(a, b)
 uint64_t she_emu_gl_mul_pow2(uint64_t a, int s) { return gl::canon(gl::mul_pow2(a, s)); }
 uint64_t she_emu_gl_add(uint64_t a, uint64_t b) { return gl::canon(gl::add(a, b)); }
 uint64_t she_emu_gl_sub(uint64_t a, uint64_t b) { return gl::canon(gl::sub(a, b)); }
+// Bounded-product butterfly primitives: raw (non-canonical) results, so the
+// tests can check the <= p bound as well as the residue.
+uint64_t she_emu_gl_shl_le(uint64_t v, int s) { return gl::shl_le(v, s); }
+uint64_t she_emu_gl_add_le(uint64_t a, uint64_t b) { return gl::add_le(a, b); }
+uint64_t she_emu_gl_sub_le(uint64_t a, uint64_t b) { return gl::sub_le(a, b); }
+uint32_t she_emu_gl_lift32_neg(uint64_t t) { return gl::lift32_neg(t); }
 }

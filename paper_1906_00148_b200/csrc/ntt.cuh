@@ -15,8 +15,10 @@
 // Only the twist is a general multiplication: L*L - (2L-1) modmuls per
 // transform instead of (N/2) log2 N for a radix-2 transform.
 //
-// The inverse runs the exact reverse (Gentleman-Sande butterflies, inverse
-// twiddles) and is unscaled: N^-1 is folded into the bootstrapping key.
+// The inverse runs both passes as inverse cyclic transforms by decimation in
+// time (CT butterflies again, bit-reversed in, natural out); the negacyclic
+// pass is then finished by the post-twist theta^(-j2) (a shift), merged into
+// the final lift.  It is unscaled: N^-1 is folded into the bootstrapping key.
 #pragma once
 #include "gl64.cuh"
 
@@ -29,32 +31,29 @@ __host__ __device__ constexpr int brev(int x, int bits) {
 }
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 
-// t = x * 2^s for a compile-time shift s in [0, 192): returns x * 2^(s mod 96)
-// and reports the sign (2^96 = -1) so butterflies swap add/sub instead of
-// negating.
-__host__ __device__ __forceinline__ uint64_t shift_twiddle(uint64_t x, int s, bool& negative) {
-  negative = s >= 96;
-  return gl::mul_pow2_pos(x, negative ? s - 96 : s);
-}
-
-// CT butterfly (lo, hi) <- (lo + w hi, lo - w hi), w = 2^s.
+// CT butterfly (lo, hi) <- (lo + w hi, lo - w hi), w = 2^s, s compile-time in
+// [0, 192).  w = -2^(s-96) for s >= 96: the sum and difference swap.  The
+// twiddle product is formed <= p (gl::shl_le) so that the sum and difference
+// need a single fold each (gl::add_le / sub_le); for w = +-1 the operand is
+// lazy and the double-fold add / sub are used.
 __host__ __device__ __forceinline__ void ct_bfly(uint64_t& lo, uint64_t& hi, int s) {
-  bool ng;
-  const uint64_t t = shift_twiddle(hi, s, ng);
+  const bool ng = s >= 96;
+  const int sp = ng ? s - 96 : s;
   const uint64_t u = lo;
-  lo = ng ? gl::sub(u, t) : gl::add(u, t);
-  hi = ng ? gl::add(u, t) : gl::sub(u, t);
+  uint64_t a, b;
+  if (sp == 0) {
+    a = gl::add(u, hi);
+    b = gl::sub(u, hi);
+  } else {
+    const uint64_t t = gl::shl_le(hi, sp);
+    a = gl::add_le(u, t);
+    b = gl::sub_le(u, t);
+  }
+  lo = ng ? b : a;
+  hi = ng ? a : b;
 }
 
-// GS butterfly (lo, hi) <- (lo + hi, (lo - hi) w), w = 2^s; for w = -2^(s-96)
-// the difference is taken the other way round instead of negating.
-__host__ __device__ __forceinline__ void gs_bfly(uint64_t& lo, uint64_t& hi, int s) {
-  const uint64_t u = lo, v = hi;
-  lo = gl::add(u, v);
-  hi = s >= 96 ? gl::mul_pow2_pos(gl::sub(v, u), s - 96) : gl::mul_pow2_pos(gl::sub(u, v), s);
-}
-
-// Twiddle shift of block b at stage k of a length-L transform.
+// Twiddle shift of block b at stage k of a length-L forward transform.
 //   negacyclic (theta = 2^SH, order 2L): theta^((2 brev_k(b) + 1) L / 2^(k+1))
 //   cyclic     (omega = 2^SH, order L) : omega^(brev_k(b) L / 2^(k+1))
 template <bool NEGA>
@@ -62,16 +61,16 @@ __host__ __device__ constexpr int stage_shift(int L, int SH, int k, int b) {
   return NEGA ? (SH * (2 * brev(b, k) + 1) * (L >> (k + 1))) % 192
               : (SH * brev(b, k) * (L >> (k + 1))) % 192;
 }
-__host__ __device__ constexpr int inv_shift(int s) { return (192 - s) % 192; }
 
-// Forward length-L transform in registers (CT, natural in, bit-reversed out).
+// Forward length-L transform in registers (CT, natural in, bit-reversed out),
+// stages K0 .. log2 L - 1.
 //   NEGA: a[q] = sum_j a_j theta^((2 brev(q) + 1) j)
 //   cyc : a[q] = sum_j a_j omega^(brev(q) j)
-template <int L, int SH, bool NEGA>
+template <int L, int SH, bool NEGA, int K0 = 0>
 __host__ __device__ __forceinline__ void fwd(uint64_t (&a)[L]) {
   constexpr int LG = ilog2(L);
 #pragma unroll
-  for (int k = 0; k < LG; ++k) {
+  for (int k = K0; k < LG; ++k) {
     const int len = L >> (k + 1);
 #pragma unroll
     for (int b = 0; b < (1 << k); ++b) {
@@ -82,49 +81,45 @@ __host__ __device__ __forceinline__ void fwd(uint64_t (&a)[L]) {
   }
 }
 
-// Exact inverse of fwd up to the factor L (GS, bit-reversed in, natural out).
-template <int L, int SH, bool NEGA>
-__host__ __device__ __forceinline__ void inv(uint64_t (&a)[L]) {
-  constexpr int LG = ilog2(L);
+// Inverse cyclic transform by decimation in time (CT butterflies, bit-reversed
+// in, natural out), unscaled:  in a[q] = X[brev(q)],  out a[j] = sum_m X[m]
+// omega^(-m j), omega = 2^SH2 of order L.  Stage h (half-size 1, 2, .., L/2),
+// position j < h in its block: twiddle omega^(-j L / 2h).
+__host__ __device__ constexpr int dit_shift(int L, int SH2, int h, int j) {
+  return (192 - (SH2 * j * (L / (2 * h))) % 192) % 192;
+}
+template <int L, int SH2>
+__host__ __device__ __forceinline__ void inv_dit(uint64_t (&a)[L]) {
 #pragma unroll
-  for (int k = LG - 1; k >= 0; --k) {
-    const int len = L >> (k + 1);
+  for (int h = 1; h < L; h *= 2) {
 #pragma unroll
-    for (int b = 0; b < (1 << k); ++b) {
-      const int s = inv_shift(stage_shift<NEGA>(L, SH, k, b));
+    for (int blk = 0; blk < L; blk += 2 * h) {
 #pragma unroll
-      for (int j = 0; j < len; ++j) gs_bfly(a[b * 2 * len + j], a[b * 2 * len + j + len], s);
+      for (int j = 0; j < h; ++j) ct_bfly(a[blk + j], a[blk + j + h], dit_shift(L, SH2, h, j));
     }
   }
 }
 
-// The inverse split over two threads H = 0, 1 holding halves a[H L/2 + m]:
-// stages k = LG-1 .. 1 never cross the halves ...
-template <int L, int SH, bool NEGA, int H>
-__host__ __device__ __forceinline__ void inv_half(uint64_t (&a)[L / 2]) {
-  constexpr int LG = ilog2(L);
+// The same transform split over two threads H = 0, 1 holding halves
+// a[H L/2 + m]: stages h = 1 .. L/4 stay inside a half ...
+template <int L, int SH2>
+__host__ __device__ __forceinline__ void inv_dit_half(uint64_t (&a)[L / 2]) {
 #pragma unroll
-  for (int k = LG - 1; k >= 1; --k) {
-    const int len = L >> (k + 1);
-    const int nb = 1 << (k - 1);  // blocks per half
+  for (int h = 1; h < L / 2; h *= 2) {
 #pragma unroll
-    for (int bb = 0; bb < nb; ++bb) {
-      const int b = H * nb + bb;
-      const int s = inv_shift(stage_shift<NEGA>(L, SH, k, b));
+    for (int blk = 0; blk < L / 2; blk += 2 * h) {
 #pragma unroll
-      for (int j = 0; j < len; ++j) gs_bfly(a[bb * 2 * len + j], a[bb * 2 * len + j + len], s);
+      for (int j = 0; j < h; ++j) ct_bfly(a[blk + j], a[blk + j + h], dit_shift(L, SH2, h, j));
     }
   }
 }
-// ... and stage 0 pairs element j with j + L/2 (one twiddle for all j).
-// Thread H computes the butterflies j in [H L/4, (H+1) L/4): it keeps u (H=0)
-// or v (H=1) for those j and receives the other operand from its partner.
-// On return lo[m] = out[H L/4 + m], hi[m] = out[H L/4 + m + L/2].
-template <int L, int SH, bool NEGA>
-__host__ __device__ __forceinline__ void inv_cross(uint64_t (&lo)[L / 4], uint64_t (&hi)[L / 4]) {
-  const int s = inv_shift(stage_shift<NEGA>(L, SH, 0, 0));
+// ... and the last stage pairs j with j + L/2 (twiddle omega^-j).  Thread H
+// computes the butterflies j in [H L/4, (H+1) L/4) from u = a[j] and
+// v = a[j + L/2]; on return lo[m] = out[H L/4 + m], hi[m] = out[H L/4 + m + L/2].
+template <int L, int SH2, int H>
+__host__ __device__ __forceinline__ void inv_dit_cross(uint64_t (&lo)[L / 4], uint64_t (&hi)[L / 4]) {
 #pragma unroll
-  for (int m = 0; m < L / 4; ++m) gs_bfly(lo[m], hi[m], s);
+  for (int m = 0; m < L / 4; ++m) ct_bfly(lo[m], hi[m], dit_shift(L, SH2, L / 2, H * (L / 4) + m));
 }
 
 // Compile-time description of the transform for a ring dimension N = L^2.

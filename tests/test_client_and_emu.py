@@ -80,9 +80,13 @@ def emu():
     L.she_emu_gl_mul.argtypes = [ctypes.c_uint64] * 2
     L.she_emu_gl_mul_pow2.restype = ctypes.c_uint64
     L.she_emu_gl_mul_pow2.argtypes = [ctypes.c_uint64, ctypes.c_int]
-    for f in ("she_emu_gl_add", "she_emu_gl_sub"):
+    for f in ("she_emu_gl_add", "she_emu_gl_sub", "she_emu_gl_add_le", "she_emu_gl_sub_le"):
         getattr(L, f).restype = ctypes.c_uint64
         getattr(L, f).argtypes = [ctypes.c_uint64] * 2
+    L.she_emu_gl_shl_le.restype = ctypes.c_uint64
+    L.she_emu_gl_shl_le.argtypes = [ctypes.c_uint64, ctypes.c_int]
+    L.she_emu_gl_lift32_neg.restype = ctypes.c_uint32
+    L.she_emu_gl_lift32_neg.argtypes = [ctypes.c_uint64]
     return L
 
 
@@ -102,6 +106,35 @@ def test_goldilocks_field_ops():
     for s in range(192):
         for x in vals[:16]:
             assert L.she_emu_gl_mul_pow2(x, s) == x * pow(2, s, P64) % P64, (s, x)
+
+
+def test_bounded_butterfly_primitives():
+    """shl_le: v 2^s mod p with the result <= p for EVERY 64-bit v (the bound the
+    single-fold add_le / sub_le rely on); add_le / sub_le exact for y <= p;
+    lift32_neg(t) = centred lift of -t.  Edge values hit every fold branch."""
+    L = emu()
+    rng = np.random.default_rng(1)
+    edge = [0, 1, 2, 2 ** 32 - 2, 2 ** 32 - 1, 2 ** 32, 2 ** 32 + 1, P64 - 2, P64 - 1, P64,
+            P64 + 1, 2 ** 64 - 2, 2 ** 64 - 1, 2 ** 63, 2 ** 63 - 1, 0xFFFFFFFF00000000,
+            0xFFFFFFFEFFFFFFFF, 0x80000000FFFFFFFF, 0x7FFFFFFF80000000, 0x00000001FFFFFFFF]
+    rand = [int(v) for v in rng.integers(0, 2 ** 64 - 1, 60, dtype=np.uint64)]
+    hi_max = [(v | 0xFFFFFFFF00000000) for v in rand[:20]]
+    lo_small = [(v & 0xFFFFFFFF00000000) | k for k, v in enumerate(rand[20:40])]
+    vals = edge + rand + hi_max + lo_small
+    for s in range(96):
+        for v in vals:
+            t = L.she_emu_gl_shl_le(v, s)
+            assert t <= P64 and t % P64 == v * pow(2, s, P64) % P64, (s, v)
+    ys = [y for y in vals if y <= P64]
+    for x in vals:
+        for y in ys:
+            a, d = L.she_emu_gl_add_le(x, y), L.she_emu_gl_sub_le(x, y)
+            assert a % P64 == (x + y) % P64 and d % P64 == (x - y) % P64, (x, y)
+    half = (P64 - 1) // 2
+    for t in ys + [half, half + 1, half + 2]:
+        y = (-t) % P64
+        want = (y - P64 if y > half else y) % 2 ** 32
+        assert L.she_emu_gl_lift32_neg(t) == want, t
 
 
 @pytest.mark.parametrize("N", [256, 1024])
