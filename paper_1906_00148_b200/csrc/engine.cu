@@ -124,9 +124,14 @@ __global__ void __launch_bounds__(128 * G, B) br_kernel(BRArgs args) {
   const uint32_t total = *args.nlanes;
   const bool active_lane = lane < L;
 
-  for (uint32_t base = blockIdx.x * G; base < total; base += gridDim.x * G) {
+  // balanced contiguous share of the lane list: CTA b serves lanes
+  // [b total / grid, (b+1) total / grid), G at a time (at most one lane more
+  // than any other CTA, so the last round does not leave SMs idle)
+  const uint32_t first = (uint32_t)(((uint64_t)blockIdx.x * total) / gridDim.x);
+  const uint32_t last = (uint32_t)(((uint64_t)(blockIdx.x + 1) * total) / gridDim.x);
+  for (uint32_t base = first; base < last; base += G) {
     const uint32_t L_id = base + g;
-    const bool on = L_id < total;
+    const bool on = L_id < last;
     uint32_t gate = 0, h = 0;
     if (on) {
       const uint32_t e = args.lanes[L_id];
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(128 * G, B) br_kernel(BRArgs args) {
           for (int q = 0; q < 8; ++q) b[q] = __ldg(bki + (size_t)q * N + p);
 #pragma unroll
           for (int gg = 0; gg < G; ++gg)
-            if (base + gg < total) {
+            if (base + gg < last) {
               br::Lane<S> other(smem + (size_t)gg * lane_bytes);
               br::pointwise_pos<S>(other.buf, p, b);
             }
@@ -571,9 +576,10 @@ cudaEvent_t mark(she_ctx* ctx, cudaStream_t stream) {
 template <class S, int G, int B>
 she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
   const size_t smem = G * br::Lane<S>::bytes(ctx->p.n);
-  const size_t groups = (max_lanes + G - 1) / G;
+  // one CTA per lane up to B per SM: narrow levels (the scheduler's deep
+  // carry chains) run one lane per SM instead of G lanes on a few SMs
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(groups, (size_t)ctx->sms * B)));
+  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms * B)));
   cfg.blockDim = dim3(128 * G);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
