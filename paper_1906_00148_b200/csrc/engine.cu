@@ -396,6 +396,110 @@ __global__ void __launch_bounds__(512) ks_kernel(KSArgs args) {
 
 constexpr int kKsG = 16, kKsCH = 64;
 
+// K4 v2, for base 4 and t = 8 (every config): thread k owns the output words
+// k and k + 256 of G gates.  With d = b0 + 2 b1 and K3' = K3 - K1 - K2,
+//   KSK[i][j][d] = b0 K1 + b1 K2 + b0 b1 K3'
+// and with the masks m = -b the subtraction acc -= KSK[i][j][d] becomes
+//   tt = K2 + m0 NK3 (NK3 = K1 + K2 - K3),  acc += m0 K1,  acc += m1 tt
+// three IMADs on the FMA pipe per word and digit; the masks of every
+// (gate, i, j) are prepared once per CTA in shared memory (broadcast LDS.64).
+// Device layout of the repacked key: [N][8][3][stride] rows (K1, K2, NK3).
+constexpr int kKs2G = 32, kKs2CH = 16, kKs2T = 256;
+
+template <int G, int CH>
+__global__ void __launch_bounds__(kKs2T) ks2_kernel(KSArgs args) {
+  constexpr int T = 8;  // digits per coefficient
+  __shared__ uint2 masks[CH][T][G];
+  __shared__ uint32_t bprime[G];
+  __shared__ int gops[G];
+  const GateSrc& src = args.src;
+  const uint32_t k = threadIdx.x, g0 = blockIdx.x * G;
+  const uint32_t N = args.N, n = args.n, stride = src.stride;
+  const uint32_t round = 1u << (32 - 2 * T - 1);  // R10: round to the top 16 bits
+
+  if (k < G) {
+    const uint32_t g = g0 + k;
+    const int op = g < src.count ? gate_op(src, g) : -1;
+    gops[k] = op;
+    uint32_t b = 0;
+    if (op >= 0 && op < SHE_NOT) {
+      b = args.ext[(size_t)(2 * g) * args.ext_stride + N];
+      if (op == SHE_MUX) b += args.ext[(size_t)(2 * g + 1) * args.ext_stride + N] + kMu;
+    }
+    bprime[k] = b;
+  }
+  __syncthreads();
+  uint32_t acc[G][2];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    acc[q][0] = (k == n) ? bprime[q] : 0u;
+    acc[q][1] = (k + kKs2T == n) ? bprime[q] : 0u;
+  }
+
+  const bool hb = k + kKs2T < stride;  // second word exists (stride 512 at C1, 160 at C0)
+  for (uint32_t i0 = 0; i0 < N; i0 += CH) {
+    __syncthreads();
+    for (uint32_t idx = k; idx < (uint32_t)G * CH; idx += kKs2T) {
+      const uint32_t q = idx / CH, ii = idx % CH, g = g0 + q;
+      const int op = gops[q];
+      uint32_t y = 0;  // digits of 0 are 0: gates without KS subtract nothing
+      if (op >= 0 && op < SHE_NOT) {
+        uint32_t a = args.ext[(size_t)(2 * g) * args.ext_stride + i0 + ii];
+        if (op == SHE_MUX) a += args.ext[(size_t)(2 * g + 1) * args.ext_stride + i0 + ii];
+        y = a + round;
+      }
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        const uint32_t d = (y >> (30 - 2 * j)) & 3u;
+        masks[ii][j][q] = make_uint2(0u - (d & 1u), 0u - (d >> 1));
+      }
+    }
+    __syncthreads();
+    for (uint32_t ii = 0; ii < CH; ++ii) {
+      const uint32_t* rows = args.ksk + (size_t)(i0 + ii) * T * 3 * stride + k;
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        const uint32_t* r = rows + (size_t)(3 * j) * stride;
+        const uint32_t k1a = __ldg(r), k2a = __ldg(r + stride), n3a = __ldg(r + 2 * stride);
+        uint32_t k1b = 0, k2b = 0, n3b = 0;
+        if (hb) {
+          k1b = __ldg(r + kKs2T);
+          k2b = __ldg(r + stride + kKs2T);
+          n3b = __ldg(r + 2 * stride + kKs2T);
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const uint2 m = masks[ii][j][q];
+          acc[q][0] += m.x * k1a + m.y * (k2a + m.x * n3a);
+          acc[q][1] += m.x * k1b + m.y * (k2b + m.x * n3b);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const uint32_t g = g0 + q;
+    const int op = gops[q];
+    if (op < 0) continue;
+    uint32_t* o = gate_out(src, g);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t kk = k + h * kKs2T;
+      if (kk >= stride) continue;
+      uint32_t v;
+      if (op == SHE_NOT || op == SHE_COPY) {
+        bool neg;
+        const uint32_t* a = gate_in(src, g, 0, neg);
+        if (op == SHE_NOT) neg = !neg;
+        v = kk <= n ? (neg ? 0u - a[kk] : a[kk]) : 0u;
+      } else {
+        v = kk <= n ? acc[q][h] : 0u;
+      }
+      o[kk] = v;
+    }
+  }
+}
+
 // Slot gather: dst[dst_first + o] = +-src[lit_o & 0x7fffffff] (bit 31 negates
 // the n+1 live words; padding stays zero).  One CTA per slot.
 __global__ void gather_kernel(uint32_t* dst, size_t dst_first, const uint32_t* src,
@@ -458,6 +562,7 @@ struct she_ctx {
   // CTA of 128 G threads, B CTAs per SM (SHE_BR_CFG="GxB" selects another
   // instantiated shape, see SHE_BR_CONFIGS)
   int br_g = 5, br_b = 1;
+  bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
   // staging for the host-buffer API
   uint8_t* h_ops = nullptr;
   uint32_t* h_io = nullptr;
@@ -647,7 +752,10 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     k.N = ctx->p.N;
     k.n = ctx->p.n;
     k.t = ctx->p.ks_t;
-    ks_kernel<kKsG, kKsCH><<<(unsigned)((cnt + kKsG - 1) / kKsG), ctx->stride, 0, stream>>>(k);
+    if (ctx->ks2)
+      ks2_kernel<kKs2G, kKs2CH><<<(unsigned)((cnt + kKs2G - 1) / kKs2G), kKs2T, 0, stream>>>(k);
+    else
+      ks_kernel<kKsG, kKsCH><<<(unsigned)((cnt + kKsG - 1) / kKsG), ctx->stride, 0, stream>>>(k);
     CK(cudaGetLastError());
     if (ctx->timing) mark(ctx, stream);
     ctx->br_launches++;
@@ -714,6 +822,13 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
         for (uint32_t v = 1; v < base; ++v)
           memcpy(&h[(((size_t)i * t + j) * 3 + (v - 1)) * ctx->stride],
                  &ck->ksk[(((size_t)i * t + j) * base + v) * (n + 1)], (n + 1) * 4);
+    ctx->ks2 = (t == 8 && base == 4 && ctx->stride <= 2 * (uint32_t)kKs2T);
+    if (ctx->ks2)  // third row -> K1 + K2 - K3 (mod 2^32), see ks2_kernel
+      for (size_t r = 0; r < (size_t)N * t; ++r) {
+        uint32_t* row = &h[r * 3 * ctx->stride];
+        for (uint32_t w = 0; w < ctx->stride; ++w)
+          row[2 * ctx->stride + w] = row[w] + row[ctx->stride + w] - row[2 * ctx->stride + w];
+      }
     cudaError_t e = cudaMalloc(&ctx->ksk, sz * 4);
     if (e == cudaSuccess) e = cudaMemcpy(ctx->ksk, h.data(), sz * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
