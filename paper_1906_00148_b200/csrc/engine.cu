@@ -404,10 +404,10 @@ constexpr int kKsG = 16, kKsCH = 64;
 // three IMADs on the FMA pipe per word and digit; the masks of every
 // (gate, i, j) are prepared once per CTA in shared memory (broadcast LDS.64).
 // Device layout of the repacked key: [N][8][3][stride] rows (K1, K2, NK3).
-constexpr int kKs2G = 32, kKs2CH = 16, kKs2T = 256;
+constexpr int kKs2G = 16, kKs2CH = 16, kKs2T = 256;
 
 template <int G, int CH>
-__global__ void __launch_bounds__(kKs2T) ks2_kernel(KSArgs args) {
+__global__ void __launch_bounds__(kKs2T, 2) ks2_kernel(KSArgs args) {
   constexpr int T = 8;  // digits per coefficient
   __shared__ uint2 masks[CH][T][G];
   __shared__ uint32_t bprime[G];
