@@ -117,14 +117,14 @@ __host__ __device__ __forceinline__ void fwd_pass2_load(int i, const uint64_t* r
   constexpr int L = S::L;
   y[0] = row[i * (L + 1)];
 #pragma unroll
-  for (int j1 = 1; j1 < L; ++j1) y[j1] = gl::mul(row[i * (L + 1) + j1], tw[j1 * L + i]);
+  for (int j1 = 1; j1 < L; ++j1) y[j1] = gl::mul_le(row[i * (L + 1) + j1], tw[j1 * L + i]);
 }
 
 // Pass 2 (cyclic, shift twiddles) + store in NTT storage order (q*L + i).
 template <class S>
 __host__ __device__ __forceinline__ void fwd_pass2_store(int i, uint64_t (&y)[S::L], uint64_t* row) {
   constexpr int L = S::L;
-  ntt::fwd<L, S::SH2, false>(y);
+  ntt::fwd<L, S::SH2, false, 0, true>(y);  // y[L/2 ..] are twisted: <= p
 #pragma unroll
   for (int q = 0; q < L; ++q) row[q * L + i] = y[q];
 }
@@ -143,8 +143,8 @@ __host__ __device__ __forceinline__ void pointwise_pos(uint64_t* buf, int p, con
     gl::mac(oa, d[r], b[2 * r + 0]);
     gl::mac(ob, d[r], b[2 * r + 1]);
   }
-  buf[0 * RS + p] = gl::reduce_acc(oa);
-  buf[1 * RS + p] = gl::reduce_acc(ob);
+  buf[0 * RS + p] = gl::reduce_acc_le(oa);  // <= p: the inverse's first stage folds once
+  buf[1 * RS + p] = gl::reduce_acc_le(ob);
 }
 
 // ---- inverse path: output component c, thread (H, lane) ----------------------
@@ -196,8 +196,9 @@ __host__ __device__ __forceinline__ void inv_a_store(int i, const uint64_t (&lo)
 #pragma unroll
   for (int m = 0; m < L / 4; ++m) {
     const int j1 = H * (L / 4) + m, j1h = j1 + L / 2;
-    row[i * (L + 1) + j1] = j1 == 0 ? lo[m] : gl::mul(lo[m], itw[j1 * L + i]);
-    row[i * (L + 1) + j1h] = gl::mul(hi[m], itw[j1h * L + i]);
+    // every pass-B input <= p (j1 = 0 is not twisted: bounded by shl_le(x, 0))
+    row[i * (L + 1) + j1] = j1 == 0 ? gl::shl_le(lo[m], 0) : gl::mul_le(lo[m], itw[j1 * L + i]);
+    row[i * (L + 1) + j1h] = gl::mul_le(hi[m], itw[j1h * L + i]);
   }
 }
 

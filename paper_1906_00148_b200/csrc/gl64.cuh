@@ -117,6 +117,23 @@ __host__ __device__ __forceinline__ uint64_t mul(uint64_t a, uint64_t b) {
   return reduce128(a * b, mulhi(a, b));
 }
 
+// (hi:lo) mod p with the result <= p (so a following butterfly with twiddle
+// 1 can fold once, see add_le / sub_le).  hl EPS + EPS = (hl : ~hl) costs no
+// instruction; w = t0 + hl EPS + EPS with carry c gives c ? w : w - EPS
+// (c: w < hl EPS + EPS <= 2^64 - 2^32; !c: w - EPS <= 2^64 - 1 - EPS = p - 1).
+__host__ __device__ __forceinline__ uint64_t reduce128_le(uint64_t lo, uint64_t hi) {
+  const uint64_t hh = hi >> 32, hl = hi & 0xFFFFFFFFull;
+  uint64_t t0 = lo - hh;
+  if (lo < hh) t0 -= EPS;  // borrow: + p (cannot borrow again)
+  const uint64_t t1 = (hl << 32) | (~hl & 0xFFFFFFFFull);
+  const uint64_t w = t0 + t1;
+  return w < t1 ? w : w - EPS;
+}
+
+__host__ __device__ __forceinline__ uint64_t mul_le(uint64_t a, uint64_t b) {
+  return reduce128_le(a * b, mulhi(a, b));
+}
+
 // x * 2^32 mod p: x1 2^64 + x0 2^32 = x1 (2^32 - 1) + x0 2^32.
 __host__ __device__ __forceinline__ uint64_t mul_2_32(uint64_t x) {
   return reduce96(x << 32, x >> 32);
@@ -374,6 +391,15 @@ __host__ __device__ __forceinline__ void mac(Acc3& A, uint64_t a, uint64_t b) {
   A.lo = (uint64_t)s;
   A.hi = (uint64_t)(s >> 64);
 #endif
+}
+
+// As reduce_acc with the result <= p (r <= p; r - t + p <= p when r < t).
+__host__ __device__ __forceinline__ uint64_t reduce_acc_le(const Acc3& A) {
+  const uint64_t r = reduce128_le(A.lo, A.hi);
+  const uint64_t t = (uint64_t)A.top << 32;  // top <= 3
+  uint64_t d = r - t;
+  if (r < t) d -= EPS;
+  return d;
 }
 
 __host__ __device__ __forceinline__ uint64_t reduce_acc(const Acc3& A) {

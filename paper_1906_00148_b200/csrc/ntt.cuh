@@ -53,6 +53,14 @@ __host__ __device__ __forceinline__ void ct_bfly(uint64_t& lo, uint64_t& hi, int
   hi = ng ? a : b;
 }
 
+// Butterfly with twiddle 1 when hi <= p is known (a bounded product feeds it):
+// single folds as in ct_bfly.
+__host__ __device__ __forceinline__ void ct_bfly_le(uint64_t& lo, uint64_t& hi) {
+  const uint64_t u = lo;
+  lo = gl::add_le(u, hi);
+  hi = gl::sub_le(u, hi);
+}
+
 // Twiddle shift of block b at stage k of a length-L forward transform.
 //   negacyclic (theta = 2^SH, order 2L): theta^((2 brev_k(b) + 1) L / 2^(k+1))
 //   cyclic     (omega = 2^SH, order L) : omega^(brev_k(b) L / 2^(k+1))
@@ -66,7 +74,9 @@ __host__ __device__ constexpr int stage_shift(int L, int SH, int k, int b) {
 // stages K0 .. log2 L - 1.
 //   NEGA: a[q] = sum_j a_j theta^((2 brev(q) + 1) j)
 //   cyc : a[q] = sum_j a_j omega^(brev(q) j)
-template <int L, int SH, bool NEGA, int K0 = 0>
+// HI_LE: the inputs a[L/2 ..] of stage 0 are <= p (bounded products), so
+// stage-0 butterflies with twiddle 1 fold once.
+template <int L, int SH, bool NEGA, int K0 = 0, bool HI_LE = false>
 __host__ __device__ __forceinline__ void fwd(uint64_t (&a)[L]) {
   constexpr int LG = ilog2(L);
 #pragma unroll
@@ -76,7 +86,10 @@ __host__ __device__ __forceinline__ void fwd(uint64_t (&a)[L]) {
     for (int b = 0; b < (1 << k); ++b) {
       const int s = stage_shift<NEGA>(L, SH, k, b);
 #pragma unroll
-      for (int j = 0; j < len; ++j) ct_bfly(a[b * 2 * len + j], a[b * 2 * len + j + len], s);
+      for (int j = 0; j < len; ++j) {
+        if (HI_LE && k == 0 && s == 0) ct_bfly_le(a[j], a[j + len]);
+        else ct_bfly(a[b * 2 * len + j], a[b * 2 * len + j + len], s);
+      }
     }
   }
 }
@@ -102,6 +115,7 @@ __host__ __device__ __forceinline__ void inv_dit(uint64_t (&a)[L]) {
 
 // The same transform split over two threads H = 0, 1 holding halves
 // a[H L/2 + m]: stages h = 1 .. L/4 stay inside a half ...
+// (all inputs are <= p: the first stage, twiddle 1 throughout, folds once)
 template <int L, int SH2>
 __host__ __device__ __forceinline__ void inv_dit_half(uint64_t (&a)[L / 2]) {
 #pragma unroll
@@ -109,7 +123,10 @@ __host__ __device__ __forceinline__ void inv_dit_half(uint64_t (&a)[L / 2]) {
 #pragma unroll
     for (int blk = 0; blk < L / 2; blk += 2 * h) {
 #pragma unroll
-      for (int j = 0; j < h; ++j) ct_bfly(a[blk + j], a[blk + j + h], dit_shift(L, SH2, h, j));
+      for (int j = 0; j < h; ++j) {
+        if (h == 1) ct_bfly_le(a[blk + j], a[blk + j + h]);
+        else ct_bfly(a[blk + j], a[blk + j + h], dit_shift(L, SH2, h, j));
+      }
     }
   }
 }
