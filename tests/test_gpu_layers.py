@@ -179,3 +179,118 @@ def test_config2_full_at_default_params(cuda):
     assert np.array_equal(got, net.config2(px, w1))
     assert check_captured(e, 6) <= 16
     she.capture(e.ctx, 0, 0, 0)
+
+
+# ----------------------------------------------------------------------------
+# config 4 (BASELINE.json configs[4]) at the default parameters, by tiles
+# ----------------------------------------------------------------------------
+# The full CIFAR-shaped net is ~0.5-0.7 G bootstrapped gates (hours on one
+# GPU), so every layer kind is checked on a seed-independent tile: rank 0 of
+# a `world`-way neuron split (the multi-GPU shard API), fed with the client's
+# encryption of that layer's exact plaintext input.  Decrypted tile outputs
+# must equal the plaintext network; sampled gate ciphertexts must equal the
+# oracle's.
+
+@pytest.fixture(scope="module")
+def config4_plain():
+    cfg = 4
+    px = si.pixels(cfg, (32, 32, 3)).astype(np.int64)
+    w1 = si.log_quant_weights(cfg, (32, 3, 3, 3), layer=0)
+    w2 = si.log_quant_weights(cfg, (32, 3, 3, 32), layer=1)
+    w3 = si.log_quant_weights(cfg, (64, 3, 3, 32), layer=2)
+    w4 = si.log_quant_weights(cfg, (10, 4096), layer=3)
+    h1 = net.relu(net.conv(px, w1, 1, 1, 16))
+    h2 = net.relu(net.conv(h1, w2, 1, 1, 16))
+    p1 = net.maxpool2x2(h2)
+    h3 = net.relu(net.conv(p1, w3, 1, 1, 16))
+    p2 = net.maxpool2x2(h3)
+    logits = net.fc(p2.ravel(), w4, 16)
+    assert np.array_equal(logits, net.config4(px, w1, w2, w3, w4))
+    return dict(px=px, w=(w1, w2, w3, w4), h1=h1, h2=h2, p1=p1, h3=h3, p2=p2, logits=logits)
+
+
+def _tile_ctx(e, world):
+    return she.Context(e.P, e.ck, device=0, rank=0, world=world)
+
+
+def _conv_tile(e, x_plain, w_in, wq, world, seed):
+    H, W, C = x_plain.shape
+    ctx = _tile_ctx(e, world)
+    x, _ = e.encrypt_words(x_plain, w_in, seed)
+    she.capture(ctx, si.sample_seed(4) + seed, 20011, 8)
+    out, w = she.she_conv_shift_acc(ctx, x, H, W, C, w_in, False, wq, 1, 1, 16, relu=True)
+    words = out.shape[0] * out.shape[1] * out.shape[2]
+    hi = -(-words // world)
+    got = net.value_of(e.decrypt_bits(out.reshape(words, w, -1)[:hi]), signed=False)
+    ops, slots = she.capture_read(ctx, 8)
+    ctx.close()
+    return got, hi, w, ops, slots
+
+
+def _check_slots(e, ops, slots):
+    if len(ops):
+        a, b, c, out = (np.ascontiguousarray(slots[:, j]) for j in range(4))
+        assert np.array_equal(oracle.gates(e.K, ops, a, b, c), out)
+
+
+def _bits_needed(v):
+    return max(1, int(np.max(v)).bit_length())
+
+
+def test_config4_conv1_tile(cuda, config4_plain):
+    e, d = env(4), config4_plain
+    got, hi, w, ops, slots = _conv_tile(e, d["px"], 8, d["w"][0], 128, 41)
+    assert np.array_equal(got, d["h1"].reshape(-1)[:hi])
+    _check_slots(e, ops, slots)
+
+
+def test_config4_conv2_tile(cuda, config4_plain):
+    """32 -> 32 channels, 288 terms per neuron, inputs = ReLU outputs of conv1."""
+    e, d = env(4), config4_plain
+    wa = she.conv_width(32, 32, 3, 8, False, d["w"][0], 1, 1, 16, relu=True)
+    assert _bits_needed(d["h1"]) <= wa
+    got, hi, w, ops, slots = _conv_tile(e, d["h1"], wa, d["w"][1], 1024, 42)
+    assert np.array_equal(got, d["h2"].reshape(-1)[:hi])
+    _check_slots(e, ops, slots)
+
+
+def test_config4_maxpool_tile(cuda, config4_plain):
+    e, d = env(4), config4_plain
+    wa = she.conv_width(32, 32, 3, 8, False, d["w"][0], 1, 1, 16, relu=True)
+    wb = she.conv_width(32, 32, 32, wa, False, d["w"][1], 1, 1, 16, relu=True)
+    world = 16
+    ctx = _tile_ctx(e, world)
+    x, _ = e.encrypt_words(d["h2"], wb, 43)
+    out = she.she_maxpool2x2(ctx, x, 32, 32, 32, wb, False)
+    words = 16 * 16 * 32
+    hi = -(-words // world)
+    got = net.value_of(e.decrypt_bits(out.reshape(words, wb, -1)[:hi]), signed=False)
+    ctx.close()
+    assert np.array_equal(got, d["p1"].reshape(-1)[:hi])
+
+
+def test_config4_conv3_tile(cuda, config4_plain):
+    e, d = env(4), config4_plain
+    wa = she.conv_width(32, 32, 3, 8, False, d["w"][0], 1, 1, 16, relu=True)
+    wb = she.conv_width(32, 32, 32, wa, False, d["w"][1], 1, 1, 16, relu=True)
+    got, hi, w, ops, slots = _conv_tile(e, d["p1"], wb, d["w"][2], 512, 44)
+    assert np.array_equal(got, d["h3"].reshape(-1)[:hi])
+    _check_slots(e, ops, slots)
+
+
+def test_config4_fc_logit_tile_wraps(cuda, config4_plain):
+    """FC 4096 -> 10: the exact sums exceed 16 bits, so the logits exercise the
+    two's-complement wrap of the accumulator cap (R13) on real data."""
+    e, d = env(4), config4_plain
+    wa = she.conv_width(32, 32, 3, 8, False, d["w"][0], 1, 1, 16, relu=True)
+    wb = she.conv_width(32, 32, 32, wa, False, d["w"][1], 1, 1, 16, relu=True)
+    wc = she.conv_width(16, 16, 32, wb, False, d["w"][2], 1, 1, 16, relu=True)
+    world = 10
+    ctx = _tile_ctx(e, world)
+    x, _ = e.encrypt_words(d["p2"].ravel(), wc, 45)
+    out, w = she.she_fc_shift_acc(ctx, x, 4096, wc, False, d["w"][3], 16)
+    got = net.value_of(e.decrypt_bits(out)[:1], signed=True)
+    ctx.close()
+    exact = net.fc_exact(d["p2"].ravel(), d["w"][3])
+    assert net.wrap_events(exact, 16) > 0
+    assert np.array_equal(got, d["logits"][:1])
