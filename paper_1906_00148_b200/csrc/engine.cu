@@ -175,19 +175,32 @@ __global__ void __launch_bounds__(128 * G, B) br_kernel(BRArgs args) {
         if (active_lane) br::fwd_pass2_store<S>(lane, x, row);
       }
       __syncthreads();
-      // ---- pointwise: BK_i read once per CTA for all G lanes ----
+      // ---- pointwise: positions [0, P1) with BK_i read once for all G lanes,
+      // the remaining (N - P1) x G (position, lane) items spread evenly, so
+      // every thread does the same number of position-lane products ----
       {
+        constexpr int P1 = T < N ? T : N;
         const uint64_t* bki = args.bk + (size_t)i * 8 * N;
-        for (int p = tid; p < N; p += T) {
+        if (tid < P1) {
           uint64_t b[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) b[q] = __ldg(bki + (size_t)q * N + p);
+          for (int q = 0; q < 8; ++q) b[q] = __ldg(bki + (size_t)q * N + tid);
 #pragma unroll
           for (int gg = 0; gg < G; ++gg)
             if (base + gg < last) {
               br::Lane<S> other(smem + (size_t)gg * lane_bytes);
-              br::pointwise_pos<S>(other.buf, p, b);
+              br::pointwise_pos<S>(other.buf, tid, b);
             }
+        }
+        for (int k = tid; k < (N - P1) * G; k += T) {
+          const int p = P1 + k / G, gg = k % G;
+          if (base + gg < last) {
+            uint64_t b[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) b[q] = __ldg(bki + (size_t)q * N + p);
+            br::Lane<S> other(smem + (size_t)gg * lane_bytes);
+            br::pointwise_pos<S>(other.buf, p, b);
+          }
         }
       }
       __syncthreads();
