@@ -190,6 +190,19 @@ she_status she_conv_shift_acc(she_ctx* ctx, const uint32_t* in, int H, int W, in
 she_status she_fc_shift_acc(she_ctx* ctx, const uint32_t* in, int K, int w_in, int in_signed,
                             const int8_t* wq, int M, int acc_cap, int relu, uint32_t* out,
                             int* w_out, void* stream);
+/* TCN baseline (SURVEY.md §8(f) NEXT-1; PAPER.md:115, :254 the TFHE version
+ * of FCN with plaintext x ciphertext multiplications): the same layers with
+ * fixed-point multipliers wm (int16, c in [-255, 255], value c / 2^7) in place
+ * of log-quantised codes.  A product is the shift-and-add over the set bits of
+ * |c|: sign(c) * sum_{b : bit b of |c|} (x >> (7 - b)), one
+ * adder-tree term per set bit, so a single-bit c = 2^(7-e) is SHE's code e+1.
+ * Layouts, widths, sharding and errors as she_conv_shift_acc / she_fc_shift_acc. */
+she_status she_conv_mul_acc(she_ctx* ctx, const uint32_t* in, int H, int W, int C, int w_in,
+                            int in_signed, const int16_t* wm, int Co, int K, int stride, int pad,
+                            int acc_cap, int relu, uint32_t* out, int* w_out, void* stream);
+she_status she_fc_mul_acc(she_ctx* ctx, const uint32_t* in, int K, int w_in, int in_signed,
+                          const int16_t* wm, int M, int acc_cap, int relu, uint32_t* out,
+                          int* w_out, void* stream);
 /* ReLU on `words` signed words of `width` bits: R_i = AND(X_i, NOT sign)
  * (SPEC.md:193-201 reading of PAPER.md F2); out: words x (width-1) unsigned. */
 she_status she_relu(she_ctx* ctx, const uint32_t* in, size_t words, int width, uint32_t* out,
@@ -229,6 +242,13 @@ she_status she_clear_conv_shift_acc(const uint8_t* in, int H, int W, int C, int 
 she_status she_clear_fc_shift_acc(const uint8_t* in, int K, int w_in, int in_signed,
                                   const int8_t* wq, int M, int acc_cap, int relu, uint8_t* out,
                                   int* w_out, int rank, int world, she_circuit_stats* stats);
+she_status she_clear_conv_mul_acc(const uint8_t* in, int H, int W, int C, int w_in,
+                                  int in_signed, const int16_t* wm, int Co, int K, int stride,
+                                  int pad, int acc_cap, int relu, uint8_t* out, int* w_out,
+                                  int rank, int world, she_circuit_stats* stats);
+she_status she_clear_fc_mul_acc(const uint8_t* in, int K, int w_in, int in_signed,
+                                const int16_t* wm, int M, int acc_cap, int relu, uint8_t* out,
+                                int* w_out, int rank, int world, she_circuit_stats* stats);
 she_status she_clear_relu(const uint8_t* in, size_t words, int width, uint8_t* out, int rank,
                           int world, she_circuit_stats* stats);
 she_status she_clear_maxpool2x2(const uint8_t* in, int H, int W, int C, int w, int in_signed,

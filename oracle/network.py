@@ -40,7 +40,33 @@ def term(x, code):
     return np.where(code == 0, 0, np.sign(code) * t)
 
 
-def conv_exact(x, wq, stride: int, pad: int):
+TCN_FRAC = 7  # TCN multipliers c stand for c / 2^7
+
+
+def term_tcn(x, c):
+    """TCN plaintext x ciphertext product (SPEC.md:238-246 build_pc_mult): the
+    shift-and-add over the set bits of |c|, sign(c) * sum_{b : bit b of |c|}
+    floor(x / 2^(7 - b)); c in [-255, 255]."""
+    x = np.asarray(x, dtype=np.int64)
+    c = np.asarray(c, dtype=np.int64)
+    mag = np.abs(c)
+    acc = np.zeros(np.broadcast(x, c).shape, dtype=np.int64)
+    for b in range(TCN_FRAC + 1):
+        bit = (mag >> b) & 1
+        acc = acc + bit * np.right_shift(x, TCN_FRAC - b)
+    return np.sign(c) * acc
+
+
+def log_quantize(c):
+    """PAPER.md:118 weightQ = Quantize(log2(weight)): the SHE code +-(e+1) of the
+    power of two 2^-e nearest (in log2) to |c| / 2^7; 0 stays 0."""
+    c = np.asarray(c, dtype=np.int64)
+    mag = np.maximum(np.abs(c), 1)
+    e = np.clip(np.rint(TCN_FRAC - np.log2(mag)), 0, 7).astype(np.int64)
+    return np.where(c == 0, 0, np.sign(c) * (e + 1)).astype(np.int8)
+
+
+def conv_exact(x, wq, stride: int, pad: int, term_fn=None):
     """Exact (unwrapped) sums of a conv layer: x (H,W,C) ints, wq (Co,K,K,C) codes."""
     x = np.asarray(x, dtype=np.int64)
     H, W, C = x.shape
@@ -55,7 +81,7 @@ def conv_exact(x, wq, stride: int, pad: int):
             patch = xp[kh:kh + stride * (Ho - 1) + 1:stride, kw:kw + stride * (Wo - 1) + 1:stride]
             # patch (Ho, Wo, C); weight codes (Co, C) for this tap
             for co in range(Co):
-                out[:, :, co] += term(patch, wq[co, kh, kw][None, None, :]).sum(axis=-1)
+                out[:, :, co] += (term_fn or term)(patch, wq[co, kh, kw][None, None, :]).sum(axis=-1)
     return out
 
 
@@ -63,13 +89,29 @@ def conv(x, wq, stride: int, pad: int, cap: int):
     return wrap(conv_exact(x, wq, stride, pad), cap)
 
 
-def fc_exact(x, wq):
+def fc_exact(x, wq, term_fn=None):
     x = np.asarray(x, dtype=np.int64).ravel()
-    return term(x[None, :], wq).sum(axis=-1)
+    return (term_fn or term)(x[None, :], wq).sum(axis=-1)
 
 
 def fc(x, wq, cap: int):
     return wrap(fc_exact(x, wq), cap)
+
+
+def conv_tcn(x, wm, stride: int, pad: int, cap: int):
+    return wrap(conv_exact(x, wm, stride, pad, term_tcn), cap)
+
+
+def fc_tcn(x, wm, cap: int):
+    return wrap(fc_exact(x, wm, term_tcn), cap)
+
+
+def config3_tcn(px, m1, m2, m3, cap=16):
+    """The config-3 topology with TCN multipliers (the paper's TCN-vs-SHE
+    ablation, PAPER.md:254)."""
+    h = relu(conv_tcn(px, m1, 2, 0, cap))
+    h = relu(fc_tcn(h.ravel(), m2, cap))
+    return fc_tcn(h, m3, cap)
 
 
 def relu(v):

@@ -433,9 +433,31 @@ she_status run_layer(uint64_t neurons, int w_out, bool signed_out, int rank, int
   return SHE_OK;
 }
 
+// Weights: SHE log-quantised codes wq (0 or +-(e+1): the term sign * (x >> e)),
+// or, for the TCN baseline, plaintext fixed-point
+// multipliers wm = c in [-255, 255] standing for c / 2^7: the product is the
+// shift-and-add over the set bits of |c| (SPEC.md:238-246 build_pc_mult),
+// sign * sum_{b : bit b of |c|} (x >> (7 - b)), i.e. one SHE term of code
+// sign * (7 - b + 1) per set bit.  A single-bit c = 2^(7-e) is exactly SHE's
+// code e + 1.
+constexpr int kTcnFrac = 7;
+
+template <class Fn>
+void for_each_code(const int8_t* wq, const int16_t* wm, size_t idx, Fn f) {
+  if (!wm) {
+    if (wq[idx]) f((int8_t)wq[idx]);
+    return;
+  }
+  const int c = wm[idx];
+  const int mag = c < 0 ? -c : c, sgn = c < 0 ? -1 : 1;
+  for (int b = kTcnFrac; b >= 0; --b)
+    if ((mag >> b) & 1) f((int8_t)(sgn * (kTcnFrac - b + 1)));
+}
+
 struct ConvGeom {
   int H, W, C, w_in, in_signed, Co, K, stride, pad, cap, relu;
   const int8_t* wq;
+  const int16_t* wm = nullptr;  // TCN multipliers (wq unused when set)
   int Ho() const { return (H + 2 * pad - K) / stride + 1; }
   int Wo() const { return (W + 2 * pad - K) / stride + 1; }
 };
@@ -450,17 +472,18 @@ Word conv_neuron(const ConvGeom& g, Circuit& c, InputMap& im, uint64_t q) {
       const int ih = oh * g.stride - g.pad + kh, iw = ow * g.stride - g.pad + kw;
       if (ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) continue;  // zero padding
       for (int ci = 0; ci < g.C; ++ci) {
-        const int8_t code = g.wq[(((size_t)co * g.K + kh) * g.K + kw) * g.C + ci];
-        if (code == 0) continue;
-        Term t;
-        t.is_signed = g.in_signed != 0;
-        t.code = code;
+        const size_t widx = (((size_t)co * g.K + kh) * g.K + kw) * g.C + ci;
         const uint32_t base = (uint32_t)((((size_t)ih * g.W + iw) * g.C + ci) * g.w_in);
-        t.x.resize(g.w_in);
-        const int e = std::abs(code) - 1;
-        for (int b = 0; b < g.w_in; ++b)  // only bits that survive the shift are inputs
-          t.x[b] = (b >= e || (t.is_signed && b == g.w_in - 1)) ? im(base + b) : F;
-        terms.push_back(std::move(t));
+        for_each_code(g.wq, g.wm, widx, [&](int8_t code) {
+          Term t;
+          t.is_signed = g.in_signed != 0;
+          t.code = code;
+          t.x.resize(g.w_in);
+          const int e = std::abs(code) - 1;
+          for (int b = 0; b < g.w_in; ++b)  // only bits that survive the shift are inputs
+            t.x[b] = (b >= e || (t.is_signed && b == g.w_in - 1)) ? im(base + b) : F;
+          terms.push_back(std::move(t));
+        });
       }
     }
   Word v = shift_accumulate(c, terms, g.cap);
@@ -470,21 +493,22 @@ Word conv_neuron(const ConvGeom& g, Circuit& c, InputMap& im, uint64_t q) {
 struct FcGeom {
   int K, w_in, in_signed, M, cap, relu;
   const int8_t* wq;
+  const int16_t* wm = nullptr;  // TCN multipliers (wq unused when set)
 };
 
 Word fc_neuron(const FcGeom& g, Circuit& c, InputMap& im, uint64_t m) {
   std::vector<Term> terms;
   for (int k = 0; k < g.K; ++k) {
-    const int8_t code = g.wq[(size_t)m * g.K + k];
-    if (code == 0) continue;
-    Term t;
-    t.is_signed = g.in_signed != 0;
-    t.code = code;
-    const int e = std::abs(code) - 1;
-    t.x.resize(g.w_in);
-    for (int b = 0; b < g.w_in; ++b)
-      t.x[b] = (b >= e || (t.is_signed && b == g.w_in - 1)) ? im((uint32_t)(k * g.w_in + b)) : F;
-    terms.push_back(std::move(t));
+    for_each_code(g.wq, g.wm, (size_t)m * g.K + k, [&](int8_t code) {
+      Term t;
+      t.is_signed = g.in_signed != 0;
+      t.code = code;
+      const int e = std::abs(code) - 1;
+      t.x.resize(g.w_in);
+      for (int b = 0; b < g.w_in; ++b)
+        t.x[b] = (b >= e || (t.is_signed && b == g.w_in - 1)) ? im((uint32_t)(k * g.w_in + b)) : F;
+      terms.push_back(std::move(t));
+    });
   }
   Word v = shift_accumulate(c, terms, g.cap);
   return g.relu ? relu(c, v.size() > 1 ? v : Word{v[0], v[0]}) : v;
@@ -535,12 +559,12 @@ int conv_width(const ConvGeom& g) {
       for (int kw = 0; kw < g.K; ++kw) {
         const int ih = oh * g.stride - g.pad + kh, iw = ow * g.stride - g.pad + kw;
         if (ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) continue;
-        for (int ci = 0; ci < g.C; ++ci) {
-          const int8_t code = g.wq[(((size_t)co * g.K + kh) * g.K + kw) * g.C + ci];
-          if (code == 0) continue;
-          int lw = leaf_width(g.w_in, g.in_signed != 0, code, g.cap);
-          if (lw) leaves.push_back(lw);
-        }
+        for (int ci = 0; ci < g.C; ++ci)
+          for_each_code(g.wq, g.wm, (((size_t)co * g.K + kh) * g.K + kw) * g.C + ci,
+                        [&](int8_t code) {
+                          int lw = leaf_width(g.w_in, g.in_signed != 0, code, g.cap);
+                          if (lw) leaves.push_back(lw);
+                        });
       }
     w = std::max(w, neuron_width(leaves, g.cap, g.relu != 0));
   }
@@ -551,18 +575,23 @@ int fc_width(const FcGeom& g) {
   int w = 1;
   for (int m = 0; m < g.M; ++m) {
     std::vector<int> leaves;
-    for (int k = 0; k < g.K; ++k) {
-      const int8_t code = g.wq[(size_t)m * g.K + k];
-      if (code == 0) continue;
-      int lw = leaf_width(g.w_in, g.in_signed != 0, code, g.cap);
-      if (lw) leaves.push_back(lw);
-    }
+    for (int k = 0; k < g.K; ++k)
+      for_each_code(g.wq, g.wm, (size_t)m * g.K + k, [&](int8_t code) {
+        int lw = leaf_width(g.w_in, g.in_signed != 0, code, g.cap);
+        if (lw) leaves.push_back(lw);
+      });
     w = std::max(w, neuron_width(leaves, g.cap, g.relu != 0));
   }
   return w;
 }
 
-she_status check_codes(const int8_t* wq, size_t n) {
+she_status check_codes(const int8_t* wq, const int16_t* wm, size_t n) {
+  if (wm) {
+    for (size_t i = 0; i < n; ++i)
+      if (wm[i] < -255 || wm[i] > 255)
+        return she::fail(SHE_ERR_ARG, "TCN multiplier %d out of [-255, 255]", wm[i]);
+    return SHE_OK;
+  }
   for (size_t i = 0; i < n; ++i)
     if (wq[i] < -8 || wq[i] > 8) return she::fail(SHE_ERR_ARG, "weight code %d out of [-8, 8]", wq[i]);
   return SHE_OK;
@@ -570,11 +599,11 @@ she_status check_codes(const int8_t* wq, size_t n) {
 
 she_status conv_common(const ConvGeom& g, int* w_out, int rank, int world, Executor* ex,
                        she_circuit_stats* st) {
-  if (!g.wq || !w_out) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if ((!g.wq && !g.wm) || !w_out) return she::fail(SHE_ERR_ARG, "NULL argument");
   if (g.H <= 0 || g.W <= 0 || g.C <= 0 || g.Co <= 0 || g.K <= 0 || g.stride <= 0 || g.pad < 0 ||
       g.w_in <= 0 || g.w_in > 32 || g.cap < 2 || g.cap > 32 || g.Ho() <= 0 || g.Wo() <= 0)
     return she::fail(SHE_ERR_SHAPE, "bad conv shape");
-  she_status s = check_codes(g.wq, (size_t)g.Co * g.K * g.K * g.C);
+  she_status s = check_codes(g.wq, g.wm, (size_t)g.Co * g.K * g.K * g.C);
   if (s != SHE_OK) return s;
   const int w = conv_width(g);
   if (!ex) {
@@ -591,10 +620,10 @@ she_status conv_common(const ConvGeom& g, int* w_out, int rank, int world, Execu
 
 she_status fc_common(const FcGeom& g, int* w_out, int rank, int world, Executor* ex,
                      she_circuit_stats* st) {
-  if (!g.wq || !w_out) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if ((!g.wq && !g.wm) || !w_out) return she::fail(SHE_ERR_ARG, "NULL argument");
   if (g.K <= 0 || g.M <= 0 || g.w_in <= 0 || g.w_in > 32 || g.cap < 2 || g.cap > 32)
     return she::fail(SHE_ERR_SHAPE, "bad fc shape");
-  she_status s = check_codes(g.wq, (size_t)g.M * g.K);
+  she_status s = check_codes(g.wq, g.wm, (size_t)g.M * g.K);
   if (s != SHE_OK) return s;
   const int w = fc_width(g);
   if (!ex) {
@@ -680,6 +709,36 @@ she_status she_fc_shift_acc(she_ctx* ctx, const uint32_t* in, int K, int w_in, i
   return fc_common(g, w_out, she::engine_rank(ctx), she::engine_world(ctx), &ex, st);
 }
 
+she_status she_conv_mul_acc(she_ctx* ctx, const uint32_t* in, int H, int W, int C, int w_in,
+                            int in_signed, const int16_t* wm, int Co, int K, int stride, int pad,
+                            int acc_cap, int relu_, uint32_t* out, int* w_out, void* stream) {
+  ConvGeom g{H, W, C, w_in, in_signed, Co, K, stride, pad, acc_cap, relu_, nullptr, wm};
+  if (!out) return conv_common(g, w_out, 0, 1, nullptr, nullptr);
+  if (!ctx || !in) return she::fail(SHE_ERR_ARG, "NULL argument");
+  GpuExec ex;
+  ex.ctx = ctx;
+  ex.in = in;
+  ex.out = out;
+  ex.stream = stream;
+  she_circuit_stats* st = she::engine_stats(ctx, true);
+  return conv_common(g, w_out, she::engine_rank(ctx), she::engine_world(ctx), &ex, st);
+}
+
+she_status she_fc_mul_acc(she_ctx* ctx, const uint32_t* in, int K, int w_in, int in_signed,
+                          const int16_t* wm, int M, int acc_cap, int relu_, uint32_t* out,
+                          int* w_out, void* stream) {
+  FcGeom g{K, w_in, in_signed, M, acc_cap, relu_, nullptr, wm};
+  if (!out) return fc_common(g, w_out, 0, 1, nullptr, nullptr);
+  if (!ctx || !in) return she::fail(SHE_ERR_ARG, "NULL argument");
+  GpuExec ex;
+  ex.ctx = ctx;
+  ex.in = in;
+  ex.out = out;
+  ex.stream = stream;
+  she_circuit_stats* st = she::engine_stats(ctx, true);
+  return fc_common(g, w_out, she::engine_rank(ctx), she::engine_world(ctx), &ex, st);
+}
+
 she_status she_relu(she_ctx* ctx, const uint32_t* in, size_t words, int width, uint32_t* out,
                     void* stream) {
   if (words == 0) return SHE_OK;
@@ -732,6 +791,35 @@ she_status she_clear_fc_shift_acc(const uint8_t* in, int K, int w_in, int in_sig
                                   const int8_t* wq, int M, int acc_cap, int relu_, uint8_t* out,
                                   int* w_out, int rank, int world, she_circuit_stats* st) {
   FcGeom g{K, w_in, in_signed, M, acc_cap, relu_, wq};
+  if (st) *st = she_circuit_stats{};
+  if (!out) return fc_common(g, w_out, 0, 1, nullptr, nullptr);
+  if (!in) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return she::fail(SHE_ERR_ARG, "bad rank/world");
+  ClearExec ex;
+  ex.in = in;
+  ex.out = out;
+  return fc_common(g, w_out, rank, world, &ex, st);
+}
+
+she_status she_clear_conv_mul_acc(const uint8_t* in, int H, int W, int C, int w_in,
+                                  int in_signed, const int16_t* wm, int Co, int K, int stride,
+                                  int pad, int acc_cap, int relu_, uint8_t* out, int* w_out,
+                                  int rank, int world, she_circuit_stats* st) {
+  ConvGeom g{H, W, C, w_in, in_signed, Co, K, stride, pad, acc_cap, relu_, nullptr, wm};
+  if (st) *st = she_circuit_stats{};
+  if (!out) return conv_common(g, w_out, 0, 1, nullptr, nullptr);
+  if (!in) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return she::fail(SHE_ERR_ARG, "bad rank/world");
+  ClearExec ex;
+  ex.in = in;
+  ex.out = out;
+  return conv_common(g, w_out, rank, world, &ex, st);
+}
+
+she_status she_clear_fc_mul_acc(const uint8_t* in, int K, int w_in, int in_signed,
+                                const int16_t* wm, int M, int acc_cap, int relu_, uint8_t* out,
+                                int* w_out, int rank, int world, she_circuit_stats* st) {
+  FcGeom g{K, w_in, in_signed, M, acc_cap, relu_, nullptr, wm};
   if (st) *st = she_circuit_stats{};
   if (!out) return fc_common(g, w_out, 0, 1, nullptr, nullptr);
   if (!in) return she::fail(SHE_ERR_ARG, "NULL argument");

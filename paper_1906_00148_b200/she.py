@@ -92,6 +92,19 @@ def lib() -> ctypes.CDLL:
             "she_fc_shift_acc": ([_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
                                   ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
                                   ctypes.POINTER(ctypes.c_int), _vp], ctypes.c_int),
+            "she_conv_mul_acc": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
+                                 + [_vp, ctypes.POINTER(ctypes.c_int), _vp], ctypes.c_int),
+            "she_fc_mul_acc": ([_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                ctypes.POINTER(ctypes.c_int), _vp], ctypes.c_int),
+            "she_clear_conv_mul_acc": ([_vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
+                                       + [_vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                          ctypes.c_int, ctypes.POINTER(she_circuit_stats)],
+                                       ctypes.c_int),
+            "she_clear_fc_mul_acc": ([_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                      ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_relu": ([_vp, _vp, _sz, ctypes.c_int, _vp, _vp], ctypes.c_int),
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
@@ -425,3 +438,83 @@ def clear_maxpool2x2(bits, H, W, C, w, in_signed, rank=0, world=1):
     _check(lib().she_clear_maxpool2x2(_np_ptr(bits), H, W, C, w, int(in_signed), _np_ptr(out),
                                       rank, world, ctypes.byref(st)))
     return out, st.as_dict()
+
+
+# ---- TCN baseline: fixed-point multipliers (she.h she_*_mul_acc) -------------
+
+def _mults(wm) -> np.ndarray:
+    return np.ascontiguousarray(wm, dtype=np.int16)
+
+
+def conv_mul_width(H, W, C, w_in, in_signed, wm, stride, pad, cap=16, relu=False) -> int:
+    wm = _mults(wm)
+    Co, K = wm.shape[0], wm.shape[1]
+    w = ctypes.c_int(0)
+    _check(lib().she_conv_mul_acc(None, None, H, W, C, w_in, int(in_signed), _np_ptr(wm), Co, K,
+                                  stride, pad, cap, int(relu), None, ctypes.byref(w), None))
+    return w.value
+
+
+def fc_mul_width(K, w_in, in_signed, wm, cap=16, relu=False) -> int:
+    wm = _mults(wm)
+    w = ctypes.c_int(0)
+    _check(lib().she_fc_mul_acc(None, None, K, w_in, int(in_signed), _np_ptr(wm), wm.shape[0],
+                                cap, int(relu), None, ctypes.byref(w), None))
+    return w.value
+
+
+def she_conv_mul_acc(ctx: Context, x, H, W, C, w_in, in_signed, wm, stride, pad, cap=16,
+                     relu=False, out=None, stream=None):
+    import torch
+    wm = _mults(wm)
+    Co, K = wm.shape[0], wm.shape[1]
+    Ho, Wo = (H + 2 * pad - K) // stride + 1, (W + 2 * pad - K) // stride + 1
+    w = ctypes.c_int(conv_mul_width(H, W, C, w_in, in_signed, wm, stride, pad, cap, relu))
+    if out is None:
+        out = torch.zeros((Ho, Wo, Co, w.value, ctx.stride), dtype=torch.int32, device=x.device)
+    _check(lib().she_conv_mul_acc(ctx.handle, _dev_ptr(x), H, W, C, w_in, int(in_signed),
+                                  _np_ptr(wm), Co, K, stride, pad, cap, int(relu), _dev_ptr(out),
+                                  ctypes.byref(w), _stream_ptr(stream)))
+    return out, w.value
+
+
+def she_fc_mul_acc(ctx: Context, x, K, w_in, in_signed, wm, cap=16, relu=False, out=None,
+                   stream=None):
+    import torch
+    wm = _mults(wm)
+    M = wm.shape[0]
+    w = ctypes.c_int(fc_mul_width(K, w_in, in_signed, wm, cap, relu))
+    if out is None:
+        out = torch.zeros((M, w.value, ctx.stride), dtype=torch.int32, device=x.device)
+    _check(lib().she_fc_mul_acc(ctx.handle, _dev_ptr(x), K, w_in, int(in_signed), _np_ptr(wm), M,
+                                cap, int(relu), _dev_ptr(out), ctypes.byref(w),
+                                _stream_ptr(stream)))
+    return out, w.value
+
+
+def clear_conv_mul_acc(bits, H, W, C, w_in, in_signed, wm, stride, pad, cap=16, relu=False,
+                       rank=0, world=1):
+    wm = _mults(wm)
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    Co, K = wm.shape[0], wm.shape[1]
+    Ho, Wo = (H + 2 * pad - K) // stride + 1, (W + 2 * pad - K) // stride + 1
+    w = ctypes.c_int(conv_mul_width(H, W, C, w_in, in_signed, wm, stride, pad, cap, relu))
+    out = np.zeros((Ho, Wo, Co, w.value), dtype=np.uint8)
+    st = she_circuit_stats()
+    _check(lib().she_clear_conv_mul_acc(_np_ptr(bits), H, W, C, w_in, int(in_signed), _np_ptr(wm),
+                                        Co, K, stride, pad, cap, int(relu), _np_ptr(out),
+                                        ctypes.byref(w), rank, world, ctypes.byref(st)))
+    return out, w.value, st.as_dict()
+
+
+def clear_fc_mul_acc(bits, K, w_in, in_signed, wm, cap=16, relu=False, rank=0, world=1):
+    wm = _mults(wm)
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    M = wm.shape[0]
+    w = ctypes.c_int(fc_mul_width(K, w_in, in_signed, wm, cap, relu))
+    out = np.zeros((M, w.value), dtype=np.uint8)
+    st = she_circuit_stats()
+    _check(lib().she_clear_fc_mul_acc(_np_ptr(bits), K, w_in, int(in_signed), _np_ptr(wm), M, cap,
+                                      int(relu), _np_ptr(out), ctypes.byref(w), rank, world,
+                                      ctypes.byref(st)))
+    return out, w.value, st.as_dict()

@@ -187,3 +187,20 @@ def log_quant_weights(cfg: int, shape, layer: int = 0) -> np.ndarray:
     e = (r & np.uint64(7)).astype(np.int64)
     code = np.where(zero, 0, sign * (e + 1)).astype(np.int8)
     return code.reshape(shape)
+
+
+def tcn_weights(cfg: int, shape, layer: int = 0) -> np.ndarray:
+    """Fixed-point multipliers for the TCN baseline:
+    int16 c in [-255, 255] standing for c / 2^7.  Same stream, sign and zero
+    pattern as log_quant_weights; the magnitude is 2^(7 - t) rounded, with t
+    uniform in [-0.5, 7.5) (so its nearest power of two spreads over the same
+    exponents e in 0..7 as the SHE weights), clipped to [1, 255]."""
+    size = int(np.prod(shape))
+    base = np.uint64(layer) << np.uint64(40)
+    r = rng_u64(weight_seed(cfg), STREAM_WEIGHTS, base + np.arange(size, dtype=np.uint64))
+    u = (r >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    zero = u < 0.1
+    sign = np.where(((r >> np.uint64(3)) & np.uint64(1)) == 1, -1, 1)
+    t = ((r >> np.uint64(16)) & np.uint64(0xFFFFFF)).astype(np.float64) / 2.0 ** 24 * 8.0 - 0.5
+    mag = np.clip(np.rint(2.0 ** (7.0 - t)), 1, 255).astype(np.int64)
+    return np.where(zero, 0, sign * mag).astype(np.int16).reshape(shape)

@@ -294,3 +294,37 @@ def test_config4_fc_logit_tile_wraps(cuda, config4_plain):
     exact = net.fc_exact(d["p2"].ravel(), d["w"][3])
     assert net.wrap_events(exact, 16) > 0
     assert np.array_equal(got, d["logits"][:1])
+
+
+# ----------------------------------------------------------------------------
+# TCN baseline: fixed-point multipliers
+# ----------------------------------------------------------------------------
+
+def test_tcn_fc_and_conv_c0_decrypted_and_sampled_ciphertexts(cuda):
+    e = env(0)
+    rng = np.random.default_rng(21)
+    x = rng.integers(-(1 << 7), 1 << 7, 10)
+    wm = rng.integers(-255, 256, (4, 10)).astype(np.int16)
+    ct, _ = e.encrypt_words(x, 8, 2121)
+    she.capture(e.ctx, si.sample_seed(0) + 7, 23, 64)
+    o, w = she.she_fc_mul_acc(e.ctx, ct, 10, 8, True, wm, cap=12)
+    assert np.array_equal(net.value_of(e.decrypt_bits(o), signed=True), net.fc_tcn(x, wm, 12))
+    px = rng.integers(0, 256, (5, 5, 1))
+    wc = si.tcn_weights(2, (2, 3, 3, 1), layer=6)
+    xc, _ = e.encrypt_words(px, 8, 2222)
+    h, wh = she.she_conv_mul_acc(e.ctx, xc, 5, 5, 1, 8, False, wc, 1, 1, 16, relu=True)
+    assert np.array_equal(net.value_of(e.decrypt_bits(h), signed=False),
+                          net.relu(net.conv_tcn(px, wc, 1, 1, 16)))
+    check_captured(e, 4)
+    she.capture(e.ctx, 0, 0, 0)
+
+
+def test_tcn_config2_shape_at_default_params(cuda):
+    """Config-2 conv with TCN multipliers at N=1024, n=500 (0.71 M gates)."""
+    e = env(2)
+    px = si.pixels(2, (28, 28, 1)).astype(np.int64)
+    m1 = si.tcn_weights(2, (5, 5, 5, 1), layer=0)
+    x, _ = e.encrypt_words(px, 8, si.input_seed(2) + 1)
+    h, w = she.she_conv_mul_acc(e.ctx, x, 28, 28, 1, 8, False, m1, 2, 0, 16, relu=True)
+    assert np.array_equal(net.value_of(e.decrypt_bits(h), signed=False),
+                          net.relu(net.conv_tcn(px, m1, 2, 0, 16)))
