@@ -156,7 +156,7 @@ def read_profile_traffic():
 # ---------------------------------------------------------------------------
 # the product arm
 # ---------------------------------------------------------------------------
-def net_latency(ctx, sk, P, world: int, rank: int):
+def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     """BASELINE.json's second metric: latency of the encrypted MNIST-shaped net
     (configs[3]: conv 5x5/2 1->5 + ReLU, FC 720->100 + ReLU, FC 100->10) at the
     default parameters, device-resident input ciphertexts -> device-resident
@@ -172,9 +172,15 @@ def net_latency(ctx, sk, P, world: int, rank: int):
 
     cfg = 3
     px = si.pixels(cfg, (28, 28, 1)).astype(np.int64)
-    w1 = si.log_quant_weights(cfg, (5, 5, 5, 1), layer=0)
-    w2 = si.log_quant_weights(cfg, (100, 720), layer=1)
-    w3 = si.log_quant_weights(cfg, (10, 100), layer=2)
+    # SHE: log-quantised codes; TCN (--tcn): 8-bit
+    # fixed-point multipliers by shift-and-add on the same engine
+    gen = si.tcn_weights if tcn else si.log_quant_weights
+    w1 = gen(cfg, (5, 5, 5, 1), layer=0)
+    w2 = gen(cfg, (100, 720), layer=1)
+    w3 = gen(cfg, (10, 100), layer=2)
+    conv_call, fc_call = ((she.she_conv_mul_acc, she.she_fc_mul_acc) if tcn
+                          else (she.she_conv_shift_acc, she.she_fc_shift_acc))
+    conv_w, fc_w = (she.conv_mul_width, she.fc_mul_width) if tcn else (she.conv_width, she.fc_width)
     stride = P.stride
     bits = net.bits_of(px, 8)
     cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0)
@@ -189,9 +195,9 @@ def net_latency(ctx, sk, P, world: int, rank: int):
     def gather(buf, words):
         return gather_shards(buf, words, rank, world)
 
-    wa = she.conv_width(28, 28, 1, 8, False, w1, 2, 0, 16, relu=True)
-    wb = she.fc_width(720, wa, False, w2, 16, relu=True)
-    wc = she.fc_width(100, wb, False, w3, 16)
+    wa = conv_w(28, 28, 1, 8, False, w1, 2, 0, 16, relu=True)
+    wb = fc_w(720, wa, False, w2, 16, relu=True)
+    wc = fc_w(100, wb, False, w3, 16)
     h1, p1 = sharded(720, wa)
     h2, p2 = sharded(100, wb)
     lo, p3 = sharded(10, wc)
@@ -202,13 +208,13 @@ def net_latency(ctx, sk, P, world: int, rank: int):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record(stream)
-    she.she_conv_shift_acc(ctx, x, 28, 28, 1, 8, False, w1, 2, 0, 16, relu=True, out=h1[:720])
+    conv_call(ctx, x, 28, 28, 1, 8, False, w1, 2, 0, 16, relu=True, out=h1[:720])
     s1 = she.layer_stats(ctx)
     gather(h1, p1)
-    she.she_fc_shift_acc(ctx, h1[:720], 720, wa, False, w2, 16, relu=True, out=h2[:100])
+    fc_call(ctx, h1[:720], 720, wa, False, w2, 16, relu=True, out=h2[:100])
     s2 = she.layer_stats(ctx)
     gather(h2, p2)
-    she.she_fc_shift_acc(ctx, h2[:100], 100, wb, False, w3, 16, out=lo[:10])
+    fc_call(ctx, h2[:100], 100, wb, False, w3, 16, out=lo[:10])
     s3 = she.layer_stats(ctx)
     gather(lo, p3)
     e1.record(stream)
@@ -221,10 +227,12 @@ def net_latency(ctx, sk, P, world: int, rank: int):
         dev_s, wall = float(v[0]), float(v[1])
     logits = net.value_of(she.she_decrypt_bits(sk, lo[:10].cpu().numpy().view(np.uint32)
                                                .reshape(-1, stride)).reshape(10, wc), signed=True)
-    want = net.config3(px, w1, w2, w3)
+    want = net.config3_tcn(px, w1, w2, w3) if tcn else net.config3(px, w1, w2, w3)
     stats = [s1, s2, s3]
+    kind = ("TCN baseline: 8-bit fixed-point multipliers (shift-and-add)" if tcn
+            else "log-quantised weights")
     return {"workload": "config3: MNIST-shaped encrypted net, 28x28x1 uint8 input, conv 5x5/2 1->5 "
-                        "+ ReLU, FC 720->100 + ReLU, FC 100->10, log-quantised weights, 16-bit "
+                        f"+ ReLU, FC 720->100 + ReLU, FC 100->10, {kind}, 16-bit "
                         "mixed-width accumulators; default TFHE parameters",
             "latency_s": round(dev_s, 3), "wall_s": round(wall, 3), "unit": "s",
             "higher_is_better": False, "host_scheduling": "inside the timed region",
@@ -356,6 +364,8 @@ def run_she(args):
             "k6_modmul_peak_per_s": round(k6, 1)}
     if not args.no_net:
         line["net_latency"] = net_latency(ctx, sk, P, world, rank)
+    if args.tcn:
+        line["tcn_net_latency"] = net_latency(ctx, sk, P, world, rank, tcn=True)
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(args)
         if "net_latency" in line:  # the paper's FIL-style projection of the oracle
@@ -439,6 +449,8 @@ def main():
     ap.add_argument("--impl", default="she", choices=["she", "reference"])
     ap.add_argument("--no-net", action="store_true",
                     help="skip the encrypted MNIST-shaped net latency (config 3, ~1.5 min)")
+    ap.add_argument("--tcn", action="store_true",
+                    help="also time the TCN baseline of the same net (fixed-point multipliers)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
