@@ -186,7 +186,7 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0)
     x = torch.from_numpy(cts.view(np.int32)).cuda().reshape(28, 28, 1, 8, stride)
 
-    from paper_1906_00148_b200.parallel import gather_shards, padded_words
+    from paper_1906_00148_b200.parallel import gather_shards, max_over_ranks, padded_words
 
     def sharded(words, width):
         return torch.zeros((padded_words(words, world), width, stride), dtype=torch.int32,
@@ -221,10 +221,7 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     dev_s = e0.elapsed_time(e1) * 1e-3
-    if world > 1:
-        v = torch.tensor([dev_s, wall], dtype=torch.float64, device="cuda")
-        dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        dev_s, wall = float(v[0]), float(v[1])
+    dev_s, wall = max_over_ranks([dev_s, wall], world)
     logits = net.value_of(she.she_decrypt_bits(sk, lo[:10].cpu().numpy().view(np.uint32)
                                                .reshape(-1, stride)).reshape(10, wc), signed=True)
     want = net.config3_tcn(px, w1, w2, w3) if tcn else net.config3(px, w1, w2, w3)
@@ -249,9 +246,17 @@ def run_she(args):
     import torch.distributed as dist
     from paper_1906_00148_b200 import she
 
+    from paper_1906_00148_b200.parallel import max_over_ranks
     world, rank, local = dist_env()
+    # SHE_BENCH_BACKEND=gloo + SHE_BENCH_DEVICE=0 run N ranks on one GPU: a
+    # functional check of the N > 1 code path only (timings meaningless).
+    backend = os.environ.get("SHE_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("SHE_BENCH_DEVICE", local))
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     P = si.CONFIG_PARAMS[CFG]
     sk, ck = she.she_keygen(P, si.key_seed(CFG))
@@ -300,11 +305,7 @@ def run_she(args):
     clk = clocks.stop()
     ctx.enable_timing(False)
     t = ctx.timing(reset=True)
-    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
-    if world > 1:
-        x = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(x, op=dist.ReduceOp.MAX)
-        dev_ms = float(x.item())
+    dev_ms = max_over_ranks([sum(a.elapsed_time(b) for a, b in evs)], world)[0]
     ms_per_step = dev_ms / args.steps
     value = world * COUNT * args.steps / (dev_ms * 1e-3)
 
@@ -338,11 +339,7 @@ def run_she(args):
         t0 = time.perf_counter()
         she.she_gate_batch_ops_host(ctx, h_ops, *h_in, h_out, stream)
         e2e_s.append(time.perf_counter() - t0)
-    e2e_total = sum(e2e_s)
-    if world > 1:
-        x = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
-        dist.all_reduce(x, op=dist.ReduceOp.MAX)
-        e2e_total = float(x.item())
+    e2e_total = max_over_ranks([sum(e2e_s)], world)[0]
     # correctness spot check of the e2e output against the device path
     assert np.array_equal(h_out, d_out.cpu().numpy().view(np.uint32)), "e2e output differs"
     dec = she.she_decrypt_bits(sk, h_out)

@@ -30,7 +30,25 @@ def gather_shards(buf, words: int, rank: int, world: int, group=None):
         return buf[:words]
     import torch.distributed as dist
     _, _, per = shard(words, rank, world)
+    if buf.is_cuda and dist.get_backend(group) == "gloo":  # CPU staging (functional tests)
+        host = buf.cpu()
+        gather_shards(host, words, rank, world, group)
+        buf.copy_(host)
+        return buf[:words]
     parts = list(buf.split(per, dim=0))
     mine = parts[rank].clone()
     dist.all_gather(parts, mine, group=group)
     return buf[:words]
+
+
+def max_over_ranks(values, world: int):
+    """Element-wise max over ranks of a list of floats (device timings are
+    reported as the max over ranks).  NCCL reduces on the GPU, gloo on the CPU."""
+    if world == 1:
+        return list(values)
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(list(values), dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
