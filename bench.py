@@ -222,6 +222,12 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     wall = time.perf_counter() - t0
     dev_s = e0.elapsed_time(e1) * 1e-3
     dev_s, wall = max_over_ranks([dev_s, wall], world)
+    lanes_total = sum(s["br_lanes"] for s in (s1, s2, s3))
+    if world > 1:  # every rank's share, for the oracle projection of the whole net
+        t = torch.tensor([float(lanes_total)], dtype=torch.float64,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t)
+        lanes_total = int(t.item())
     logits = net.value_of(she.she_decrypt_bits(sk, lo[:10].cpu().numpy().view(np.uint32)
                                                .reshape(-1, stride)).reshape(10, wc), signed=True)
     want = net.config3_tcn(px, w1, w2, w3) if tcn else net.config3(px, w1, w2, w3)
@@ -236,9 +242,10 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
             "gates_per_rank": int(sum(s["gates"] for s in stats)),
             "br_lanes_per_rank": int(sum(s["br_lanes"] for s in stats)),
             "levels": int(sum(s["levels"] for s in stats)),
+            "br_lanes_total": int(lanes_total),
             "logits_match_plaintext_network": bool(np.array_equal(logits, want)),
-            "parallelism": f"neuron-sharded x{world}, NCCL all-gather between layers"
-                           if world > 1 else "1 GPU"}
+            "parallelism": f"neuron-sharded x{world}, {dist.get_backend()} all-gather between "
+                           "layers" if world > 1 else "1 GPU"}
 
 
 def run_she(args):
@@ -369,7 +376,7 @@ def run_she(args):
             cb = line["cpu_baseline"]
             lanes_s = cb["value"] * si.br_lanes(ops[:12 * cb["cores"]]) / min(COUNT, 12 * cb["cores"])
             line["net_latency"]["oracle_projected_s"] = round(
-                line["net_latency"]["br_lanes_per_rank"] / lanes_s, 1)
+                line["net_latency"]["br_lanes_total"] / lanes_s, 1)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -109,6 +109,10 @@ __device__ __forceinline__ void pair_sync(int id) {
 // they share the instruction stream and each BK_i load); warp roles per lane
 // as described in bootstrap_core.cuh.  No iteration is skipped (a~_i = 0
 // gives digits 0 and an exactly-zero update, R9), so all lanes stay in step.
+__device__ __forceinline__ void lane_sync(int id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
 template <class S, int G, int B>
 __global__ void __launch_bounds__(128 * G, B) br_kernel(BRArgs args) {
   constexpr int N = S::N, L = S::L;
@@ -252,8 +256,11 @@ __global__ void __launch_bounds__(128 * G, B) br_kernel(BRArgs args) {
             br::inv_b_acc<S, 1>(lane, lo, hi, me.acc + c * N);
           }
         }
+        // the next forward of this lane reads its accumulator and rewrites its
+        // rows: only the lane's 4 warps need to agree (other lanes meet again
+        // at the CTA-wide barrier after the forward)
+        lane_sync(1 + 2 * G + g);
       }
-      __syncthreads();
     }
 
     // sample extract: a'_0 = A_0, a'_j = -A_{N-j}, b' = B_0

@@ -308,7 +308,7 @@ __host__ __device__ __forceinline__ uint64_t shl_le(uint64_t v, const int s) {
         "addc.u32 %4, %1, 0xFFFFFFFF;"
         : "=&r"(w0), "=&r"(w1), "=&r"(c), "=&r"(e0), "=&r"(e1)
         : "r"(T2 + 1), "r"(T0), "r"(T1));
-    o0 = c ? w0 : e0;
+    o0 = c ? w0 : e0;  // (an IMAD form e + c EPS measured 1.4 % slower in the kernel)
     o1 = c ? w1 : e1;
   } else if (q == 1) {
     uint32_t s0, H, e0, e1;
