@@ -363,6 +363,7 @@ def run_she(args):
             "config": {"workload": WORKLOAD, "gates_per_rank": COUNT, "br_lanes_per_rank": lanes,
                        "parallelism": f"gate-sharded x{world} (independent batches, no collective)",
                        "l2": "flushed between timed steps (256 MiB write), outside the event pairs"},
+            "br_lanes_per_s": round(world * lanes * args.steps / (dev_ms * 1e-3), 1),
             "roofline": roof, "clocks": clk, "e2e": e2e,
             "gpu_launches": int(t["br_launches"] + t["ks_launches"]),
             "k6_modmul_peak_per_s": round(k6, 1)}
@@ -371,7 +372,7 @@ def run_she(args):
     if args.tcn:
         line["tcn_net_latency"] = net_latency(ctx, sk, P, world, rank, tcn=True)
     if rank == 0:
-        line["cpu_baseline"] = cpu_baseline(args)
+        line["cpu_baseline"] = cpu_baseline(args, h_out)
         if "net_latency" in line:  # the paper's FIL-style projection of the oracle
             cb = line["cpu_baseline"]
             lanes_s = cb["value"] * si.br_lanes(ops[:12 * cb["cores"]]) / min(COUNT, 12 * cb["cores"])
@@ -404,15 +405,22 @@ def _oracle_sample(oracle, P, K, ops, bits, start: int, size: int):
     return out, dt
 
 
-def cpu_baseline(args):
+def cpu_baseline(args, gpu_out=None):
+    """The oracle timed on the host cores on the first gates of the batch; when
+    the GPU outputs of rank 0 are given, the same oracle outputs double as a
+    word-for-word parity check of this very run."""
     oracle, P, K, ops, bits = _oracle_workload()
     cores = oracle.threads()
     size = min(COUNT, 12 * cores)
-    _, dt = _oracle_sample(oracle, P, K, ops, bits, 0, size)
-    return {"value": round(size / dt, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"first {size} gates of config 1 ({si.br_lanes(ops[:size])} BR lanes), "
-                      f"{dt:.1f} s wall, schoolbook negacyclic products, OpenMP over gates, "
-                      f"gcc {oracle.COMPILER_FLAGS} {oracle.lib().variant}"}
+    ref, dt = _oracle_sample(oracle, P, K, ops, bits, 0, size)
+    out = {"value": round(size / dt, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"first {size} gates of config 1 ({si.br_lanes(ops[:size])} BR lanes), "
+                     f"{dt:.1f} s wall, schoolbook negacyclic products, OpenMP over gates, "
+                     f"gcc {oracle.COMPILER_FLAGS} {oracle.lib().variant}"}
+    if gpu_out is not None:
+        bad = int(np.sum(np.any(gpu_out[:size] != ref, axis=1)))
+        out["parity"] = {"ciphertexts_compared": size, "ciphertext_mismatches": bad}
+    return out
 
 
 def run_reference(args):
