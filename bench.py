@@ -248,6 +248,96 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
                            "layers" if world > 1 else "1 GPU"}
 
 
+def dshe_latency(ctx, sk, P, world: int, rank: int, H=28, ch=4, k=4):
+    """a DSHE-style deeper net (PAPER.md T3 :202-203,
+    [C-B-A-C-B-A-P] x k - F - F) at the default parameters: 28x28x1 uint8
+    input, 3x3 'same' convs with `ch` channels, BN lowered to shift + constant
+    (she_bn_shift_add), ReLU, max-pool; FC -> 8 + ReLU, FC -> 10.  Device-
+    resident input to device-resident logits, host scheduling included; the
+    decrypted logits are checked against the plaintext network."""
+    import torch
+    from oracle import network as net
+    from paper_1906_00148_b200 import she
+    from paper_1906_00148_b200.parallel import gather_shards, max_over_ranks, padded_words
+
+    cfg, stride = 5, P.stride
+    px = si.pixels(cfg, (H, H, 1)).astype(np.int64)
+    blocks, cin = [], 1
+    for b in range(k):
+        wa = si.log_quant_weights(cfg, (ch, 3, 3, cin), layer=10 * b)
+        wb = si.log_quant_weights(cfg, (ch, 3, 3, ch), layer=10 * b + 1)
+        blocks.append((wa, si.bn_params(cfg, ch, 10 * b), wb, si.bn_params(cfg, ch, 10 * b + 1)))
+        cin = ch
+    side = H >> k
+    fc1 = si.log_quant_weights(cfg, (8, side * side * ch), layer=90)
+    fc2 = si.log_quant_weights(cfg, (10, 8), layer=91)
+    cts = she.she_encrypt_bits(sk, net.bits_of(px, 8).ravel(), si.input_seed(cfg), 0)
+    x = torch.from_numpy(cts.view(np.int32)).cuda().reshape(H, H, 1, 8, stride)
+
+    def buf(words, width):
+        return torch.zeros((padded_words(words, world), width, stride), dtype=torch.int32,
+                           device="cuda")
+
+    lanes = levels = 0
+
+    def tally():
+        nonlocal lanes, levels
+        st = she.layer_stats(ctx)
+        lanes += st["br_lanes"]
+        levels += st["levels"]
+
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h, Hc, C, w, signed = x, H, 1, 8, False
+    for wa, bna, wb, bnb in blocks:
+        for wq, bn in ((wa, bna), (wb, bnb)):
+            co = wq.shape[0]
+            words = Hc * Hc * co
+            wc = she.conv_width(Hc, Hc, C, w, signed, wq, 1, 1, 16)
+            o = buf(words, wc)
+            she.she_conv_shift_acc(ctx, h, Hc, Hc, C, w, signed, wq, 1, 1, 16, out=o[:words])
+            tally()
+            gather_shards(o, words, rank, world)
+            wbn = she.bn_width(words, co, wc, True, *bn, cap=16, relu=True)
+            o2 = buf(words, wbn)
+            she.she_bn_shift_add(ctx, o[:words], words, co, wc, True, *bn, cap=16, relu=True,
+                                 out=o2[:words])
+            tally()
+            h, C, w, signed = gather_shards(o2, words, rank, world), co, wbn, False
+        words = (Hc // 2) * (Hc // 2) * C
+        o3 = buf(words, w)
+        she.she_maxpool2x2(ctx, h, Hc, Hc, C, w, False, out=o3[:words])
+        tally()
+        h, Hc = gather_shards(o3, words, rank, world), Hc // 2
+    w1 = she.fc_width(Hc * Hc * C, w, False, fc1, 16, relu=True)
+    o4 = buf(8, w1)
+    she.she_fc_shift_acc(ctx, h, Hc * Hc * C, w, False, fc1, 16, relu=True, out=o4[:8])
+    tally()
+    h = gather_shards(o4, 8, rank, world)
+    w2 = she.fc_width(8, w1, False, fc2, 16)
+    o5 = buf(10, w2)
+    she.she_fc_shift_acc(ctx, h, 8, w1, False, fc2, 16, out=o5[:10])
+    tally()
+    lo = gather_shards(o5, 10, rank, world)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dev_s = max_over_ranks([e0.elapsed_time(e1) * 1e-3], world)[0]
+    logits = net.value_of(she.she_decrypt_bits(sk, lo.cpu().numpy().view(np.uint32)
+                                               .reshape(-1, stride)).reshape(10, w2), signed=True)
+    return {"workload": f"DSHE-style net (NEXT-3): {H}x{H}x1 uint8, [conv3x3 {ch}ch + BN(shift+const) "
+                        f"+ ReLU] x2 + maxpool, x{k} blocks, FC->8 + ReLU, FC->10; default TFHE "
+                        "parameters",
+            "latency_s": round(dev_s, 3), "unit": "s", "higher_is_better": False,
+            "br_lanes_per_rank": int(lanes), "levels": int(levels),
+            "logits_match_plaintext_network": bool(np.array_equal(
+                logits, net.dshe(px, blocks, fc1, fc2)))}
+
+
 def run_she(args):
     import torch
     import torch.distributed as dist
@@ -371,6 +461,8 @@ def run_she(args):
         line["net_latency"] = net_latency(ctx, sk, P, world, rank)
     if args.tcn:
         line["tcn_net_latency"] = net_latency(ctx, sk, P, world, rank, tcn=True)
+    if args.dshe:
+        line["dshe_net_latency"] = dshe_latency(ctx, sk, P, world, rank)
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(args, h_out)
         if "net_latency" in line:  # the paper's FIL-style projection of the oracle
@@ -463,6 +555,8 @@ def main():
                     help="skip the encrypted MNIST-shaped net latency (config 3, ~1.5 min)")
     ap.add_argument("--tcn", action="store_true",
                     help="also time the TCN baseline of the same net (fixed-point multipliers)")
+    ap.add_argument("--dshe", action="store_true",
+                    help="also time a DSHE-style deeper net with batch norm (NEXT-3)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -207,6 +207,20 @@ she_status she_fc_mul_acc(she_ctx* ctx, const uint32_t* in, int K, int w_in, int
  * (SPEC.md:193-201 reading of PAPER.md F2); out: words x (width-1) unsigned. */
 she_status she_relu(she_ctx* ctx, const uint32_t* in, size_t words, int width, uint32_t* out,
                     void* stream);
+/* Batch normalisation lowered to shift + constant (the
+ * B layers of PAPER.md T3 :202-203): on `words` words of w_in bits laid out
+ * HWC (channel = word index mod C),
+ *   y = wrap_acc_cap(sign_c * scale(x, shift_c) + bias_c)
+ * with scale(x, s) = x 2^s for s >= 0, floor(x / 2^-s) for s < 0 (shift in
+ * [-8, 8], host int8[C]), sign_c = -1 where neg[c] != 0 (host uint8[C], NULL =
+ * all +1), bias host int32[C] in [-2^20, 2^20].  The scale is rewiring, the
+ * sign NOT flags + a carry-in, the bias an adder against constant bits.  relu
+ * != 0 fuses the ReLU (unsigned outputs of width w-1).  *w_out as in the conv
+ * call; words % C == 0. */
+she_status she_bn_shift_add(she_ctx* ctx, const uint32_t* in, size_t words, int C, int w_in,
+                            int in_signed, const int8_t* shift, const uint8_t* neg,
+                            const int32_t* bias, int acc_cap, int relu, uint32_t* out,
+                            int* w_out, void* stream);
 /* 2x2 stride-2 max-pool on [H][W][C][w][stride]: max = subtract-comparator
  * sign driving per-bit MUXes (PAPER.md F2); out [H/2][W/2][C][w][stride],
  * same signedness as the input. */
@@ -251,6 +265,10 @@ she_status she_clear_fc_mul_acc(const uint8_t* in, int K, int w_in, int in_signe
                                 int* w_out, int rank, int world, she_circuit_stats* stats);
 she_status she_clear_relu(const uint8_t* in, size_t words, int width, uint8_t* out, int rank,
                           int world, she_circuit_stats* stats);
+she_status she_clear_bn_shift_add(const uint8_t* in, size_t words, int C, int w_in,
+                                  int in_signed, const int8_t* shift, const uint8_t* neg,
+                                  const int32_t* bias, int acc_cap, int relu, uint8_t* out,
+                                  int* w_out, int rank, int world, she_circuit_stats* stats);
 she_status she_clear_maxpool2x2(const uint8_t* in, int H, int W, int C, int w, int in_signed,
                                 uint8_t* out, int rank, int world, she_circuit_stats* stats);
 

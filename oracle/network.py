@@ -118,6 +118,18 @@ def relu(v):
     return np.maximum(np.asarray(v, dtype=np.int64), 0)
 
 
+def bn_shift_add(v, shift, neg, bias, cap: int):
+    """Batch normalisation lowered to a power-of-two scale and a constant
+    (SURVEY.md §8(f) NEXT-3): per channel (last axis), wrap_cap(sign * scale +
+    bias) with scale = v * 2^s (s >= 0) or floor(v / 2^-s) (s < 0)."""
+    v = np.asarray(v, dtype=np.int64)
+    shift = np.asarray(shift, dtype=np.int64)
+    sign = np.where(np.asarray(neg, dtype=np.int64) != 0, -1, 1)
+    scaled = np.where(shift >= 0, v * (2 ** np.maximum(shift, 0)),
+                      np.right_shift(v, np.maximum(-shift, 0)))
+    return wrap(sign * scaled + np.asarray(bias, dtype=np.int64), cap)
+
+
 def maxpool2x2(v):
     v = np.asarray(v, dtype=np.int64)
     H, W = v.shape[0] // 2 * 2, v.shape[1] // 2 * 2
@@ -164,3 +176,17 @@ def config4(px, w1, w2, w3, w4, cap=16):
     h = relu(conv(h, w3, 1, 1, cap))
     h = maxpool2x2(h)
     return fc(h.ravel(), w4, cap)
+
+
+def dshe(px, blocks, fc1, fc2, cap=16):
+    """DSHE-style deeper net (PAPER.md T3 :202-203, [C-B-A-C-B-A-P] x k - F - F;
+    SURVEY.md §8(f) NEXT-3): blocks = [(wa, bna, wb, bnb), ...] with 3x3 'same'
+    convs, BN lowered to shift + constant, ReLU, 2x2 max-pool; then FC + ReLU,
+    FC (logits)."""
+    h = np.asarray(px, dtype=np.int64)
+    for wa, bna, wb, bnb in blocks:
+        h = relu(bn_shift_add(conv(h, wa, 1, 1, cap), *bna, cap))
+        h = relu(bn_shift_add(conv(h, wb, 1, 1, cap), *bnb, cap))
+        h = maxpool2x2(h)
+    h = relu(fc(h.ravel(), fc1, cap))
+    return fc(h, fc2, cap)

@@ -649,6 +649,85 @@ she_status relu_common(size_t words, int width, int rank, int world, Executor& e
                    ex, st);
 }
 
+// Batch normalisation lowered to a power-of-two scale and a constant
+// (SURVEY.md §8(f) NEXT-3; the B layers of PAPER.md T3, :202-203):
+//   y = wrap_cap(sign * scale(x, s) + bias),  scale(x, s) = x 2^s (s >= 0) or
+//   floor(x / 2^-s) (s < 0)
+// The scale is rewiring, the sign NOT flags plus a carry-in, the bias an adder
+// against constant bits (constant folding leaves ~2 gates per bit).
+struct BnGeom {
+  size_t words;
+  int C, w_in, in_signed, cap, relu;
+  const int8_t* shift;   // [C], in [-8, 8]
+  const uint8_t* neg;    // [C], 0 / 1 (may be NULL: all positive)
+  const int32_t* bias;   // [C]
+};
+
+int bits_signed(int64_t v) {  // two's-complement width of a constant
+  int w = 1;
+  while (w < 40 && (v < -(int64_t(1) << (w - 1)) || v >= (int64_t(1) << (w - 1)))) ++w;
+  return w;
+}
+
+int bn_scaled_width(const BnGeom& g, int ch) {
+  const int s = g.shift[ch];
+  const int base = g.in_signed ? g.w_in : g.w_in + 1;  // with the (constant-0) sign bit
+  return std::max(1, base + s);
+}
+
+int bn_width(const BnGeom& g, int ch) {
+  const int w = std::max(bn_scaled_width(g, ch), bits_signed(g.bias[ch])) + 1;
+  const int y = std::min(w, g.cap);
+  return g.relu ? std::max(1, y - 1) : y;
+}
+
+Word bn_word(const BnGeom& g, Circuit& c, const Word& x, int ch) {
+  const int s = g.shift[ch];
+  Word v = x;  // LSB first
+  if (!g.in_signed) v.push_back(F);
+  if (s > 0) v.insert(v.begin(), (size_t)s, F);
+  if (s < 0) {
+    const size_t drop = (size_t)(-s);
+    if (drop >= v.size()) v = Word{v.back()};
+    else v.erase(v.begin(), v.begin() + (long)drop);
+  }
+  if ((int)v.size() > g.cap) v.resize(g.cap);
+  const bool ng = g.neg && g.neg[ch];
+  const int width = std::min(std::max((int)v.size(), bits_signed(g.bias[ch])) + 1, g.cap);
+  Word k(width);
+  for (int i = 0; i < width; ++i) k[i] = ((int64_t)g.bias[ch] >> std::min(i, 39)) & 1 ? T : F;
+  Word y = c.add(ng ? c.neg_bits(v) : v, k, ng ? T : F, width);  // -v = !v + 1
+  return g.relu ? relu(c, y.size() > 1 ? y : Word{y[0], y[0]}) : y;
+}
+
+she_status bn_common(const BnGeom& g, int* w_out, int rank, int world, Executor* ex,
+                     she_circuit_stats* st) {
+  if (!g.shift || !g.bias || !w_out) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if (g.C <= 0 || g.w_in <= 0 || g.w_in > 32 || g.cap < 2 || g.cap > 32 || g.words % g.C)
+    return she::fail(SHE_ERR_SHAPE, "bad batch-norm shape");
+  int w = 1;
+  for (int ch = 0; ch < g.C; ++ch) {
+    if (g.shift[ch] < -8 || g.shift[ch] > 8)
+      return she::fail(SHE_ERR_ARG, "BN shift %d out of [-8, 8]", g.shift[ch]);
+    if (g.bias[ch] < -(1 << 20) || g.bias[ch] > (1 << 20))
+      return she::fail(SHE_ERR_ARG, "BN bias %d out of [-2^20, 2^20]", g.bias[ch]);
+    w = std::max(w, bn_width(g, ch));
+  }
+  if (!ex) {
+    *w_out = w;
+    return SHE_OK;
+  }
+  if (*w_out < w) return she::fail(SHE_ERR_SHAPE, "output word capacity %d < width %d", *w_out, w);
+  *w_out = w;
+  return run_layer(g.words, w, g.relu == 0, rank, world,
+                   [&](Circuit& c, InputMap& im, uint64_t q) {
+                     Word x(g.w_in);
+                     for (int b = 0; b < g.w_in; ++b) x[b] = im((uint32_t)(q * g.w_in + b));
+                     return bn_word(g, c, x, (int)(q % g.C));
+                   },
+                   *ex, st);
+}
+
 she_status maxpool_common(int H, int W, int C, int w, int in_signed, int rank, int world,
                           Executor& ex, she_circuit_stats* st) {
   if (H < 2 || W < 2 || C <= 0 || w <= 0) return she::fail(SHE_ERR_SHAPE, "bad maxpool shape");
@@ -752,6 +831,23 @@ she_status she_relu(she_ctx* ctx, const uint32_t* in, size_t words, int width, u
                      she::engine_stats(ctx, true));
 }
 
+she_status she_bn_shift_add(she_ctx* ctx, const uint32_t* in, size_t words, int C, int w_in,
+                            int in_signed, const int8_t* shift, const uint8_t* neg,
+                            const int32_t* bias, int acc_cap, int relu_, uint32_t* out,
+                            int* w_out, void* stream) {
+  BnGeom g{words, C, w_in, in_signed, acc_cap, relu_, shift, neg, bias};
+  if (!out) return bn_common(g, w_out, 0, 1, nullptr, nullptr);
+  if (words == 0) return SHE_OK;
+  if (!ctx || !in) return she::fail(SHE_ERR_ARG, "NULL argument");
+  GpuExec ex;
+  ex.ctx = ctx;
+  ex.in = in;
+  ex.out = out;
+  ex.stream = stream;
+  she_circuit_stats* st = she::engine_stats(ctx, true);
+  return bn_common(g, w_out, she::engine_rank(ctx), she::engine_world(ctx), &ex, st);
+}
+
 she_status she_maxpool2x2(she_ctx* ctx, const uint32_t* in, int H, int W, int C, int w,
                           int in_signed, uint32_t* out, void* stream) {
   if (!ctx || !in || !out) return she::fail(SHE_ERR_ARG, "NULL argument");
@@ -840,6 +936,22 @@ she_status she_clear_relu(const uint8_t* in, size_t words, int width, uint8_t* o
   ex.in = in;
   ex.out = out;
   return relu_common(words, width, rank, world, ex, st);
+}
+
+she_status she_clear_bn_shift_add(const uint8_t* in, size_t words, int C, int w_in,
+                                  int in_signed, const int8_t* shift, const uint8_t* neg,
+                                  const int32_t* bias, int acc_cap, int relu_, uint8_t* out,
+                                  int* w_out, int rank, int world, she_circuit_stats* st) {
+  BnGeom g{words, C, w_in, in_signed, acc_cap, relu_, shift, neg, bias};
+  if (st) *st = she_circuit_stats{};
+  if (!out) return bn_common(g, w_out, 0, 1, nullptr, nullptr);
+  if (words == 0) return SHE_OK;
+  if (!in) return she::fail(SHE_ERR_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return she::fail(SHE_ERR_ARG, "bad rank/world");
+  ClearExec ex;
+  ex.in = in;
+  ex.out = out;
+  return bn_common(g, w_out, rank, world, &ex, st);
 }
 
 she_status she_clear_maxpool2x2(const uint8_t* in, int H, int W, int C, int w, int in_signed,

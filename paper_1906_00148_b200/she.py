@@ -106,6 +106,13 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_relu": ([_vp, _vp, _sz, ctypes.c_int, _vp, _vp], ctypes.c_int),
+            "she_bn_shift_add": ([_vp, _vp, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                  _vp, _vp, ctypes.c_int, ctypes.c_int, _vp,
+                                  ctypes.POINTER(ctypes.c_int), _vp], ctypes.c_int),
+            "she_clear_bn_shift_add": ([_vp, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                        _vp, _vp, ctypes.c_int, ctypes.c_int, _vp,
+                                        ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_ctx_capture": ([_vp, ctypes.c_uint64, ctypes.c_uint32, _sz], ctypes.c_int),
@@ -517,4 +524,51 @@ def clear_fc_mul_acc(bits, K, w_in, in_signed, wm, cap=16, relu=False, rank=0, w
     _check(lib().she_clear_fc_mul_acc(_np_ptr(bits), K, w_in, int(in_signed), _np_ptr(wm), M, cap,
                                       int(relu), _np_ptr(out), ctypes.byref(w), rank, world,
                                       ctypes.byref(st)))
+    return out, w.value, st.as_dict()
+
+
+# ---- batch normalisation as shift + constant (she.h she_bn_shift_add) --------
+
+def _bn_args(shift, neg, bias):
+    shift = np.ascontiguousarray(shift, dtype=np.int8)
+    neg = np.ascontiguousarray(np.zeros_like(shift, dtype=np.uint8) if neg is None else neg,
+                               dtype=np.uint8)
+    bias = np.ascontiguousarray(bias, dtype=np.int32)
+    return shift, neg, bias
+
+
+def bn_width(words, C, w_in, in_signed, shift, neg, bias, cap=16, relu=False) -> int:
+    shift, neg, bias = _bn_args(shift, neg, bias)
+    w = ctypes.c_int(0)
+    _check(lib().she_bn_shift_add(None, None, words, C, w_in, int(in_signed), _np_ptr(shift),
+                                  _np_ptr(neg), _np_ptr(bias), cap, int(relu), None,
+                                  ctypes.byref(w), None))
+    return w.value
+
+
+def she_bn_shift_add(ctx: Context, x, words, C, w_in, in_signed, shift, neg, bias, cap=16,
+                     relu=False, out=None, stream=None):
+    """x: device [words][w_in][stride] (HWC); returns (out [words][w][stride], w)."""
+    import torch
+    shift, neg, bias = _bn_args(shift, neg, bias)
+    w = ctypes.c_int(bn_width(words, C, w_in, in_signed, shift, neg, bias, cap, relu))
+    if out is None:
+        out = torch.zeros((words, w.value, ctx.stride), dtype=torch.int32, device=x.device)
+    _check(lib().she_bn_shift_add(ctx.handle, _dev_ptr(x), words, C, w_in, int(in_signed),
+                                  _np_ptr(shift), _np_ptr(neg), _np_ptr(bias), cap, int(relu),
+                                  _dev_ptr(out), ctypes.byref(w), _stream_ptr(stream)))
+    return out, w.value
+
+
+def clear_bn_shift_add(bits, words, C, w_in, in_signed, shift, neg, bias, cap=16, relu=False,
+                       rank=0, world=1):
+    shift, neg, bias = _bn_args(shift, neg, bias)
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    w = ctypes.c_int(bn_width(words, C, w_in, in_signed, shift, neg, bias, cap, relu))
+    out = np.zeros((words, w.value), dtype=np.uint8)
+    st = she_circuit_stats()
+    _check(lib().she_clear_bn_shift_add(_np_ptr(bits), words, C, w_in, int(in_signed),
+                                        _np_ptr(shift), _np_ptr(neg), _np_ptr(bias), cap,
+                                        int(relu), _np_ptr(out), ctypes.byref(w), rank, world,
+                                        ctypes.byref(st)))
     return out, w.value, st.as_dict()

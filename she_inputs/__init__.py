@@ -204,3 +204,15 @@ def tcn_weights(cfg: int, shape, layer: int = 0) -> np.ndarray:
     t = ((r >> np.uint64(16)) & np.uint64(0xFFFFFF)).astype(np.float64) / 2.0 ** 24 * 8.0 - 0.5
     mag = np.clip(np.rint(2.0 ** (7.0 - t)), 1, 255).astype(np.int64)
     return np.where(zero, 0, sign * mag).astype(np.int16).reshape(shape)
+
+
+def bn_params(cfg: int, C: int, layer: int = 0):
+    """Synthetic batch-norm folding for the BN layers:
+    per channel a power-of-two scale shift in [-2, 1], a sign flip w.p. 1/8 and
+    an integer bias uniform in [-64, 64]."""
+    base = (np.uint64(1) << np.uint64(52)) + (np.uint64(layer) << np.uint64(40))
+    r = rng_u64(weight_seed(cfg), STREAM_WEIGHTS, base + np.arange(C, dtype=np.uint64))
+    shift = ((r & np.uint64(3)).astype(np.int64) - 2).astype(np.int8)
+    neg = (((r >> np.uint64(8)) & np.uint64(7)) == 0).astype(np.uint8)
+    bias = (((r >> np.uint64(16)) % np.uint64(129)).astype(np.int64) - 64).astype(np.int32)
+    return shift, neg, bias

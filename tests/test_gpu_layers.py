@@ -328,3 +328,45 @@ def test_tcn_config2_shape_at_default_params(cuda):
     h, w = she.she_conv_mul_acc(e.ctx, x, 28, 28, 1, 8, False, m1, 2, 0, 16, relu=True)
     assert np.array_equal(net.value_of(e.decrypt_bits(h), signed=False),
                           net.relu(net.conv_tcn(px, m1, 2, 0, 16)))
+
+
+# ----------------------------------------------------------------------------
+# NEXT-3: batch norm as shift + constant, a DSHE-style deeper chain (C0)
+# ----------------------------------------------------------------------------
+
+def test_bn_and_dshe_chain_c0(cuda):
+    e = env(0)
+    rng = np.random.default_rng(31)
+    C, words, w_in = 3, 12, 9
+    x = rng.integers(-(1 << 8), 1 << 8, words)
+    shift = np.array([-2, 0, 3], np.int8)
+    neg = np.array([0, 1, 0], np.uint8)
+    bias = np.array([17, -40, 5], np.int32)
+    ct, _ = e.encrypt_words(x, w_in, 3131)
+    she.capture(e.ctx, si.sample_seed(0) + 9, 11, 64)
+    y, w = she.she_bn_shift_add(e.ctx, ct, words, C, w_in, True, shift, neg, bias, cap=14)
+    want = net.bn_shift_add(x.reshape(-1, C), shift, neg, bias, 14).ravel()
+    assert np.array_equal(net.value_of(e.decrypt_bits(y), signed=True), want)
+    check_captured(e, 4)
+    she.capture(e.ctx, 0, 0, 0)
+    # [C-B-A-C-B-A-P] x 1 - F - F on an 6x6 input, 2 channels
+    px = rng.integers(0, 256, (6, 6, 1))
+    wa = si.log_quant_weights(5, (2, 3, 3, 1), layer=70)
+    wb = si.log_quant_weights(5, (2, 3, 3, 2), layer=71)
+    bna, bnb = si.bn_params(5, 2, 70), si.bn_params(5, 2, 71)
+    fc1 = si.log_quant_weights(5, (4, 3 * 3 * 2), layer=72)
+    fc2 = si.log_quant_weights(5, (3, 4), layer=73)
+    h, _ = e.encrypt_words(px, 8, 3232)
+    Hc, Cc, wc, sg = 6, 1, 8, False
+    for wq, bn in ((wa, bna), (wb, bnb)):
+        h, wc = she.she_conv_shift_acc(e.ctx, h, Hc, Hc, Cc, wc, sg, wq, 1, 1, 16)
+        Cc = wq.shape[0]
+        h, wc = she.she_bn_shift_add(e.ctx, h.reshape(-1, wc, e.P.stride), Hc * Hc * Cc, Cc, wc,
+                                     True, *bn, cap=16, relu=True)
+        h, sg = h.reshape(Hc, Hc, Cc, wc, e.P.stride), False
+    h = she.she_maxpool2x2(e.ctx, h, 6, 6, 2, wc, False)
+    h, w1 = she.she_fc_shift_acc(e.ctx, h.reshape(-1, wc, e.P.stride), 18, wc, False, fc1, 16,
+                                 relu=True)
+    o, w2 = she.she_fc_shift_acc(e.ctx, h, 4, w1, False, fc2, 16)
+    want = net.dshe(px, [(wa, bna, wb, bnb)], fc1, fc2)
+    assert np.array_equal(net.value_of(e.decrypt_bits(o), signed=True), want)
