@@ -167,6 +167,27 @@ def test_ragged_batches_and_uniform_ops(env0, count):
         assert np.array_equal(got, ref), si.OP_NAMES[op]
 
 
+def test_batch_larger_than_one_launch(env0):
+    """Maximum-size path: more gates than one BR+KS launch pair takes (65536,
+    csrc/engine.cu kChunk), mixed ops, ragged tail.  Every output decrypts to
+    the truth table; a seed-sampled subset on both sides of each chunk seam is
+    recomputed by the oracle word for word."""
+    P = env0.P
+    count = 2 * 65536 + 77
+    rng = np.random.default_rng(65537)
+    ops = rng.choice(si.BOOTSTRAPPED_MIX, count).astype(np.uint8)
+    bits = rng.integers(0, 2, (count, 3)).astype(np.uint8)
+    cts = she.she_encrypt_bits(env0.sk, bits.ravel(), 6553).reshape(count, 3, P.stride)
+    a, b, c = (cts[:, j].copy() for j in range(3))
+    out = env0.run_ops(ops, a, b, c)
+    want = np.array([si.truth(o, *bb) for o, bb in zip(ops, bits)])
+    assert np.array_equal(she.she_decrypt_bits(env0.sk, out), want)
+    pick = np.unique(np.concatenate([[0, 65535, 65536, 131071, 131072, count - 1],
+                                     rng.choice(count, 10, replace=False)]))
+    ref = oracle.gates(env0.K, ops[pick], a[pick], b[pick], c[pick])
+    assert np.array_equal(out[pick], ref)
+
+
 def test_mux_aliased_inputs(env0):
     P = env0.P
     bits = np.array([0, 1, 1, 0], np.uint8)
