@@ -105,14 +105,6 @@ __host__ __device__ __forceinline__ uint64_t reduce128(uint64_t lo, uint64_t hi)
   return r;
 }
 
-// (x2:x1:x0) 96-bit value (x2 < 2^32) mod p: lo + x2 (2^32 - 1).
-__host__ __device__ __forceinline__ uint64_t reduce96(uint64_t lo, uint64_t x2) {
-  uint64_t t1 = (x2 << 32) - x2;
-  uint64_t r = lo + t1;
-  if (r < t1) r += EPS;
-  return r;
-}
-
 __host__ __device__ __forceinline__ uint64_t mul(uint64_t a, uint64_t b) {
   return reduce128(a * b, mulhi(a, b));
 }
@@ -132,96 +124,6 @@ __host__ __device__ __forceinline__ uint64_t reduce128_le(uint64_t lo, uint64_t 
 
 __host__ __device__ __forceinline__ uint64_t mul_le(uint64_t a, uint64_t b) {
   return reduce128_le(a * b, mulhi(a, b));
-}
-
-// x * 2^32 mod p: x1 2^64 + x0 2^32 = x1 (2^32 - 1) + x0 2^32.
-__host__ __device__ __forceinline__ uint64_t mul_2_32(uint64_t x) {
-  return reduce96(x << 32, x >> 32);
-}
-
-// x * 2^s mod p for 0 <= s < 96, as a non-negative lazy value.
-// Write y = x * 2^(s mod 32) exactly as 96 bits (w2:w1:w0), w2 < 2^31, then
-// fold the powers 2^64 = 2^32 - 1, 2^96 = -1, 2^128 = -2^32:
-//   s in [0, 32):   y              = (w1:w0) + w2 EPS
-//   s in [32, 64):  y 2^32         = (w0 << 32) + w1 EPS - w2
-//   s in [64, 96):  y 2^64         = w0 EPS - (w2:w1)
-// Each case needs at most one carry and one borrow fold (bounds in DESIGN.md).
-// x + y with ONE carry fold (callers guarantee no second wrap).
-__host__ __device__ __forceinline__ uint64_t add_fold1(uint64_t x, uint64_t y) {
-#if defined(__CUDA_ARCH__) && defined(GL_ADDSUB_PTX)
-  uint32_t s0, s1, c;
-  asm("add.cc.u32 %0, %3, %5;\n\t"
-      "addc.cc.u32 %1, %4, %6;\n\t"
-      "addc.u32 %2, 0, 0;\n\t"
-      "mad.lo.cc.u32 %0, %2, 0xFFFFFFFF, %0;\n\t"
-      "madc.hi.u32 %1, %2, 0xFFFFFFFF, %1;"
-      : "=&r"(s0), "=&r"(s1), "=&r"(c)
-      : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32)));
-  return ((uint64_t)s1 << 32) | s0;
-#else
-  uint64_t v = x + y;
-  if (v < y) v += EPS;
-  return v;
-#endif
-}
-
-// x - y with ONE borrow fold (+p; callers guarantee no second borrow).
-__host__ __device__ __forceinline__ uint64_t sub_fold1(uint64_t x, uint64_t y) {
-#if defined(__CUDA_ARCH__) && defined(GL_ADDSUB_PTX)
-  uint32_t d0, d1, bw;
-  asm("sub.cc.u32 %0, %3, %5;\n\t"
-      "subc.cc.u32 %1, %4, %6;\n\t"
-      "subc.u32 %2, 0, 0;\n\t"
-      "sub.cc.u32 %0, %0, %2;\n\t"
-      "subc.u32 %1, %1, 0;"
-      : "=&r"(d0), "=&r"(d1), "=&r"(bw)
-      : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32)));
-  return ((uint64_t)d1 << 32) | d0;
-#else
-  uint64_t d = x - y;
-  if (x < y) d -= EPS;
-  return d;
-#endif
-}
-
-__host__ __device__ __forceinline__ uint64_t mul_pow2_pos(uint64_t x, int s) {
-  if (s == 0) return x;
-  const int r = s & 31;
-  const uint32_t x0 = (uint32_t)x, x1 = (uint32_t)(x >> 32);
-  uint32_t w0, w1, w2;
-  if (r == 0) {
-    w0 = x0;
-    w1 = x1;
-    w2 = 0;
-  } else {
-#if defined(__CUDA_ARCH__) && defined(GL_ADDSUB_PTX)
-    // x * 2^r as two IMAD.WIDE on the FMA pipe (instead of funnel shifts)
-    uint64_t P, W;
-    const uint32_t m = 1u << r;
-    asm("mul.wide.u32 %0, %1, %2;" : "=l"(P) : "r"(x0), "r"(m));
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(W) : "r"(x1), "r"(m), "l"(P >> 32));
-#else
-    const uint64_t P = (uint64_t)x0 << r;                  // x0 2^r
-    const uint64_t W = ((uint64_t)x1 << r) + (P >> 32);    // (w2:w1), < 2^63
-#endif
-    w0 = (uint32_t)P;
-    w1 = (uint32_t)W;
-    w2 = (uint32_t)(W >> 32);
-  }
-  if (s < 32) {  // (w1:w0) + w2 EPS; after a carry the sum is < w2 EPS < 2^63
-    return add_fold1(((uint64_t)w1 << 32) | w0, ((uint64_t)w2 << 32) - w2);
-  }
-  if (s < 64) {  // (w0 << 32) + w1 EPS - w2; after the carry fold v < 2^64 - 2^32
-    const uint64_t v = add_fold1((uint64_t)w0 << 32, ((uint64_t)w1 << 32) - w1);
-    return sub_fold1(v, w2);  // v - w2 >= -2^31: one borrow at most
-  }
-  // 64 <= s < 96: w0 EPS - (w2:w1); w0 EPS < p, (w2:w1) < 2^63
-  return sub_fold1(((uint64_t)w0 << 32) - w0, ((uint64_t)w2 << 32) | w1);
-}
-
-// x * 2^s mod p for 0 <= s < 192 (2^96 = -1).
-__host__ __device__ __forceinline__ uint64_t mul_pow2(uint64_t x, int s) {
-  return s >= 96 ? neg(mul_pow2_pos(x, s - 96)) : mul_pow2_pos(x, s);
 }
 
 // ---- butterfly primitives with a bounded twiddle product ----
@@ -357,6 +259,12 @@ __host__ __device__ __forceinline__ uint64_t shl_le(uint64_t v, const int s) {
   const uint64_t Lv = Hh - G;
   return (T0 < T2 || Hh < G) ? Lv - EPS : Lv;
 #endif
+}
+
+// x * 2^s mod p for 0 <= s < 192 (2^96 = -1): the bounded product, negated
+// for s >= 96 (setup and tests; the butterflies fold the sign into +/-).
+__host__ __device__ __forceinline__ uint64_t mul_pow2(uint64_t x, int s) {
+  return s >= 96 ? neg(shl_le(x, s - 96)) : shl_le(x, s);
 }
 
 __host__ __device__ inline uint64_t pow(uint64_t b, uint64_t e) {
