@@ -132,6 +132,14 @@ she_status she_ctx_timing(she_ctx* ctx, int reset, double* br_ms, double* ks_ms,
  * kernel's own field multiplication on every SM; the roofline denominator). */
 she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms);
 
+/* Test instrumentation: evaluate the device Goldilocks primitives (hand-written
+ * PTX carry chains) on n input triples (HOST buffers a, b: uint64[n]; c:
+ * uint32[n]) and return out[n][104]: add, sub, add_le, sub_le (y = b), mul,
+ * mul_le, reduce128_le(lo = a, hi = b), reduce_acc_le(a, b, top = c & 3),
+ * shl_le(a, s) for s = 0..95.  Results are lazy residues (the *_le ones <= p). */
+she_status she_field_selftest(int device, const uint64_t* a, const uint64_t* b, const uint32_t* c,
+                              size_t n, uint64_t* out);
+
 /* Bootstrapped gates, all with the same op (north_star signature).  a, b, c,
  * out: device, count slots each (c read only for MUX, b not read for
  * NOT/COPY; unused pointers may be NULL).  out must not overlap any input.

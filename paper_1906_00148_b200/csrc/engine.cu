@@ -559,6 +559,32 @@ __global__ void modmul_peak_kernel(uint64_t* sink, uint32_t iters, uint64_t seed
   if (r == 0x12345) sink[0] = r;  // keep the work alive
 }
 
+// Test instrumentation: the device field primitives on caller-given inputs,
+// so that their rare carry / borrow branches (hand-written PTX) are checked
+// against exact arithmetic on edge values (tests/test_gpu_gates.py).
+constexpr int kSelftestOps = 8 + 96;
+__global__ void field_selftest_kernel(const uint64_t* a, const uint64_t* b, const uint32_t* c,
+                                      size_t n, uint64_t* out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t x = a[i], y = b[i];
+  uint64_t* o = out + i * kSelftestOps;
+  o[0] = gl::add(x, y);
+  o[1] = gl::sub(x, y);
+  o[2] = gl::add_le(x, y);
+  o[3] = gl::sub_le(x, y);
+  o[4] = gl::mul(x, y);
+  o[5] = gl::mul_le(x, y);
+  o[6] = gl::reduce128_le(x, y);
+  gl::Acc3 A;
+  A.lo = x;
+  A.hi = y;
+  A.top = c[i] & 3u;
+  o[7] = gl::reduce_acc_le(A);
+#pragma unroll
+  for (int s = 0; s < 96; ++s) o[8 + s] = gl::shl_le(x, s);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -957,6 +983,34 @@ she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms) {
   if (modmul_per_s) *modmul_per_s = total / (best * 1e-3);
   if (ms) *ms = best;
   return SHE_OK;
+}
+
+she_status she_field_selftest(int device, const uint64_t* a, const uint64_t* b, const uint32_t* c,
+                              size_t n, uint64_t* out) {
+  if (n == 0) return SHE_OK;
+  if (!a || !b || !c || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  CK(cudaSetDevice(device));
+  uint64_t *da = nullptr, *db = nullptr, *dout = nullptr;
+  uint32_t* dc = nullptr;
+  she_status st = SHE_OK;
+  cudaError_t e = cudaMalloc(&da, n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&db, n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&dc, n * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, n * 8 * kSelftestOps);
+  if (e == cudaSuccess) e = cudaMemcpy(da, a, n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(db, b, n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dc, c, n * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    field_selftest_kernel<<<(unsigned)((n + 127) / 128), 128>>>(da, db, dc, n, dout);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, n * 8 * kSelftestOps, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) st = cuda_fail(e, "field selftest");
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(dc);
+  cudaFree(dout);
+  return st;
 }
 
 she_status she_ctx_synchronize(she_ctx* ctx) {

@@ -114,12 +114,35 @@ __host__ __device__ __forceinline__ uint64_t mul(uint64_t a, uint64_t b) {
 // instruction; w = t0 + hl EPS + EPS with carry c gives c ? w : w - EPS
 // (c: w < hl EPS + EPS <= 2^64 - 2^32; !c: w - EPS <= 2^64 - 1 - EPS = p - 1).
 __host__ __device__ __forceinline__ uint64_t reduce128_le(uint64_t lo, uint64_t hi) {
+#if defined(__CUDA_ARCH__)
+  // carry/borrow chains instead of 64-bit compares and selects
+  const uint32_t l0 = (uint32_t)lo, l1 = (uint32_t)(lo >> 32);
+  const uint32_t h0 = (uint32_t)hi, h1 = (uint32_t)(hi >> 32);
+  uint32_t t0, t1, bw, w0, w1, c, e0, e1, r0, r1;
+  asm("sub.cc.u32 %0, %10, %13;\n\t"        // t = lo - hh
+      "subc.cc.u32 %1, %11, 0;\n\t"
+      "subc.u32 %2, 0, 0;\n\t"              // -borrow
+      "sub.cc.u32 %0, %0, %2;\n\t"          // + p on a borrow (- EPS mod 2^64)
+      "subc.u32 %1, %1, 0;\n\t"
+      "add.cc.u32 %3, %0, %14;\n\t"         // w = t + (hl : ~hl) = t + hl EPS + EPS
+      "addc.cc.u32 %4, %1, %12;\n\t"
+      "addc.u32 %5, 0, 0;\n\t"              // c
+      "add.cc.u32 %6, %3, 1;\n\t"           // e = w - EPS
+      "addc.u32 %7, %4, 0xFFFFFFFF;\n\t"
+      "mad.lo.cc.u32 %8, %5, 0xFFFFFFFF, %6;\n\t"  // c ? w : e  =  e + c EPS
+      "madc.hi.u32 %9, %5, 0xFFFFFFFF, %7;"
+      : "=&r"(t0), "=&r"(t1), "=&r"(bw), "=&r"(w0), "=&r"(w1), "=&r"(c), "=&r"(e0), "=&r"(e1),
+        "=&r"(r0), "=&r"(r1)
+      : "r"(l0), "r"(l1), "r"(h0), "r"(h1), "r"(~h0));
+  return ((uint64_t)r1 << 32) | r0;
+#else
   const uint64_t hh = hi >> 32, hl = hi & 0xFFFFFFFFull;
   uint64_t t0 = lo - hh;
   if (lo < hh) t0 -= EPS;  // borrow: + p (cannot borrow again)
   const uint64_t t1 = (hl << 32) | (~hl & 0xFFFFFFFFull);
   const uint64_t w = t0 + t1;
   return w < t1 ? w : w - EPS;
+#endif
 }
 
 __host__ __device__ __forceinline__ uint64_t mul_le(uint64_t a, uint64_t b) {
@@ -304,10 +327,22 @@ __host__ __device__ __forceinline__ void mac(Acc3& A, uint64_t a, uint64_t b) {
 // As reduce_acc with the result <= p (r <= p; r - t + p <= p when r < t).
 __host__ __device__ __forceinline__ uint64_t reduce_acc_le(const Acc3& A) {
   const uint64_t r = reduce128_le(A.lo, A.hi);
+#if defined(__CUDA_ARCH__)
+  uint32_t d0, d1, bw;
+  asm("sub.cc.u32 %0, %3, 0;\n\t"           // r - top 2^32
+      "subc.cc.u32 %1, %4, %5;\n\t"
+      "subc.u32 %2, 0, 0;\n\t"
+      "sub.cc.u32 %0, %0, %2;\n\t"          // + p on a borrow
+      "subc.u32 %1, %1, 0;"
+      : "=&r"(d0), "=&r"(d1), "=&r"(bw)
+      : "r"((uint32_t)r), "r"((uint32_t)(r >> 32)), "r"(A.top));
+  return ((uint64_t)d1 << 32) | d0;
+#else
   const uint64_t t = (uint64_t)A.top << 32;  // top <= 3
   uint64_t d = r - t;
   if (r < t) d -= EPS;
   return d;
+#endif
 }
 
 __host__ __device__ __forceinline__ uint64_t reduce_acc(const Acc3& A) {

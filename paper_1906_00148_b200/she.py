@@ -115,6 +115,7 @@ def lib() -> ctypes.CDLL:
                                         ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
+            "she_field_selftest": ([ctypes.c_int, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
             "she_ctx_capture": ([_vp, ctypes.c_uint64, ctypes.c_uint32, _sz], ctypes.c_int),
             "she_ctx_capture_read": ([_vp, _vp, _vp, _sz, ctypes.POINTER(_sz)], ctypes.c_int),
             "she_clear_conv_shift_acc": ([_vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
@@ -572,3 +573,13 @@ def clear_bn_shift_add(bits, words, C, w_in, in_signed, shift, neg, bias, cap=16
                                         int(relu), _np_ptr(out), ctypes.byref(w), rank, world,
                                         ctypes.byref(st)))
     return out, w.value, st.as_dict()
+
+
+def field_selftest(device: int, a, b, c) -> np.ndarray:
+    """Device field primitives on (a, b, c) triples (test instrumentation, she.h)."""
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    b = np.ascontiguousarray(b, dtype=np.uint64)
+    c = np.ascontiguousarray(c, dtype=np.uint32)
+    out = np.zeros((len(a), 104), dtype=np.uint64)
+    _check(lib().she_field_selftest(device, _np_ptr(a), _np_ptr(b), _np_ptr(c), len(a), _np_ptr(out)))
+    return out

@@ -167,13 +167,44 @@ def test_ragged_batches_and_uniform_ops(env0, count):
         assert np.array_equal(got, ref), si.OP_NAMES[op]
 
 
+def test_device_field_primitives_edge_values(cuda):
+    """The hand-written PTX carry/borrow chains of the device Goldilocks
+    primitives on edge values that reach their rare branches (a borrow of
+    lo - hi_hi, the second fold, inputs in (p, 2^64)), against exact integer
+    arithmetic, with the <= p bound of the *_le results."""
+    P64 = 2 ** 64 - 2 ** 32 + 1
+    edge = [0, 1, 2, 2 ** 32 - 2, 2 ** 32 - 1, 2 ** 32, 2 ** 32 + 1, P64 - 2, P64 - 1, P64,
+            P64 + 1, 2 ** 64 - 2, 2 ** 64 - 1, 2 ** 63, 2 ** 63 - 1, 0xFFFFFFFF00000000,
+            0xFFFFFFFEFFFFFFFF, 0x80000000FFFFFFFF, 0x00000001FFFFFFFF, 0x00000000FFFFFFFE]
+    rng = np.random.default_rng(77)
+    rand = [int(v) for v in rng.integers(0, 2 ** 64 - 1, 40, dtype=np.uint64)]
+    vals = edge + rand
+    pairs = [(x, y) for x in vals for y in vals]
+    a = np.array([x for x, _ in pairs], np.uint64)
+    b = np.array([y for _, y in pairs], np.uint64)
+    c = np.arange(len(pairs), dtype=np.uint32)
+    out = she.field_selftest(0, a, b, c)
+    for k, (x, y) in enumerate(pairs):
+        o = [int(v) for v in out[k]]
+        assert o[0] % P64 == (x + y) % P64 and o[1] % P64 == (x - y) % P64
+        if y <= P64:
+            assert o[2] % P64 == (x + y) % P64 and o[3] % P64 == (x - y) % P64
+        assert o[4] % P64 == x * y % P64
+        assert o[5] <= P64 and o[5] % P64 == x * y % P64
+        assert o[6] <= P64 and o[6] % P64 == (x + y * 2 ** 64) % P64
+        top = k & 3
+        assert o[7] <= P64 and o[7] % P64 == (x + y * 2 ** 64 + top * 2 ** 128) % P64
+        for s_ in range(96):
+            assert o[8 + s_] <= P64 and o[8 + s_] % P64 == x * pow(2, s_, P64) % P64, (x, s_)
+
+
 def test_batch_larger_than_one_launch(env0):
     """Maximum-size path: more gates than one BR+KS launch pair takes (65536,
     csrc/engine.cu kChunk), mixed ops, ragged tail.  Every output decrypts to
     the truth table; a seed-sampled subset on both sides of each chunk seam is
     recomputed by the oracle word for word."""
     P = env0.P
-    count = 2 * 65536 + 77
+    count = 2 * 65536 + 76  # ragged (not a multiple of the launch size), 4-byte aligned ops
     rng = np.random.default_rng(65537)
     ops = rng.choice(si.BOOTSTRAPPED_MIX, count).astype(np.uint8)
     bits = rng.integers(0, 2, (count, 3)).astype(np.uint8)
