@@ -156,6 +156,14 @@ def read_profile_traffic():
 # ---------------------------------------------------------------------------
 # the product arm
 # ---------------------------------------------------------------------------
+def _logit_wrap_events(net, px, w1, w2, w3, tcn: bool) -> int:
+    """Logits of the config-3 net whose exact sum leaves the 16-bit cap (R13)."""
+    conv, fc = (net.conv_tcn, net.fc_tcn) if tcn else (net.conv, net.fc)
+    h = net.relu(conv(px, w1, 2, 0, 16))
+    h = net.relu(fc(h.ravel(), w2, 16))
+    return int(net.wrap_events(net.fc_exact(h, w3, net.term_tcn if tcn else None), 16))
+
+
 def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     """BASELINE.json's second metric: latency of the encrypted MNIST-shaped net
     (configs[3]: conv 5x5/2 1->5 + ReLU, FC 720->100 + ReLU, FC 100->10) at the
@@ -244,6 +252,7 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
             "levels": int(sum(s["levels"] for s in stats)),
             "br_lanes_total": int(lanes_total),
             "logits_match_plaintext_network": bool(np.array_equal(logits, want)),
+            "wrap16_events_in_logits": _logit_wrap_events(net, px, w1, w2, w3, tcn),
             "parallelism": f"neuron-sharded x{world}, {dist.get_backend()} all-gather between "
                            "layers" if world > 1 else "1 GPU"}
 
@@ -442,6 +451,7 @@ def run_she(args):
     dec = she.she_decrypt_bits(sk, h_out)
     want = np.array([si.truth(o, *b) for o, b in zip(ops, bits)])
     assert np.array_equal(dec, want), "decryption mismatch"
+    decrypted = {"decrypted_compared": int(COUNT), "decrypted_mismatches": int(np.sum(dec != want))}
     e2e = {"value": round(world * COUNT * args.steps / e2e_total, 2), "unit": UNIT,
            "h2d_bytes_per_step": int(COUNT + 3 * COUNT * stride * 4),
            "d2h_bytes_per_step": int(COUNT * stride * 4)}
@@ -454,6 +464,7 @@ def run_she(args):
                        "parallelism": f"gate-sharded x{world} (independent batches, no collective)",
                        "l2": "flushed between timed steps (256 MiB write), outside the event pairs"},
             "br_lanes_per_s": round(world * lanes * args.steps / (dev_ms * 1e-3), 1),
+            "parity": decrypted,
             "roofline": roof, "clocks": clk, "e2e": e2e,
             "gpu_launches": int(t["br_launches"] + t["ks_launches"]),
             "k6_modmul_peak_per_s": round(k6, 1)}
@@ -512,6 +523,13 @@ def cpu_baseline(args, gpu_out=None):
     if gpu_out is not None:
         bad = int(np.sum(np.any(gpu_out[:size] != ref, axis=1)))
         out["parity"] = {"ciphertexts_compared": size, "ciphertext_mismatches": bad}
+    import platform
+    try:
+        model = [ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo")
+                 if ln.startswith("model name")][0]
+    except (OSError, IndexError):
+        model = platform.processor()
+    out["cpu_model"] = model
     return out
 
 
