@@ -144,6 +144,17 @@ def roofline_peak(device: int, lib_path: str, sm_max_mhz: float | None):
     return peak, measured, derived, ipm, src
 
 
+def read_ncu_summary():
+    """Instruction-level evidence of the dominant kernel from the committed ncu
+    capture (profiles/ncu_summary.json): issue-slot and pipe utilisation."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            br = json.load(f)["br_kernel"]
+        return {k: br[k] for k in ("issue_active_pct", "alu_pipe_pct", "fma_pipe_pct")}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def read_profile_traffic():
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -425,7 +436,7 @@ def run_she(args):
             "kernel_ms_per_launch": round(br_ms_per_launch, 3),
             "kernel_share_of_step": round(t["br_ms"] / dev_ms, 4) if dev_ms else None,
             "ks_kernel_ms_per_launch": round(t["ks_ms"] / max(1, t["ks_launches"]), 3),
-            "peak_source": peak_src}
+            "peak_source": peak_src, "ncu_profile": read_ncu_summary()}
 
     # ---- end to end through the public host-buffer API (H2D + D2H inside) ----
     pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()

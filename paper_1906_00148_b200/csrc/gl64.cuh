@@ -360,8 +360,8 @@ __host__ __device__ __forceinline__ uint64_t from_i64(int64_t v) {
 
 // Centred lift of x in F_p to Z, reduced mod 2^32 (torus32).  Valid when the
 // exact integer has |value| < (p-1)/2.  (x - p) mod 2^32 = (x - 1) mod 2^32.
+// Any lazy x works: x >= p implies x > (p-1)/2 and (x - p) = x - 1 mod 2^32.
 __host__ __device__ __forceinline__ uint32_t lift32(uint64_t x) {
-  x = canon(x);
   return (uint32_t)x - (x > (P - 1) / 2 ? 1u : 0u);
 }
 
