@@ -202,7 +202,9 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     conv_w, fc_w = (she.conv_mul_width, she.fc_mul_width) if tcn else (she.conv_width, she.fc_width)
     stride = P.stride
     bits = net.bits_of(px, 8)
+    t_enc = time.perf_counter()  # client side (host): the paper's EDL column
     cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0)
+    t_enc = time.perf_counter() - t_enc
     x = torch.from_numpy(cts.view(np.int32)).cuda().reshape(28, 28, 1, 8, stride)
 
     from paper_1906_00148_b200.parallel import gather_shards, max_over_ranks, padded_words
@@ -247,8 +249,11 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
                          device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t)
         lanes_total = int(t.item())
-    logits = net.value_of(she.she_decrypt_bits(sk, lo[:10].cpu().numpy().view(np.uint32)
-                                               .reshape(-1, stride)).reshape(10, wc), signed=True)
+    out_cts = lo[:10].cpu().numpy().view(np.uint32).reshape(-1, stride)
+    t_dec = time.perf_counter()
+    dec_bits = she.she_decrypt_bits(sk, out_cts)
+    t_dec = time.perf_counter() - t_dec
+    logits = net.value_of(dec_bits.reshape(10, wc), signed=True)
     want = net.config3_tcn(px, w1, w2, w3) if tcn else net.config3(px, w1, w2, w3)
     stats = [s1, s2, s3]
     kind = ("TCN baseline: 8-bit fixed-point multipliers (shift-and-add)" if tcn
@@ -264,6 +269,11 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
             "br_lanes_total": int(lanes_total),
             "logits_match_plaintext_network": bool(np.array_equal(logits, want)),
             "wrap16_events_in_logits": _logit_wrap_events(net, px, w1, w2, w3, tcn),
+            "client": {"encrypt_s": round(t_enc, 4), "decrypt_s": round(t_dec, 5),
+                       "edl_s": round(t_enc + t_dec, 4),
+                       "msize_bytes": int(bits.size * (P.n + 1) * 4),
+                       "note": "host client (she_encrypt_bits / she_decrypt_bits): 784 pixels x 8 "
+                               "bit-wise LWE ciphertexts of n+1 = 501 words (PAPER.md:256 MSize)"},
             "parallelism": f"neuron-sharded x{world}, {dist.get_backend()} all-gather between "
                            "layers" if world > 1 else "1 GPU"}
 
