@@ -253,6 +253,24 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     t_dec = time.perf_counter()
     dec_bits = she.she_decrypt_bits(sk, out_cts)
     t_dec = time.perf_counter() - t_dec
+    # the same client steps on the GPU (NEXT-4): host noise + device masks,
+    # bit-identical ciphertexts; device decryption of the logits
+    torch.cuda.synchronize()
+    g0 = time.perf_counter()
+    noise = she.she_encrypt_noise(sk, bits.size, si.input_seed(cfg), 0)
+    g_ct = she.she_encrypt_bits_gpu(sk, torch.from_numpy(bits.ravel().astype(np.uint8)).cuda(),
+                                    torch.from_numpy(noise.view(np.int32)).cuda(),
+                                    si.input_seed(cfg), 0)
+    torch.cuda.synchronize()
+    g_enc = time.perf_counter() - g0
+    g0 = time.perf_counter()
+    g_bits = she.she_decrypt_bits_gpu(sk, lo[:10].reshape(-1, stride)).cpu().numpy()
+    g_dec = time.perf_counter() - g0
+    gpu_client = {"encrypt_s": round(g_enc, 4), "decrypt_s": round(g_dec, 5),
+                  "edl_s": round(g_enc + g_dec, 4),
+                  "bit_exact_with_host_client": bool(
+                      np.array_equal(g_ct.cpu().numpy().view(np.uint32), cts)
+                      and np.array_equal(g_bits, dec_bits))}
     logits = net.value_of(dec_bits.reshape(10, wc), signed=True)
     want = net.config3_tcn(px, w1, w2, w3) if tcn else net.config3(px, w1, w2, w3)
     stats = [s1, s2, s3]
@@ -273,7 +291,8 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
                        "edl_s": round(t_enc + t_dec, 4),
                        "msize_bytes": int(bits.size * (P.n + 1) * 4),
                        "note": "host client (she_encrypt_bits / she_decrypt_bits): 784 pixels x 8 "
-                               "bit-wise LWE ciphertexts of n+1 = 501 words (PAPER.md:256 MSize)"},
+                               "bit-wise LWE ciphertexts of n+1 = 501 words (PAPER.md:256 MSize)",
+                       "gpu": gpu_client},
             "parallelism": f"neuron-sharded x{world}, {dist.get_backend()} all-gather between "
                            "layers" if world > 1 else "1 GPU"}
 

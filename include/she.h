@@ -107,6 +107,26 @@ she_status she_encrypt_bits(const she_secret_key* sk, const uint8_t* bits, size_
 she_status she_decrypt_bits(const she_secret_key* sk, const uint32_t* in, size_t count,
                             uint8_t* bits);
 
+/* ---- client side on the GPU --------------------- */
+/* Host: the rounded-Gaussian noise words that fresh ciphertexts first_index ..
+ * first_index + count - 1 draw (stream 8 of she_rng.h), i.e. exactly what
+ * she_encrypt_bits adds, so that the device encryption below reproduces the
+ * host client bit for bit (the Gaussian uses libm, which differs between host
+ * and device; the integer masks do not).  noise: host uint32[count]. */
+she_status she_encrypt_noise(const she_secret_key* sk, size_t count, uint64_t seed,
+                             uint64_t first_index, uint32_t* noise);
+/* Device: encrypt count bits (device uint8[count]); masks drawn on the device
+ * from stream 7, noise given (device uint32[count], from she_encrypt_noise);
+ * out: device count x stride words, padding zeroed.  One warp per ciphertext,
+ * asynchronous on `stream` (a cudaStream_t on CUDA `device`). */
+she_status she_encrypt_bits_gpu(const she_secret_key* sk, const uint8_t* bits,
+                                const uint32_t* noise, size_t count, uint64_t seed,
+                                uint64_t first_index, uint32_t* out, int device, void* stream);
+/* Device: decrypt count ciphertexts (device count x stride) into bits (device
+ * uint8[count]), R5 rule as she_decrypt_bits.  Asynchronous on `stream`. */
+she_status she_decrypt_bits_gpu(const she_secret_key* sk, const uint32_t* in, size_t count,
+                                uint8_t* bits, int device, void* stream);
+
 /* ---- server side (device) ------------------------------------------------ */
 
 /* Create a context on CUDA `device`: uploads BK and KSK, transforms BK into the

@@ -188,6 +188,17 @@ she_status she_encrypt_bits(const she_secret_key* sk, const uint8_t* bits, size_
   return SHE_OK;
 }
 
+she_status she_encrypt_noise(const she_secret_key* sk, size_t count, uint64_t seed,
+                             uint64_t first_index, uint32_t* noise) {
+  if (count == 0) return SHE_OK;
+  if (!sk || !noise) return fail(SHE_ERR_ARG, "NULL argument");
+#pragma omp parallel for schedule(static) if (count > 256)
+  for (int64_t c = 0; c < (int64_t)count; ++c)
+    noise[c] = she_rng_gauss32(seed, SHE_STREAM_ENC_NOISE, first_index + (uint64_t)c,
+                               sk->p.alpha_lwe);
+  return SHE_OK;
+}
+
 she_status she_decrypt_bits(const she_secret_key* sk, const uint32_t* in, size_t count,
                             uint8_t* bits) {
   if (count == 0) return SHE_OK;

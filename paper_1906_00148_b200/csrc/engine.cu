@@ -18,6 +18,7 @@
 #include <new>
 #include <vector>
 
+#include "../../she_inputs/she_rng.h"
 #include "bootstrap_core.cuh"
 #include "common.h"
 #include "engine.h"
@@ -559,6 +560,46 @@ __global__ void modmul_peak_kernel(uint64_t* sink, uint32_t iters, uint64_t seed
   if (r == 0x12345) sink[0] = r;  // keep the work alive
 }
 
+// ---- client side on the GPU (NEXT-4): one warp per ciphertext ---------------
+// Encryption (PAPER.md:142 bit-wise; R4): a_k from the shared counter-based
+// stream 7 (the host client's numbering), b = <a, s> + (m ? mu : -mu) + e with
+// e given.  Decryption: m = [(int32)(b - <a, s>) >= 0] (R5).
+__global__ void enc_gpu_kernel(const uint8_t* s, uint32_t n, uint32_t stride, const uint8_t* bits,
+                               const uint32_t* noise, size_t count, uint64_t seed,
+                               uint64_t first, uint32_t* out) {
+  const size_t c = (size_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  if (c >= count) return;
+  const uint64_t q = first + c;
+  uint32_t* ct = out + c * stride;
+  uint32_t acc = 0;
+  for (uint32_t k = lane; k < stride; k += 32) {
+    uint32_t a = 0;
+    if (k < n) {
+      a = she_rng_u32(seed, SHE_STREAM_ENC_MASK, she_idx_enc_mask(n, q, k));
+      if (s[k]) acc += a;
+    }
+    if (k != n) ct[k] = a;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if (lane == 0) ct[n] = acc + (bits[c] ? kMu : 0u - kMu) + noise[c];
+}
+
+__global__ void dec_gpu_kernel(const uint8_t* s, uint32_t n, uint32_t stride, const uint32_t* in,
+                               size_t count, uint8_t* bits) {
+  const size_t c = (size_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  if (c >= count) return;
+  const uint32_t* ct = in + c * stride;
+  uint32_t acc = 0;
+  for (uint32_t k = lane; k < n; k += 32)
+    if (s[k]) acc += ct[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if (lane == 0) bits[c] = (int32_t)(ct[n] - acc) >= 0 ? 1 : 0;
+}
+
 // Test instrumentation: the device field primitives on caller-given inputs,
 // so that their rare carry / borrow branches (hand-written PTX) are checked
 // against exact arithmetic on edge values (tests/test_gpu_gates.py).
@@ -982,6 +1023,48 @@ she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms) {
   const double total = (double)blocks * threads * kChains * iters;
   if (modmul_per_s) *modmul_per_s = total / (best * 1e-3);
   if (ms) *ms = best;
+  return SHE_OK;
+}
+
+// The secret key's n bits, uploaded for one call (n bytes; freed stream-ordered).
+static she_status upload_key(const she_secret_key* sk, int device, cudaStream_t st,
+                             uint8_t** d_s) {
+  CK(cudaSetDevice(device));
+  CK(cudaMallocAsync(d_s, sk->s.size(), st));
+  CK(cudaMemcpyAsync(*d_s, sk->s.data(), sk->s.size(), cudaMemcpyHostToDevice, st));
+  return SHE_OK;
+}
+
+she_status she_encrypt_bits_gpu(const she_secret_key* sk, const uint8_t* bits,
+                                const uint32_t* noise, size_t count, uint64_t seed,
+                                uint64_t first_index, uint32_t* out, int device, void* stream) {
+  if (count == 0) return SHE_OK;
+  if (!sk || !bits || !noise || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* d_s = nullptr;
+  she_status r = upload_key(sk, device, st, &d_s);
+  if (r != SHE_OK) return r;
+  const uint32_t stride = (uint32_t)lwe_stride(sk->p);
+  enc_gpu_kernel<<<(unsigned)((count + 7) / 8), 256, 0, st>>>(d_s, sk->p.n, stride, bits, noise,
+                                                              count, seed, first_index, out);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(d_s, st));
+  return SHE_OK;
+}
+
+she_status she_decrypt_bits_gpu(const she_secret_key* sk, const uint32_t* in, size_t count,
+                                uint8_t* bits, int device, void* stream) {
+  if (count == 0) return SHE_OK;
+  if (!sk || !in || !bits) return fail(SHE_ERR_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* d_s = nullptr;
+  she_status r = upload_key(sk, device, st, &d_s);
+  if (r != SHE_OK) return r;
+  dec_gpu_kernel<<<(unsigned)((count + 7) / 8), 256, 0, st>>>(d_s, sk->p.n,
+                                                              (uint32_t)lwe_stride(sk->p), in,
+                                                              count, bits);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(d_s, st));
   return SHE_OK;
 }
 

@@ -116,6 +116,10 @@ def lib() -> ctypes.CDLL:
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_field_selftest": ([ctypes.c_int, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_encrypt_noise": ([_vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
+            "she_encrypt_bits_gpu": ([_vp, _vp, _vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp,
+                                      ctypes.c_int, _vp], ctypes.c_int),
+            "she_decrypt_bits_gpu": ([_vp, _vp, _sz, _vp, ctypes.c_int, _vp], ctypes.c_int),
             "she_ctx_capture": ([_vp, ctypes.c_uint64, ctypes.c_uint32, _sz], ctypes.c_int),
             "she_ctx_capture_read": ([_vp, _vp, _vp, _sz, ctypes.POINTER(_sz)], ctypes.c_int),
             "she_clear_conv_shift_acc": ([_vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
@@ -582,4 +586,37 @@ def field_selftest(device: int, a, b, c) -> np.ndarray:
     c = np.ascontiguousarray(c, dtype=np.uint32)
     out = np.zeros((len(a), 104), dtype=np.uint64)
     _check(lib().she_field_selftest(device, _np_ptr(a), _np_ptr(b), _np_ptr(c), len(a), _np_ptr(out)))
+    return out
+
+
+# ---- client side on the GPU (she.h, NEXT-4) -----------------------------------
+
+def she_encrypt_noise(sk: SecretKey, count: int, seed: int, first_index: int = 0) -> np.ndarray:
+    noise = np.zeros(max(count, 1), np.uint32)
+    _check(lib().she_encrypt_noise(sk.handle, count, seed, first_index, _np_ptr(noise)))
+    return noise[:count]
+
+
+def she_encrypt_bits_gpu(sk: SecretKey, bits, noise, seed: int, first_index: int = 0,
+                         out=None, stream=None):
+    """bits: device uint8 tensor [count]; noise: device int32 tensor [count]
+    (she_encrypt_noise); returns device int32 [count][stride]."""
+    import torch
+    count = bits.numel()
+    if out is None:
+        out = torch.empty((count, stride(sk.params)), dtype=torch.int32, device=bits.device)
+    _check(lib().she_encrypt_bits_gpu(sk.handle, _dev_ptr(bits), _dev_ptr(noise), count, seed,
+                                      first_index, _dev_ptr(out), bits.device.index or 0,
+                                      _stream_ptr(stream)))
+    return out
+
+
+def she_decrypt_bits_gpu(sk: SecretKey, cts, out=None, stream=None):
+    """cts: device int32 [count][stride]; returns device uint8 [count]."""
+    import torch
+    count = cts.shape[0]
+    if out is None:
+        out = torch.empty((count,), dtype=torch.uint8, device=cts.device)
+    _check(lib().she_decrypt_bits_gpu(sk.handle, _dev_ptr(cts), count, _dev_ptr(out),
+                                      cts.device.index or 0, _stream_ptr(stream)))
     return out

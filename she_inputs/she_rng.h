@@ -30,6 +30,14 @@
 
 #define SHE_GOLDEN 0x9E3779B97F4A7C15ULL
 
+/* The integer streams are also compiled for the device (the GPU client of
+ * csrc/engine.cu draws its masks here); the Gaussian stays host-only. */
+#if defined(__CUDACC__)
+#define SHE_RNG_FN __host__ __device__ static inline
+#else
+#define SHE_RNG_FN static inline
+#endif
+
 enum {
   SHE_STREAM_LWE_KEY = 1,   /* s_i, i < n            (bit = u64 & 1)            */
   SHE_STREAM_TRLWE_KEY = 2, /* S_j, j < N            (bit = u64 & 1)            */
@@ -41,22 +49,22 @@ enum {
   SHE_STREAM_ENC_NOISE = 8  /* e of fresh ciphertexts                          */
 };
 
-static inline uint64_t she_mix64(uint64_t z) {
+SHE_RNG_FN uint64_t she_mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
 }
 
-static inline uint64_t she_rng_u64(uint64_t seed, uint32_t stream, uint64_t index) {
+SHE_RNG_FN uint64_t she_rng_u64(uint64_t seed, uint32_t stream, uint64_t index) {
   uint64_t key = she_mix64(seed ^ she_mix64(SHE_GOLDEN * (uint64_t)(stream + 1u)));
   return she_mix64(key + SHE_GOLDEN * (index + 1u));
 }
 
-static inline uint32_t she_rng_u32(uint64_t seed, uint32_t stream, uint64_t index) {
+SHE_RNG_FN uint32_t she_rng_u32(uint64_t seed, uint32_t stream, uint64_t index) {
   return (uint32_t)(she_rng_u64(seed, stream, index) >> 32);
 }
 
-static inline uint32_t she_rng_bit(uint64_t seed, uint32_t stream, uint64_t index) {
+SHE_RNG_FN uint32_t she_rng_bit(uint64_t seed, uint32_t stream, uint64_t index) {
   return (uint32_t)(she_rng_u64(seed, stream, index) & 1u);
 }
 
@@ -77,19 +85,19 @@ static inline uint32_t she_rng_gauss32(uint64_t seed, uint32_t stream, uint64_t 
 /* ---- input-object numbering (the contract both sides follow) ---------- */
 
 /* BK row r of TRGSW i (r = c*l + j, c=0 for the A block, 1 for B), coeff m. */
-static inline uint64_t she_idx_bk(uint32_t N, uint32_t l, uint32_t i, uint32_t r, uint32_t m) {
+SHE_RNG_FN uint64_t she_idx_bk(uint32_t N, uint32_t l, uint32_t i, uint32_t r, uint32_t m) {
   return ((uint64_t)i * (2u * l) + r) * N + m;
 }
 /* KSK entry (i < N, j < t, v < base), mask word k < n.  Noise index = entry. */
-static inline uint64_t she_idx_ksk_entry(uint32_t t, uint32_t base, uint32_t i, uint32_t j,
+SHE_RNG_FN uint64_t she_idx_ksk_entry(uint32_t t, uint32_t base, uint32_t i, uint32_t j,
                                          uint32_t v) {
   return ((uint64_t)i * t + j) * base + v;
 }
-static inline uint64_t she_idx_ksk_mask(uint32_t n, uint64_t entry, uint32_t k) {
+SHE_RNG_FN uint64_t she_idx_ksk_mask(uint32_t n, uint64_t entry, uint32_t k) {
   return entry * n + k;
 }
 /* Fresh ciphertext number q (global ordinal), mask word k < n.  Noise index = q. */
-static inline uint64_t she_idx_enc_mask(uint32_t n, uint64_t q, uint32_t k) {
+SHE_RNG_FN uint64_t she_idx_enc_mask(uint32_t n, uint64_t q, uint32_t k) {
   return q * n + k;
 }
 

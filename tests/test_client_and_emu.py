@@ -168,3 +168,19 @@ def test_device_blind_rotation_matches_oracle(params):
                                   K.bk.ctypes.data_as(u32p), ct.ctypes.data_as(u32p),
                                   acc.ctypes.data_as(u32p)) == 0
     assert np.array_equal(acc, oracle.blind_rotate(K, ct))
+
+
+
+@pytest.mark.parametrize("params", [si.C0, si.C1], ids=["C0", "C1"])
+def test_encrypt_noise_is_the_host_clients_noise(params):
+    """she_encrypt_noise (the noise the GPU client is handed) equals the noise
+    inside the host client's ciphertexts: e = b - <a, s> - (m ? mu : -mu)."""
+    import oracle
+    sk, _ = she.she_keygen(params, 7)
+    bits = np.array([0, 1, 1, 0, 1] * 7, np.uint8)
+    cts = she.she_encrypt_bits(sk, bits, 4242, 100)
+    noise = she.she_encrypt_noise(sk, len(bits), 4242, 100)
+    K = oracle.keygen(params, 7)
+    mu = np.where(bits == 1, 1 << 29, (1 << 32) - (1 << 29)).astype(np.uint64)
+    ph = oracle.phases(params, K.s, cts).astype(np.uint64)
+    assert np.array_equal((ph - mu) % (1 << 32), noise.astype(np.uint64))

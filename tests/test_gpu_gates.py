@@ -326,3 +326,31 @@ def test_bad_arguments_raise(env1):
         she.she_gate_batch(env1.ctx, 99, x, x, x, torch.zeros_like(x))
     with pytest.raises(she.SheError):
         she.she_gate_batch(env1.ctx, si.AND, x, x, x, x)  # out overlaps inputs
+
+
+
+# ----------------------------------------------------------------------------
+# client side on the GPU
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_gpu_client_matches_host_client(cuda, cfg):
+    """Device encryption (masks drawn on the GPU from the shared counter-based
+    stream, host-drawn noise) is bit-identical to she_encrypt_bits; device
+    decryption equals the host decryption, including on bootstrapped outputs."""
+    P = si.CONFIG_PARAMS[cfg]
+    sk, _ = she.she_keygen(P, si.key_seed(cfg))
+    rng = np.random.default_rng(cfg + 50)
+    count = 6272 if cfg == 1 else 1000  # the MNIST image's 784 x 8 bit ciphertexts
+    bits = rng.integers(0, 2, count).astype(np.uint8)
+    host_ct = she.she_encrypt_bits(sk, bits, 5151, 7)
+    noise = she.she_encrypt_noise(sk, count, 5151, 7)
+    d_bits = torch.from_numpy(bits).cuda()
+    d_noise = torch.from_numpy(noise.view(np.int32)).cuda()
+    d_ct = she.she_encrypt_bits_gpu(sk, d_bits, d_noise, 5151, 7)
+    torch.cuda.synchronize()
+    assert np.array_equal(host(d_ct), host_ct)
+    back = she.she_decrypt_bits_gpu(sk, d_ct)
+    torch.cuda.synchronize()
+    assert np.array_equal(back.cpu().numpy(), bits)
+    assert np.array_equal(she.she_decrypt_bits(sk, host_ct), bits)
