@@ -909,7 +909,11 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
         for (uint32_t v = 1; v < base; ++v)
           memcpy(&h[(((size_t)i * t + j) * 3 + (v - 1)) * ctx->stride],
                  &ck->ksk[(((size_t)i * t + j) * base + v) * (n + 1)], (n + 1) * 4);
-    ctx->ks2 = (t == 8 && base == 4 && ctx->stride <= 2 * (uint32_t)kKs2T);
+    // SHE_KS_KERNEL=legacy forces ks_kernel (the general-parameter path) so
+    // that the tests can pin it on the configs' parameters as well
+    const char* ksk_env = getenv("SHE_KS_KERNEL");
+    const bool legacy = ksk_env && strcmp(ksk_env, "legacy") == 0;
+    ctx->ks2 = !legacy && (t == 8 && base == 4 && ctx->stride <= 2 * (uint32_t)kKs2T);
     if (ctx->ks2)  // third row -> K1 + K2 - K3 (mod 2^32), see ks2_kernel
       for (size_t r = 0; r < (size_t)N * t; ++r) {
         uint32_t* row = &h[r * 3 * ctx->stride];

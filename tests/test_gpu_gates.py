@@ -354,3 +354,24 @@ def test_gpu_client_matches_host_client(cuda, cfg):
     torch.cuda.synchronize()
     assert np.array_equal(back.cpu().numpy(), bits)
     assert np.array_equal(she.she_decrypt_bits(sk, host_ct), bits)
+
+
+
+def test_legacy_key_switch_kernel_c0(cuda, monkeypatch):
+    """ks_kernel (any base / t; used when the key-switching parameters are not
+    base 4, t = 8) on the config-0 gates: bit-exact with the oracle too."""
+    monkeypatch.setenv("SHE_KS_KERNEL", "legacy")
+    cfg, count = 0, 16
+    P = si.CONFIG_PARAMS[cfg]
+    sk, ck = she.she_keygen(P, si.key_seed(cfg))
+    ctx = she.Context(P, ck, device=0)
+    ops = si.gate_ops(cfg, count)
+    bits = si.gate_input_bits(cfg, count)
+    cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0).reshape(count, 3, -1)
+    a, b, c = (np.ascontiguousarray(cts[:, j]) for j in range(3))
+    out = torch.zeros((count, P.stride), dtype=torch.int32, device="cuda")
+    she.she_gate_batch_ops(ctx, dev(ops), dev(a), dev(b), dev(c), out)
+    torch.cuda.synchronize()
+    K = oracle.keygen(P, si.key_seed(cfg))
+    assert np.array_equal(host(out), oracle.gates(K, ops, a, b, c))
+    ctx.close()
