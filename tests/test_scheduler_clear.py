@@ -261,3 +261,42 @@ def test_config4_shaped_small_clear():
     o, wd, _ = she.clear_fc_shift_acc(h.reshape(-1), 32, wc, False, w4, 16)
     ref = net.config4(px, w1, w2, w3, w4)
     assert np.array_equal(net.value_of(o, signed=True), ref)
+
+
+def test_layer_argument_errors_are_reported():
+    """Bad shapes and out-of-range weights fail with a status (SheError), never
+    a crash or a silent result (include/she.h error contract)."""
+    x = net.bits_of(np.arange(16) % 200, 8)
+    ok = np.ones((2, 3, 3, 1), np.int8)
+    with pytest.raises(she.SheError):
+        she.clear_conv_shift_acc(x.reshape(4, 4, 1, 8), 4, 4, 1, 8, False,
+                                 np.full((2, 3, 3, 1), 9, np.int8), 1, 1)  # code out of [-8, 8]
+    with pytest.raises(she.SheError):
+        she.clear_conv_shift_acc(x.reshape(4, 4, 1, 8), 4, 4, 1, 8, False, ok, 1, 0, cap=40)
+    with pytest.raises(she.SheError):
+        she.clear_fc_mul_acc(x.reshape(-1), 16, 8, False, np.full((1, 16), 300, np.int16))
+    with pytest.raises(she.SheError):
+        she.clear_bn_shift_add(x.reshape(-1), 16, 4, 8, False, np.array([9, 0, 0, 0], np.int8),
+                               None, np.zeros(4, np.int32))
+    with pytest.raises(she.SheError):  # words not a multiple of the channel count
+        she.clear_bn_shift_add(x.reshape(-1)[:120], 15, 4, 8, False, np.zeros(4, np.int8), None,
+                               np.zeros(4, np.int32))
+    with pytest.raises(she.SheError):
+        she.clear_relu(x.reshape(-1)[:16], 16, 1)  # ReLU needs width >= 2
+    with pytest.raises(she.SheError):
+        she.clear_fc_shift_acc(x.reshape(-1), 16, 8, False, np.ones((1, 16), np.int8), rank=2,
+                               world=2)
+
+
+def test_degenerate_layers():
+    """All-zero weights give the constant 0 word; a 1x1 kernel is a per-pixel
+    shift; cap 2 wraps everything to 2 bits."""
+    px = np.arange(12).reshape(2, 2, 3) * 20
+    z = np.zeros((2, 1, 1, 3), np.int8)
+    out, w, st = she.clear_conv_shift_acc(net.bits_of(px, 8), 2, 2, 3, 8, False, z, 1, 0, 16)
+    assert not out.any() and st["gates"] == 0
+    k1 = np.array([[[[1, 0, 0]]], [[[0, -3, 0]]]], np.int8)
+    out, w, _ = she.clear_conv_shift_acc(net.bits_of(px, 8), 2, 2, 3, 8, False, k1, 1, 0, 16)
+    assert np.array_equal(net.value_of(out, signed=True), net.conv(px, k1, 1, 0, 16))
+    out, w, _ = she.clear_conv_shift_acc(net.bits_of(px, 8), 2, 2, 3, 8, False, k1, 1, 0, 2)
+    assert w <= 2 and np.array_equal(net.value_of(out, signed=True), net.conv(px, k1, 1, 0, 2))
