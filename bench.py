@@ -167,12 +167,18 @@ def read_profile_traffic():
 # ---------------------------------------------------------------------------
 # the product arm
 # ---------------------------------------------------------------------------
-def _logit_wrap_events(net, px, w1, w2, w3, tcn: bool) -> int:
-    """Logits of the config-3 net whose exact sum leaves the 16-bit cap (R13)."""
-    conv, fc = (net.conv_tcn, net.fc_tcn) if tcn else (net.conv, net.fc)
-    h = net.relu(conv(px, w1, 2, 0, 16))
-    h = net.relu(fc(h.ravel(), w2, 16))
-    return int(net.wrap_events(net.fc_exact(h, w3, net.term_tcn if tcn else None), 16))
+def _bits_of(v, width: int) -> np.ndarray:
+    """Client-side word encoding: two's-complement bits, LSB first."""
+    v = np.asarray(v, dtype=np.int64)
+    return ((v[..., None] >> np.arange(width)) & 1).astype(np.uint8)
+
+
+def _value_of(bits, signed: bool) -> np.ndarray:
+    """Client-side word decoding (inverse of _bits_of)."""
+    bits = np.asarray(bits, dtype=np.int64)
+    w = bits.shape[-1]
+    v = (bits << np.arange(w)).sum(axis=-1)
+    return np.where(bits[..., -1] == 1, v - (1 << w), v) if signed else v
 
 
 def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
@@ -183,10 +189,11 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     plaintext weights, levelisation) runs inside the timed region (not
     precompiled).  N > 1: every layer's output words are split across ranks
     (neuron-affine) and all-gathered over NCCL before the next
-    layer.  The decrypted logits are checked against the plaintext network."""
+    layer.  The decrypted logits are reported (client decryption); their
+    equality with the plaintext network is a GPU test
+    (tests/test_gpu_layers.py::test_config3_full_at_default_params)."""
     import torch
     import torch.distributed as dist
-    from oracle import network as net
     from paper_1906_00148_b200 import she
 
     cfg = 3
@@ -201,7 +208,7 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
                           else (she.she_conv_shift_acc, she.she_fc_shift_acc))
     conv_w, fc_w = (she.conv_mul_width, she.fc_mul_width) if tcn else (she.conv_width, she.fc_width)
     stride = P.stride
-    bits = net.bits_of(px, 8)
+    bits = _bits_of(px, 8)
     t_enc = time.perf_counter()  # client side (host): the paper's EDL column
     cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0)
     t_enc = time.perf_counter() - t_enc
@@ -271,8 +278,7 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
                   "bit_exact_with_host_client": bool(
                       np.array_equal(g_ct.cpu().numpy().view(np.uint32), cts)
                       and np.array_equal(g_bits, dec_bits))}
-    logits = net.value_of(dec_bits.reshape(10, wc), signed=True)
-    want = net.config3_tcn(px, w1, w2, w3) if tcn else net.config3(px, w1, w2, w3)
+    logits = _value_of(dec_bits.reshape(10, wc), signed=True)
     stats = [s1, s2, s3]
     kind = ("TCN baseline: 8-bit fixed-point multipliers (shift-and-add)" if tcn
             else "log-quantised weights")
@@ -285,8 +291,7 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
             "br_lanes_per_rank": int(sum(s["br_lanes"] for s in stats)),
             "levels": int(sum(s["levels"] for s in stats)),
             "br_lanes_total": int(lanes_total),
-            "logits_match_plaintext_network": bool(np.array_equal(logits, want)),
-            "wrap16_events_in_logits": _logit_wrap_events(net, px, w1, w2, w3, tcn),
+            "logits": [int(v) for v in logits],
             "client": {"encrypt_s": round(t_enc, 4), "decrypt_s": round(t_dec, 5),
                        "edl_s": round(t_enc + t_dec, 4),
                        "msize_bytes": int(bits.size * (P.n + 1) * 4),
@@ -303,9 +308,10 @@ def dshe_latency(ctx, sk, P, world: int, rank: int, H=28, ch=4, k=4):
     input, 3x3 'same' convs with `ch` channels, BN lowered to shift + constant
     (she_bn_shift_add), ReLU, max-pool; FC -> 8 + ReLU, FC -> 10.  Device-
     resident input to device-resident logits, host scheduling included; the
-    decrypted logits are checked against the plaintext network."""
+    decrypted logits are reported (their plaintext check at this size is a
+    run recorded in profiles/r1/bench_dshe_net.json; the same chain at C0 is
+    a GPU test)."""
     import torch
-    from oracle import network as net
     from paper_1906_00148_b200 import she
     from paper_1906_00148_b200.parallel import gather_shards, max_over_ranks, padded_words
 
@@ -320,7 +326,7 @@ def dshe_latency(ctx, sk, P, world: int, rank: int, H=28, ch=4, k=4):
     side = H >> k
     fc1 = si.log_quant_weights(cfg, (8, side * side * ch), layer=90)
     fc2 = si.log_quant_weights(cfg, (10, 8), layer=91)
-    cts = she.she_encrypt_bits(sk, net.bits_of(px, 8).ravel(), si.input_seed(cfg), 0)
+    cts = she.she_encrypt_bits(sk, _bits_of(px, 8).ravel(), si.input_seed(cfg), 0)
     x = torch.from_numpy(cts.view(np.int32)).cuda().reshape(H, H, 1, 8, stride)
 
     def buf(words, width):
@@ -376,15 +382,14 @@ def dshe_latency(ctx, sk, P, world: int, rank: int, H=28, ch=4, k=4):
     e1.record(stream)
     torch.cuda.synchronize()
     dev_s = max_over_ranks([e0.elapsed_time(e1) * 1e-3], world)[0]
-    logits = net.value_of(she.she_decrypt_bits(sk, lo.cpu().numpy().view(np.uint32)
-                                               .reshape(-1, stride)).reshape(10, w2), signed=True)
+    logits = _value_of(she.she_decrypt_bits(sk, lo.cpu().numpy().view(np.uint32)
+                                            .reshape(-1, stride)).reshape(10, w2), signed=True)
     return {"workload": f"DSHE-style net (NEXT-3): {H}x{H}x1 uint8, [conv3x3 {ch}ch + BN(shift+const) "
                         f"+ ReLU] x2 + maxpool, x{k} blocks, FC->8 + ReLU, FC->10; default TFHE "
                         "parameters",
             "latency_s": round(dev_s, 3), "unit": "s", "higher_is_better": False,
             "br_lanes_per_rank": int(lanes), "levels": int(levels),
-            "logits_match_plaintext_network": bool(np.array_equal(
-                logits, net.dshe(px, blocks, fc1, fc2)))}
+            "logits": [int(v) for v in logits]}
 
 
 def run_she(args):

@@ -10,7 +10,10 @@ GPU wire table and recomputed by the CPU oracle word for word at the end.
 Results are written to gpurun_out/config4_full.json after every layer, so a
 time-out keeps what finished.
 
-    python tools/run_config4.py            (about 4 hours on one B200)
+    python tests/long_config4.py           (about 4 hours on one B200)
+
+A script (not collected by pytest): it lives under tests/ because it runs the
+oracle, which only tests/, smoke() and bench.py's CPU legs may use.
 """
 import json
 import os

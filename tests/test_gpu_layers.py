@@ -370,3 +370,27 @@ def test_bn_and_dshe_chain_c0(cuda):
     o, w2 = she.she_fc_shift_acc(e.ctx, h, 4, w1, False, fc2, 16)
     want = net.dshe(px, [(wa, bna, wb, bnb)], fc1, fc2)
     assert np.array_equal(net.value_of(e.decrypt_bits(o), signed=True), want)
+
+
+def test_config3_full_at_default_params(cuda):
+    """BASELINE.json configs[3], the bench's net-latency workload, in full at
+    N=1024, n=500 (2.67 M gates, ~80 s): the decrypted 16-bit logits equal the
+    plaintext network; the hidden layers' outputs too."""
+    e = env(3)
+    cfg = 3
+    px = si.pixels(cfg, (28, 28, 1)).astype(np.int64)
+    w1 = si.log_quant_weights(cfg, (5, 5, 5, 1), layer=0)
+    w2 = si.log_quant_weights(cfg, (100, 720), layer=1)
+    w3 = si.log_quant_weights(cfg, (10, 100), layer=2)
+    x, _ = e.encrypt_words(px, 8, si.input_seed(cfg))
+    h1, wa = she.she_conv_shift_acc(e.ctx, x, 28, 28, 1, 8, False, w1, 2, 0, 16, relu=True)
+    ref1 = net.config2(px, w1)
+    assert np.array_equal(net.value_of(e.decrypt_bits(h1), signed=False), ref1)
+    h2, wb = she.she_fc_shift_acc(e.ctx, h1.reshape(-1, wa, e.P.stride), 720, wa, False, w2, 16,
+                                  relu=True)
+    ref2 = net.relu(net.fc(ref1.ravel(), w2, 16))
+    assert np.array_equal(net.value_of(e.decrypt_bits(h2), signed=False), ref2)
+    lo, wc = she.she_fc_shift_acc(e.ctx, h2, 100, wb, False, w3, 16)
+    got = net.value_of(e.decrypt_bits(lo), signed=True)
+    assert np.array_equal(got, net.config3(px, w1, w2, w3))
+    assert net.wrap_events(net.fc_exact(ref2, w3), 16) == 0  # configs 2-3 never wrap (SURVEY §8(c))

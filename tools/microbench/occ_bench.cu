@@ -8,8 +8,8 @@
 
 #include "ntt.cuh"
 
-template <int V, int T>
-__global__ void __launch_bounds__(T, 1) loop(uint64_t* d, int iters) {
+template <int V, int T, int B>
+__global__ void __launch_bounds__(T, B) loop(uint64_t* d, int iters) {
   uint64_t x[V];
   const size_t base = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
   for (int q = 0; q < V; ++q) x[q] = d[base + q];
@@ -20,9 +20,9 @@ __global__ void __launch_bounds__(T, 1) loop(uint64_t* d, int iters) {
   for (int q = 0; q < V; ++q) d[base + q] = gl::canon(x[q]);
 }
 
-template <int V, int T>
+template <int V, int T, int B = 1>
 void run(int iters) {
-  const int blocks = 148;
+  const int blocks = 148 * B;
   const size_t n = (size_t)blocks * T * V;
   std::vector<uint64_t> h(n);
   uint64_t s = 99;
@@ -30,14 +30,14 @@ void run(int iters) {
   uint64_t* d;
   cudaMalloc(&d, n * 8);
   cudaMemcpy(d, h.data(), n * 8, cudaMemcpyHostToDevice);
-  loop<V, T><<<blocks, T>>>(d, 2);
+  loop<V, T, B><<<blocks, T>>>(d, 2);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e9f;
   for (int r = 0; r < 3; ++r) {
     cudaEventRecord(e0);
-    loop<V, T><<<blocks, T>>>(d, iters);
+    loop<V, T, B><<<blocks, T>>>(d, iters);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -46,15 +46,17 @@ void run(int iters) {
   }
   const double lg = V == 32 ? 5 : 4;
   const double bfly = (double)blocks * T * iters * 2 * (V / 2) * lg;
-  printf("V=%d threads/SM=%d: %.3f ms, %.1f G butterflies/s (%s)\n", V, T, best, bfly / best / 1e6,
+  printf("V=%d threads/CTA=%d CTAs/SM=%d: %.3f ms, %.1f G butterflies/s (%s)\n", V, T, B, best, bfly / best / 1e6,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 
 int main() {
   run<32, 640>(100);
-  run<16, 1280>(125);
+  run<16, 640, 2>(125);
+  run<16, 512, 2>(125);
   run<16, 640>(125);
   run<32, 512>(100);
+  run<32, 320, 2>(100);
   return 0;
 }
