@@ -392,6 +392,39 @@ def dshe_latency(ctx, sk, P, world: int, rank: int, H=28, ch=4, k=4):
             "logits": [int(v) for v in logits]}
 
 
+def batch_sweep(ctx, sk, P, sizes=(148, 740, 1480, 4096, 8192, 16384, 32768)):
+    """Gates/s against the batch size (config-1 gates; one lane per CTA below
+    148 lanes, G = 5 lock-step lanes per CTA above): where the persistent
+    kernel's waves fill the 148 SMs (`--sweep`)."""
+    import torch
+    from paper_1906_00148_b200 import she
+    res = []
+    big = max(sizes)
+    ops = si.gate_ops(CFG, big)
+    bits = si.gate_input_bits(CFG, big)
+    cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(CFG), 0).reshape(big, 3, -1)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).cuda()
+    d_ops = dev(np.pad(ops, (0, (-big) % 4)))
+    d_a, d_b, d_c = (dev(cts[:, j].copy()) for j in range(3))
+    out = torch.empty((big, P.stride), dtype=torch.int32, device="cuda")
+    for n in sizes:
+        run = lambda: she.she_gate_batch_ops(ctx, d_ops[: (n + 3) // 4].view(torch.uint8)[:n],
+                                             d_a[:n], d_b[:n], d_c[:n], out[:n])
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, 8192 // n)
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        res.append({"gates": n, "br_lanes": si.br_lanes(ops[:n]), "ms": round(ms, 3),
+                    "gates_per_s": round(n / (ms * 1e-3), 1)})
+    return res
+
+
 def run_she(args):
     import torch
     import torch.distributed as dist
@@ -519,6 +552,8 @@ def run_she(args):
         line["tcn_net_latency"] = net_latency(ctx, sk, P, world, rank, tcn=True)
     if args.dshe:
         line["dshe_net_latency"] = dshe_latency(ctx, sk, P, world, rank)
+    if args.sweep:
+        line["batch_sweep"] = batch_sweep(ctx, sk, P)
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(args, h_out)
         if "net_latency" in line:  # the paper's FIL-style projection of the oracle
@@ -620,6 +655,8 @@ def main():
                     help="also time the TCN baseline of the same net (fixed-point multipliers)")
     ap.add_argument("--dshe", action="store_true",
                     help="also time a DSHE-style deeper net with batch norm (NEXT-3)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also report gates/s against the batch size")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
