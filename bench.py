@@ -105,8 +105,9 @@ class ClockSampler:
 # roofline peak: Goldilocks modmuls per second the ALUs can issue
 # ---------------------------------------------------------------------------
 def modmul_sass_instructions(lib_path: str) -> float | None:
-    """SASS instructions per gl::mul, from the K6 loop body of libshe.so
-    (non-uniform-datapath instructions of the loop / 8 independent chains)."""
+    """SASS instructions per gl::mul_le (the kernel's general multiply), from
+    the K6 loop body of libshe.so (non-uniform-datapath instructions of the
+    one-iteration loop / 8 independent chains)."""
     try:
         sass = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True,
                               timeout=120).stdout
@@ -115,9 +116,9 @@ def modmul_sass_instructions(lib_path: str) -> float | None:
     m = re.search(r"Function : \S*modmul_peak_kernel\S*\n(.*?)(?:\n\s*Function :|\Z)", sass, re.S)
     if not m:
         return None
-    lines = re.findall(r"/\*([0-9a-f]{4})\*/\s+([^;]+);", m.group(1))
+    lines = re.findall(r"/\*([0-9a-f]{4,6})\*/\s+([^;]+);", m.group(1))
     ins = [(int(a, 16), t.strip()) for a, t in lines]
-    back = [(a, t) for a, t in ins if t.split()[0].endswith("BRA.U") and "UP0" in t and not t.startswith("@")]
+    back = [(a, t) for a, t in ins if t.split()[0].endswith("BRA.U") and not t.startswith("@")]
     for a, t in back:
         tgt = int(t.split(",")[-1].strip(), 16)
         if tgt < a:

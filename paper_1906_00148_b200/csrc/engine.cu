@@ -541,7 +541,8 @@ __global__ void const_slot_kernel(uint32_t* table, uint32_t stride, uint32_t n) 
 }
 
 // K6: peak Goldilocks modmul throughput (roofline denominator).  Each thread
-// runs kChains independent chains of the same gl::mul the NTT uses.
+// runs kChains independent chains of the kernel's own general multiply
+// (gl::mul_le, the twist / untwist product).
 constexpr int kChains = 8;
 __global__ void modmul_peak_kernel(uint64_t* sink, uint32_t iters, uint64_t seed) {
   uint64_t x[kChains], c[kChains];
@@ -550,9 +551,10 @@ __global__ void modmul_peak_kernel(uint64_t* sink, uint32_t iters, uint64_t seed
     x[q] = seed ^ (0x9E3779B97F4A7C15ull * (threadIdx.x + 1 + q * 977 + blockIdx.x * 131));
     c[q] = x[q] * 0xBF58476D1CE4E5B9ull + q;
   }
+#pragma unroll 1  // one iteration per loop body: bench.py counts its SASS per modmul
   for (uint32_t it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int q = 0; q < kChains; ++q) x[q] = gl::mul(x[q], c[q]);
+    for (int q = 0; q < kChains; ++q) x[q] = gl::mul_le(x[q], c[q]);  // the twist multiply
   }
   uint64_t r = 0;
 #pragma unroll
