@@ -28,6 +28,8 @@ def main(src=None, dst=None):
                   "sampled_gate_ciphertexts_compared", "sampled_gate_ciphertext_mismatches"):
             L[k] += e[k]
     rows = [layers[k] for k in ORDER if k in layers]
+    for r in rows:
+        r["device_s"] = round(r["device_s"], 2)
     out = {"workload": "config4 (CIFAR-10-shaped net) at the default parameters on one B200, by "
                        "layer / rank shard (tests/long_config4.py); each layer fed with the "
                        "client's encryption of its exact plaintext input",
