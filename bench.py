@@ -555,13 +555,14 @@ def run_she(args):
         line["dshe_net_latency"] = dshe_latency(ctx, sk, P, world, rank)
     if args.sweep:
         line["batch_sweep"] = batch_sweep(ctx, sk, P)
-    if rank == 0:
+    if rank == 0 and world == 1:  # the CPU baseline is reported at N = 1 only
         line["cpu_baseline"] = cpu_baseline(args, h_out)
         if "net_latency" in line:  # the paper's FIL-style projection of the oracle
             cb = line["cpu_baseline"]
             lanes_s = cb["value"] * si.br_lanes(ops[:12 * cb["cores"]]) / min(COUNT, 12 * cb["cores"])
             line["net_latency"]["oracle_projected_s"] = round(
                 line["net_latency"]["br_lanes_total"] / lanes_s, 1)
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
