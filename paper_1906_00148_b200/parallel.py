@@ -37,7 +37,11 @@ def gather_shards(buf, words: int, rank: int, world: int, group=None):
         return buf[:words]
     parts = list(buf.split(per, dim=0))
     mine = parts[rank].clone()
-    dist.all_gather(parts, mine, group=group)
+    if buf.is_cuda and buf.is_contiguous():
+        # one NCCL all-gather straight into the (contiguous) gather buffer
+        dist.all_gather_into_tensor(buf, mine, group=group)
+    else:
+        dist.all_gather(parts, mine, group=group)
     return buf[:words]
 
 
