@@ -41,6 +41,10 @@ METRIC = "bootstrapped gates/s"
 UNIT = "gates/s"
 CFG = 1
 COUNT = 4096
+# FP64 engine (N = 1024): FP64 instructions (DADD, DMUL, DFMA
+# one each) per CMux of one lane: 4 forward FFTs x 19584 + 4 inverse x 19712 +
+# pointwise 512 x 4 x 16
+FP64_OPS_PER_CMUX = 4 * 19_584 + 4 * 19_712 + 512 * 4 * 16
 MODMUL_PER_LANE = {1024: 19_456_000, 256: 1_048_576}  # n[(k+1)l+(k+1)](N/2)log2N + n(k+1)l(k+1)N
 WORKLOAD = ("config1: 4096 independent bootstrapped gates, ops uniform over "
             "NAND/AND/OR/XOR/XNOR/MUX, uniform input bits; TFHE N=1024 k=1 n=500 "
@@ -145,22 +149,22 @@ def roofline_peak(device: int, lib_path: str, sm_max_mhz: float | None):
     return peak, measured, derived, ipm, src
 
 
-def read_ncu_summary():
+def read_ncu_summary(kernel: str = "br_kernel"):
     """Instruction-level evidence of the dominant kernel from the committed ncu
     capture (profiles/ncu_summary.json): issue-slot and pipe utilisation."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            br = json.load(f)["br_kernel"]
-        return {k: br[k] for k in ("issue_active_pct", "alu_pipe_pct", "fma_pipe_pct")}
+            br = json.load(f)[kernel]
+        return {k: v for k, v in br.items() if k.endswith("_pct") or k.endswith("_per_launch")}
     except (OSError, ValueError, KeyError):
         return None
 
 
-def read_profile_traffic():
+def read_profile_traffic(kernel: str = "br_kernel"):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get("br_kernel_dram_bytes_per_launch")
+            return json.load(f).get(f"{kernel}_dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
 
@@ -464,6 +468,8 @@ def run_she(args):
         she.she_gate_batch_ops(ctx, d_ops, d_a, d_b, d_c, d_out, stream)
 
     peak, k6, derived, ipm, peak_src = roofline_peak(local, she.LIB_PATH, None)
+    engine = she.br_engine(ctx)
+    fp64_peak = she.fp64_peak(local)[0] if engine else None
 
     for _ in range(args.warmup):
         step()
@@ -496,15 +502,33 @@ def run_she(args):
 
     # dominant kernel: the blind rotation (K2+K3)
     br_ms_per_launch = t["br_ms"] / max(1, t["br_launches"])
-    achieved = lanes * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3)
-    roof = {"bound": "alu", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
-            "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": read_profile_traffic(),
-            "kernel": "br_kernel (gate prologue + blind rotation + sample extract)",
-            "algorithmic_per_launch": f"{lanes} BR lanes x {MODMUL_PER_LANE[P.N]} modmul",
-            "kernel_ms_per_launch": round(br_ms_per_launch, 3),
-            "kernel_share_of_step": round(t["br_ms"] / dev_ms, 4) if dev_ms else None,
-            "ks_kernel_ms_per_launch": round(t["ks_ms"] / max(1, t["ks_launches"]), 3),
-            "peak_source": peak_src, "ncu_profile": read_ncu_summary()}
+    common = {"kernel_ms_per_launch": round(br_ms_per_launch, 3),
+              "kernel_share_of_step": round(t["br_ms"] / dev_ms, 4) if dev_ms else None,
+              "ks_kernel_ms_per_launch": round(t["ks_ms"] / max(1, t["ks_launches"]), 3)}
+    if engine:  # FP64 FFT engine: bound by the FP64 pipe
+        fp64_ops = lanes * P.n * FP64_OPS_PER_CMUX
+        achieved = fp64_ops / (br_ms_per_launch * 1e-3)
+        roof = {"bound": "fp64", "achieved": round(achieved / 1e12, 3),
+                "peak": round(fp64_peak / 1e12, 3), "unit": "T FP64-instr/s",
+                "frac": round(achieved / fp64_peak, 4), "traffic": read_profile_traffic("br_fft_kernel"),
+                "kernel": f"br_fft_kernel<{engine}> (gate prologue + blind rotation by exact FP64 "
+                          "FFT + sample extract)",
+                "algorithmic_per_launch": f"{lanes} BR lanes x {P.n} CMux x {FP64_OPS_PER_CMUX} "
+                                          "FP64 instr (DESIGN.md §4.2b)",
+                **common,
+                "peak_source": f"K7 measured {fp64_peak / 1e12:.2f} T DFMA/s on {torch.cuda.get_device_properties(local).multi_processor_count} SMs "
+                               "(nominal 64 FP64 lanes/SM/clk)",
+                "ntt_engine_equivalent": {"achieved_gmodmul_s": round(lanes * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3) / 1e9, 1),
+                                          "ntt_peak_gmodmul_s": round(peak / 1e9, 1)},
+                "ncu_profile": read_ncu_summary("br_fft_kernel")}
+    else:
+        achieved = lanes * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3)
+        roof = {"bound": "alu", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
+                "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": read_profile_traffic(),
+                "kernel": "br_kernel (gate prologue + blind rotation + sample extract)",
+                "algorithmic_per_launch": f"{lanes} BR lanes x {MODMUL_PER_LANE[P.N]} modmul",
+                **common,
+                "peak_source": peak_src, "ncu_profile": read_ncu_summary()}
 
     # ---- end to end through the public host-buffer API (H2D + D2H inside) ----
     pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()
@@ -537,7 +561,7 @@ def run_she(args):
 
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64" if engine else "u64",
             "data": "synthetic (seeded she_inputs; keys 1001, inputs 2001, ops 4001)",
             "config": {"workload": WORKLOAD, "gates_per_rank": COUNT, "br_lanes_per_rank": lanes,
                        "parallelism": f"gate-sharded x{world} (independent batches, no collective)",

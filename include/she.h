@@ -152,6 +152,16 @@ she_status she_ctx_timing(she_ctx* ctx, int reset, double* br_ms, double* ks_ms,
  * kernel's own field multiplication on every SM; the roofline denominator). */
 she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms);
 
+/* K7: peak FP64 instruction throughput of `device` (independent DFMA chains on
+ * every SM, one DFMA = one op; the roofline denominator of the FFT engine). */
+she_status she_bench_fp64_peak(int device, double* ops_per_s, double* ms);
+
+/* Blind-rotation engine of a context: *fft_lanes = G > 0 for the FP64 FFT
+ * engine (br_fft_kernel, G lanes per CTA; the default for N = 1024), 0 for the
+ * Goldilocks NTT engine (br_kernel; N = 256, or SHE_BR_ENGINE=ntt).  Both are
+ * exact, so the outputs are bit-identical. */
+she_status she_ctx_br_engine(const she_ctx* ctx, int* fft_lanes);
+
 /* Test instrumentation: evaluate the device Goldilocks primitives (hand-written
  * PTX carry chains) on n input triples (HOST buffers a, b: uint64[n]; c:
  * uint32[n]) and return out[n][104]: add, sub, add_le, sub_le (y = b), mul,

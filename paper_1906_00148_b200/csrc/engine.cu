@@ -20,6 +20,7 @@
 
 #include "../../she_inputs/she_rng.h"
 #include "bootstrap_core.cuh"
+#include "fft_core.cuh"
 #include "common.h"
 #include "engine.h"
 #include "keys.h"
@@ -276,6 +277,192 @@ __global__ void __launch_bounds__(128 * G, B) br_kernel(BRArgs args) {
       }
     }
     __syncthreads();
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// K3, FP64 engine (N = 1024): the same lock-step persistent
+// CTA as br_kernel (G lanes x 4 warps), with the CMux product computed by the
+// exact double-precision negacyclic FFT of fft_core.cuh instead of the
+// Goldilocks NTT.  Warp w of a lane: forward FFT of digit row w; CTA: the
+// pointwise sum with BK_i (16 planes (w, o, half), 1/512 folded, read once per
+// CTA for all G lanes); warp w: inverse FFT of output (o, half) = (w >> 1,
+// w & 1), rounded and added into ACC_o (hi half shifted by 16).
+// ---------------------------------------------------------------------------
+struct FLane {
+  static constexpr int N = fft::kN;
+  static constexpr size_t bytes(uint32_t n) {
+    return (size_t)2 * N * 4 + (size_t)4 * fft::kRow * 16 + ((n + 1) * 2 + 15) / 16 * 16;
+  }
+  uint32_t* acc;
+  double2* rows;
+  uint16_t* abar;
+  __device__ explicit FLane(uint8_t* base)
+      : acc(reinterpret_cast<uint32_t*>(base)),
+        rows(reinterpret_cast<double2*>(base + 2 * N * 4)),
+        abar(reinterpret_cast<uint16_t*>(base + 2 * N * 4 + 4 * fft::kRow * 16)) {}
+  __device__ double2* row(int r) const { return rows + (size_t)r * fft::kRow; }
+};
+
+struct BRFArgs {
+  GateSrc src;
+  const uint32_t* lanes;
+  const uint32_t* nlanes;
+  const double2* bkf;  // [n][16][512]: plane (w * 2 + o) * 2 + half
+  const double2* bases;  // [3][32] per-lane twiddle bases (fft::make_bases)
+  uint32_t* ext;
+  uint32_t ext_stride;
+  br::Geometry geo;
+};
+
+template <int G>
+__global__ void __launch_bounds__(128 * G, 1) br_fft_kernel(BRFArgs args) {
+  using S = ntt::Shape<1024>;
+  constexpr int N = fft::kN, M = fft::kM, T = 128 * G;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const GateSrc& src = args.src;
+  const br::Geometry& geo = args.geo;
+  const uint32_t n = geo.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp >> 2, w = warp & 3, lt = tid & 127;
+  const size_t lane_bytes = FLane::bytes(n);
+  FLane me(smem + (size_t)g * lane_bytes);
+  const uint32_t total = *args.nlanes;
+  const double2* bases = args.bases;
+
+  const uint32_t first = (uint32_t)(((uint64_t)blockIdx.x * total) / gridDim.x);
+  const uint32_t last = (uint32_t)(((uint64_t)(blockIdx.x + 1) * total) / gridDim.x);
+  for (uint32_t base = first; base < last; base += G) {
+    const uint32_t L_id = base + g;
+    const bool on = L_id < last;
+    uint32_t gate = 0, h = 0;
+    if (on) {
+      const uint32_t e = args.lanes[L_id];
+      gate = e & 0x7FFFFFFFu;
+      h = e >> 31;
+      const LaneForm f = lane_form(gate_op(src, gate), (int)h);
+      bool n0, n1;
+      const uint32_t* x0 = gate_in(src, gate, 0, n0);
+      const uint32_t* x1 = gate_in(src, gate, f.j1, n1);
+      const uint32_t k0 = (uint32_t)(n0 ? -f.k0 : f.k0), k1 = (uint32_t)(n1 ? -f.k1 : f.k1);
+      for (uint32_t k = lt; k <= n; k += 128) {
+        uint32_t v = k0 * x0[k] + k1 * x1[k];
+        if (k == n) v += f.kappa;
+        me.abar[k] = (uint16_t)br::modswitch(v, geo.lg2N);
+      }
+    }
+    __syncthreads();
+    if (on) {
+      const uint32_t bbar = me.abar[n];
+      for (int m = lt; m < N; m += 128) {
+        me.acc[m] = 0;
+        me.acc[N + m] = br::testvec_coeff(m, bbar, N);
+      }
+    }
+    __syncthreads();
+
+    for (uint32_t i = 0; i < n; ++i) {
+      if (on) {  // forward FFT of digit row w
+        int32_t d[32];
+        br::load_digits<S>(geo, w, lane, me.acc, me.abar[i], d);
+        double re[16], im[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          re[m] = fft::i2d(d[m]);
+          im[m] = fft::i2d(d[m + 16]);
+        }
+        fft::forward(re, im, lane, __ldg(bases + lane), __ldg(bases + 32 + lane), me.row(w));
+      }
+      __syncthreads();
+      {  // pointwise: frequency k, all lanes of the CTA, BK_i planes read once
+        const double2* bki = args.bkf + (size_t)i * 16 * M;
+        for (int k = tid; k < M; k += T) {
+          double2 b[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) b[q] = __ldg(bki + (size_t)q * M + k);
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg)
+            if (base + gg < last) {
+              FLane other(smem + (size_t)gg * lane_bytes);
+              double2 a[4];
+#pragma unroll
+              for (int r = 0; r < 4; ++r) a[r] = other.row(r)[k];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {  // q = o * 2 + half
+                double2 c = fft::cmul(a[0], b[q]);
+#pragma unroll
+                for (int r = 1; r < 4; ++r) {
+                  const double2 bb = b[r * 4 + q];
+                  c.x = fma(a[r].x, bb.x, fma(-a[r].y, bb.y, c.x));
+                  c.y = fma(a[r].x, bb.y, fma(a[r].y, bb.x, c.y));
+                }
+                other.row(q)[k] = c;
+              }
+            }
+        }
+      }
+      __syncthreads();
+      if (on) {  // inverse of output (o, half) = (w >> 1, w & 1), added into ACC_o
+        double2 x[8], y[8];
+        fft::inverse(me.row(w), lane, __ldg(bases + 64 + lane), me.row(w), x, y);
+        uint32_t* acc = me.acc + (w >> 1) * N;
+        const int sh = (w & 1) ? 0 : 16;
+        const int k2 = lane >> 1, hh = lane & 1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n_x = k2 + 16 * (8 * hh + j), n_y = k2 + 16 * (16 + 8 * hh + j);
+          atomicAdd(acc + n_x, fft::d2u_round(x[j].x) << sh);
+          atomicAdd(acc + n_x + M, fft::d2u_round(x[j].y) << sh);
+          atomicAdd(acc + n_y, fft::d2u_round(y[j].x) << sh);
+          atomicAdd(acc + n_y + M, fft::d2u_round(y[j].y) << sh);
+        }
+        lane_sync(1 + g);
+      }
+    }
+
+    if (on) {
+      uint32_t* e = args.ext + (size_t)(2 * gate + h) * args.ext_stride;
+      for (int m = lt; m <= N; m += 128) {
+        uint32_t v;
+        if (m == 0) v = me.acc[0];
+        else if (m < N) v = 0u - me.acc[N - m];
+        else v = me.acc[N];
+        e[m] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// K1 for the FP64 engine: BK poly (i, w, o) -> two planes (halves), forward
+// FFT, 1/512 folded.  One warp per (poly, half).
+__global__ void fft_bases_kernel(double2* tab) { fft::make_bases(threadIdx.x, tab); }
+
+__global__ void bk_fft_kernel(const uint32_t* bk, const double2* bases, double2* out,
+                              uint32_t polys) {
+  __shared__ double2 row[fft::kRow];
+  const uint32_t item = blockIdx.x, poly = item >> 1, half = item & 1;
+  if (poly >= polys) return;
+  const int lane = threadIdx.x;
+  const double2 z = bases[lane], wl = bases[32 + lane];
+  const uint32_t* b = bk + (size_t)poly * fft::kN;
+  double re[16], im[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int32_t v0 = (int32_t)b[lane + 32 * m], v1 = (int32_t)b[lane + 32 * m + 512];
+    const int32_t l0 = (int16_t)(v0 & 0xFFFF), l1 = (int16_t)(v1 & 0xFFFF);
+    re[m] = half ? (double)l0 : (double)((v0 - l0) >> 16);
+    im[m] = half ? (double)l1 : (double)((v1 - l1) >> 16);
+  }
+  fft::forward(re, im, lane, z, wl, row);
+  __syncwarp();
+  // storage: [i][plane][512], plane = (w * 2 + o) * 2 + half, poly = i * 8 + w * 2 + o
+  const uint32_t i = poly >> 3, wo = poly & 7;
+  double2* o = out + ((size_t)i * 16 + wo * 2 + half) * fft::kM;
+  for (int k = lane; k < fft::kM; k += 32) {
+    const double2 v = row[k];
+    o[k] = make_double2(v.x * (1.0 / 512), v.y * (1.0 / 512));
   }
 }
 
@@ -562,6 +749,27 @@ __global__ void modmul_peak_kernel(uint64_t* sink, uint32_t iters, uint64_t seed
   if (r == 0x12345) sink[0] = r;  // keep the work alive
 }
 
+// K7: peak FP64 instruction throughput (roofline denominator of the FFT
+// engine): kChains independent DFMA chains per thread, one DFMA = one op.
+__global__ void fp64_peak_kernel(double* sink, uint32_t iters, double seed) {
+  double x[kChains];
+#pragma unroll
+  for (int q = 0; q < kChains; ++q) x[q] = seed + threadIdx.x + q;
+  const double a = 1.0000000001, b = 1e-9 * seed;
+#pragma unroll 1
+  for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+#pragma unroll
+      for (int q = 0; q < kChains; ++q) x[q] = fma(x[q], a, b);
+    }
+  }
+  double r = 0;
+#pragma unroll
+  for (int q = 0; q < kChains; ++q) r += x[q];
+  if (r == 0.125) sink[0] = r;
+}
+
 // ---- client side on the GPU (NEXT-4): one warp per ciphertext ---------------
 // Encryption (PAPER.md:142 bit-wise; R4): a_k from the shared counter-based
 // stream 7 (the host client's numbering), b = <a, s> + (m ? mu : -mu) + e with
@@ -651,6 +859,11 @@ struct she_ctx {
   // CTA of 128 G threads, B CTAs per SM (SHE_BR_CFG="GxB" selects another
   // instantiated shape, see SHE_BR_CONFIGS)
   int br_g = 5, br_b = 1;
+  // FP64 FFT engine (br_fft_kernel, N = 1024): G lanes per CTA, 0 = NTT engine
+  // (SHE_BR_ENGINE=fft | fft3 | fft4 | ntt)
+  int fft_g = 4;
+  double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain
+  double2* fft_bases = nullptr;  // [3][32]
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
   // staging for the host-buffer API
   uint8_t* h_ops = nullptr;
@@ -726,6 +939,18 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
   bk_transform_kernel<S><<<(unsigned)polys, 32>>>(d_bk32, ctx->bk, ctx->tw, ninv, (uint32_t)polys);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
+  if (ctx->fft_g && S::N == fft::kN) {
+    CK(cudaMalloc(&ctx->bkf, (size_t)p.n * 16 * fft::kM * sizeof(double2)));
+    CK(cudaMalloc(&ctx->fft_bases, 96 * sizeof(double2)));
+    fft_bases_kernel<<<1, 32>>>(ctx->fft_bases);
+    bk_fft_kernel<<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->fft_bases, ctx->bkf, (uint32_t)polys);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaFuncSetAttribute(br_fft_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(3 * FLane::bytes(p.n))));
+    CK(cudaFuncSetAttribute(br_fft_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(4 * FLane::bytes(p.n))));
+  }
   cudaFree(d_bk32);
 #define SHE_BR_SMEM(G, B)                                                            \
   CK(cudaFuncSetAttribute(br_kernel<S, G, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -792,6 +1017,23 @@ she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream
   return SHE_OK;
 }
 
+template <int G>
+she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
+  BRFArgs f;
+  f.src = a.src;
+  f.lanes = a.lanes;
+  f.nlanes = a.nlanes;
+  f.bkf = ctx->bkf;
+  f.bases = ctx->fft_bases;
+  f.ext = a.ext;
+  f.ext_stride = a.ext_stride;
+  f.geo = a.geo;
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms));
+  br_fft_kernel<G><<<grid, 128 * G, G * FLane::bytes(ctx->p.n), stream>>>(f);
+  CK(cudaGetLastError());
+  return SHE_OK;
+}
+
 template <class S>
 she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
   const size_t total = src.count;
@@ -826,10 +1068,15 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     a.geo = ctx->geo;
     if (ctx->timing) mark(ctx, stream);
     st = fail(SHE_ERR_STATE, "no blind-rotation kernel for config %dx%d", ctx->br_g, ctx->br_b);
+    if (ctx->bkf && S::N == fft::kN) {
+      st = ctx->fft_g == 3 ? launch_br_fft<3>(ctx, a, 2 * cnt, stream)
+                           : launch_br_fft<4>(ctx, a, 2 * cnt, stream);
+    } else {
 #define SHE_BR_LAUNCH(G, B) \
     if (ctx->br_g == G && ctx->br_b == B) st = launch_br<S, G, B>(ctx, a, 2 * cnt, stream);
     SHE_BR_CONFIGS(SHE_BR_LAUNCH)
 #undef SHE_BR_LAUNCH
+    }
     if (st != SHE_OK) return st;
     if (ctx->timing) mark(ctx, stream);
 
@@ -896,6 +1143,16 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
     ctx->br_g = g;
     ctx->br_b = b;
   }
+  if (const char* e = getenv("SHE_BR_ENGINE")) {
+    if (strcmp(e, "fft") == 0 || strcmp(e, "fft4") == 0) ctx->fft_g = 4;
+    else if (strcmp(e, "fft3") == 0) ctx->fft_g = 3;
+    else if (strcmp(e, "ntt") == 0) ctx->fft_g = 0;
+    else {
+      delete ctx;
+      return fail(SHE_ERR_ARG, "SHE_BR_ENGINE=%s: expected fft, fft3, fft4 or ntt", e);
+    }
+  }
+  if (p->N != fft::kN) ctx->fft_g = 0;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
     she_ctx_destroy(ctx);
@@ -949,6 +1206,8 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   cudaFree(ctx->bk);
+  cudaFree(ctx->bkf);
+  cudaFree(ctx->fft_bases);
   cudaFree(ctx->ksk);
   cudaFree(ctx->tw);
   cudaFree(ctx->itw);
@@ -1029,6 +1288,43 @@ she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms) {
   const double total = (double)blocks * threads * kChains * iters;
   if (modmul_per_s) *modmul_per_s = total / (best * 1e-3);
   if (ms) *ms = best;
+  return SHE_OK;
+}
+
+she_status she_bench_fp64_peak(int device, double* ops_per_s, double* ms) {
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* sink = nullptr;
+  CK(cudaMalloc(&sink, 8));
+  const unsigned blocks = (unsigned)sms * 4, threads = 512;
+  const uint32_t iters = 2048;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  fp64_peak_kernel<<<blocks, threads>>>(sink, iters, 1.0);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    CK(cudaEventRecord(e0));
+    fp64_peak_kernel<<<blocks, threads>>>(sink, iters, rep + 2.0);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    best = std::min(best, t);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  const double total = (double)blocks * threads * kChains * 8 * iters;
+  if (ops_per_s) *ops_per_s = total / (best * 1e-3);
+  if (ms) *ms = best;
+  return SHE_OK;
+}
+
+she_status she_ctx_br_engine(const she_ctx* ctx, int* fft_lanes) {
+  if (!ctx || !fft_lanes) return fail(SHE_ERR_ARG, "null argument");
+  *fft_lanes = ctx->bkf ? ctx->fft_g : 0;
   return SHE_OK;
 }
 

@@ -1,0 +1,305 @@
+// fft_core.cuh — FP64 negacyclic FFT of the blind rotation (N = 1024), the
+// second engine of K3.
+//
+// The CMux product sum_r digit_r(X) * BK_{i,r}(X) mod (X^N + 1) (PAPER.md:31,
+// TFHE bootstrapping) is computed EXACTLY in double
+// precision: BK is split into 16-bit halves (b = 2^16 b_hi + b_lo, |b_*| <=
+// 2^15), so every partial product sum is an integer of magnitude <= 4 * 1024 *
+// 512 * 2^15 = 2^36, and the FFT round-off on it (<= ~1e-3)
+// is far below 1/2: rounding to the nearest integer recovers the exact value,
+// and (2^16 C_hi + C_lo) mod 2^32 is the exact torus32 product.
+//
+// Folding: a real negacyclic polynomial a is evaluated at zeta^(4k+1),
+// zeta = exp(i pi / N), through the N/2-point DFT of u_n = (a_n + i a_{n+N/2})
+// zeta^n (n < N/2); the inverse takes the conjugate path and reads a_n, a_{n+N/2}
+// from the real and imaginary parts.  N/2 = 512 = 16 x 32 in two passes per warp:
+//   pass A  thread n1 = lane: 16-point DFT over n2 of points n1 + 32 n2, then
+//           the twiddle omega_512^(n1 k2) (times the thread's twist factor);
+//   pass B  thread (k2 = t >> 1, h = t & 1): 16-point DFT of the even (h = 0) or
+//           odd (h = 1) points n1 of column k2, then one radix-2 step across the
+//           thread pair (shfl.xor 1) gives X[k2 + 16 k1] for k1 = 8h + j and
+//           16 + 8h + j (j < 8).
+// One padded shared-memory transpose (17 complex per row: conflict-free both
+// ways) sits between the passes.  Constant twiddles come from the constant bank
+// (compile-time indices); per-thread twiddles by recurrence.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fft {
+
+constexpr int kN = 1024, kM = 512, kRow = 32 * 17;  // complex per scratch row
+
+// W128[k] = exp(2 pi i k / 128)
+__constant__ double2 c_w128[128] = {
+    {1.0, 0.0},
+    {0.9987954562051724, 0.049067674327418015},
+    {0.9951847266721969, 0.0980171403295606},
+    {0.989176509964781, 0.14673047445536175},
+    {0.9807852804032304, 0.19509032201612825},
+    {0.970031253194544, 0.24298017990326387},
+    {0.9569403357322088, 0.29028467725446233},
+    {0.9415440651830208, 0.33688985339222005},
+    {0.9238795325112867, 0.3826834323650898},
+    {0.9039892931234433, 0.4275550934302821},
+    {0.881921264348355, 0.47139673682599764},
+    {0.8577286100002721, 0.5141027441932217},
+    {0.8314696123025452, 0.5555702330196022},
+    {0.8032075314806449, 0.5956993044924334},
+    {0.773010453362737, 0.6343932841636455},
+    {0.7409511253549591, 0.6715589548470183},
+    {0.7071067811865476, 0.7071067811865475},
+    {0.6715589548470183, 0.7409511253549591},
+    {0.6343932841636455, 0.773010453362737},
+    {0.5956993044924335, 0.8032075314806448},
+    {0.5555702330196023, 0.8314696123025452},
+    {0.5141027441932217, 0.8577286100002721},
+    {0.4713967368259978, 0.8819212643483549},
+    {0.4275550934302822, 0.9039892931234433},
+    {0.38268343236508984, 0.9238795325112867},
+    {0.33688985339222005, 0.9415440651830208},
+    {0.29028467725446233, 0.9569403357322089},
+    {0.24298017990326398, 0.970031253194544},
+    {0.19509032201612833, 0.9807852804032304},
+    {0.14673047445536175, 0.989176509964781},
+    {0.09801714032956077, 0.9951847266721968},
+    {0.049067674327418126, 0.9987954562051724},
+    {0.0, 1.0},
+    {-0.04906767432741801, 0.9987954562051724},
+    {-0.09801714032956065, 0.9951847266721969},
+    {-0.14673047445536164, 0.989176509964781},
+    {-0.1950903220161282, 0.9807852804032304},
+    {-0.24298017990326387, 0.970031253194544},
+    {-0.29028467725446216, 0.9569403357322089},
+    {-0.33688985339221994, 0.9415440651830208},
+    {-0.3826834323650897, 0.9238795325112867},
+    {-0.42755509343028186, 0.9039892931234434},
+    {-0.4713967368259977, 0.881921264348355},
+    {-0.5141027441932217, 0.8577286100002721},
+    {-0.555570233019602, 0.8314696123025455},
+    {-0.5956993044924334, 0.8032075314806449},
+    {-0.6343932841636454, 0.7730104533627371},
+    {-0.6715589548470184, 0.740951125354959},
+    {-0.7071067811865475, 0.7071067811865476},
+    {-0.7409511253549589, 0.6715589548470186},
+    {-0.773010453362737, 0.6343932841636455},
+    {-0.8032075314806448, 0.5956993044924335},
+    {-0.8314696123025453, 0.5555702330196022},
+    {-0.857728610000272, 0.5141027441932218},
+    {-0.8819212643483549, 0.47139673682599786},
+    {-0.9039892931234433, 0.42755509343028203},
+    {-0.9238795325112867, 0.3826834323650899},
+    {-0.9415440651830207, 0.33688985339222033},
+    {-0.9569403357322088, 0.2902846772544624},
+    {-0.970031253194544, 0.24298017990326407},
+    {-0.9807852804032304, 0.1950903220161286},
+    {-0.989176509964781, 0.1467304744553618},
+    {-0.9951847266721968, 0.09801714032956083},
+    {-0.9987954562051724, 0.049067674327417966},
+    {-1.0, 0.0},
+    {-0.9987954562051724, -0.049067674327417724},
+    {-0.9951847266721969, -0.09801714032956059},
+    {-0.989176509964781, -0.14673047445536158},
+    {-0.9807852804032304, -0.19509032201612836},
+    {-0.970031253194544, -0.24298017990326382},
+    {-0.9569403357322089, -0.2902846772544621},
+    {-0.9415440651830208, -0.3368898533922201},
+    {-0.9238795325112868, -0.38268343236508967},
+    {-0.9039892931234434, -0.4275550934302818},
+    {-0.881921264348355, -0.47139673682599764},
+    {-0.8577286100002721, -0.5141027441932216},
+    {-0.8314696123025455, -0.555570233019602},
+    {-0.8032075314806449, -0.5956993044924332},
+    {-0.7730104533627371, -0.6343932841636453},
+    {-0.7409511253549591, -0.6715589548470184},
+    {-0.7071067811865477, -0.7071067811865475},
+    {-0.6715589548470187, -0.7409511253549589},
+    {-0.6343932841636459, -0.7730104533627367},
+    {-0.5956993044924331, -0.803207531480645},
+    {-0.5555702330196022, -0.8314696123025452},
+    {-0.5141027441932218, -0.857728610000272},
+    {-0.47139673682599786, -0.8819212643483549},
+    {-0.4275550934302825, -0.9039892931234431},
+    {-0.38268343236509034, -0.9238795325112865},
+    {-0.33688985339221994, -0.9415440651830208},
+    {-0.29028467725446244, -0.9569403357322088},
+    {-0.24298017990326412, -0.970031253194544},
+    {-0.19509032201612866, -0.9807852804032303},
+    {-0.1467304744553623, -0.9891765099647809},
+    {-0.09801714032956045, -0.9951847266721969},
+    {-0.04906767432741803, -0.9987954562051724},
+    {0.0, -1.0},
+    {0.04906767432741766, -0.9987954562051724},
+    {0.09801714032956009, -0.9951847266721969},
+    {0.14673047445536194, -0.9891765099647809},
+    {0.1950903220161283, -0.9807852804032304},
+    {0.24298017990326376, -0.970031253194544},
+    {0.29028467725446205, -0.9569403357322089},
+    {0.3368898533922196, -0.9415440651830209},
+    {0.38268343236509, -0.9238795325112866},
+    {0.42755509343028214, -0.9039892931234433},
+    {0.4713967368259976, -0.881921264348355},
+    {0.5141027441932216, -0.8577286100002722},
+    {0.5555702330196018, -0.8314696123025455},
+    {0.5956993044924329, -0.8032075314806453},
+    {0.6343932841636456, -0.7730104533627369},
+    {0.6715589548470183, -0.7409511253549591},
+    {0.7071067811865474, -0.7071067811865477},
+    {0.7409511253549589, -0.6715589548470187},
+    {0.7730104533627367, -0.6343932841636459},
+    {0.803207531480645, -0.5956993044924332},
+    {0.8314696123025452, -0.5555702330196022},
+    {0.857728610000272, -0.5141027441932219},
+    {0.8819212643483548, -0.4713967368259979},
+    {0.9039892931234431, -0.42755509343028253},
+    {0.9238795325112865, -0.3826834323650904},
+    {0.9415440651830208, -0.33688985339222},
+    {0.9569403357322088, -0.2902846772544625},
+    {0.970031253194544, -0.24298017990326418},
+    {0.9807852804032303, -0.19509032201612872},
+    {0.9891765099647809, -0.1467304744553624},
+    {0.9951847266721969, -0.0980171403295605},
+    {0.9987954562051724, -0.04906767432741809}
+};
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+
+// a * W128[e]^SIGN for a compile-time e (after unrolling)
+template <int SIGN>
+__device__ __forceinline__ double2 rot(double2 a, int e) {
+  e &= 127;
+  if (e == 0) return a;
+  if (e == 64) return make_double2(-a.x, -a.y);
+  if (e == 32) return SIGN > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+  if (e == 96) return SIGN > 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+  return SIGN > 0 ? cmul(a, c_w128[e]) : cmulc(a, c_w128[e]);
+}
+
+__device__ __forceinline__ constexpr int brev4(int k) {
+  return ((k & 1) << 3) | ((k & 2) << 1) | ((k & 4) >> 1) | ((k & 8) >> 3);
+}
+
+// In-register 16-point DFT, X[k] = sum_n a[n] w16^(SIGN n k), radix-2 DIF:
+// natural input, output a[brev4(k)] = X[k].
+template <int SIGN>
+__device__ __forceinline__ void dft16(double2 (&a)[16]) {
+#pragma unroll
+  for (int half = 8; half >= 1; half >>= 1) {
+#pragma unroll
+    for (int s = 0; s < 16; s += 2 * half) {
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const double2 u = a[s + j], v = a[s + j + half];
+        a[s + j] = cadd(u, v);
+        a[s + j + half] = rot<SIGN>(csub(u, v), j * (64 / half));  // w_(2 half)^j
+      }
+    }
+  }
+}
+
+// Pass A + transpose + pass B of one 512-point DFT (direction SIGN) on warp-
+// private scratch (kRow complex).  In: a[n2] = point lane + 32 n2.  Per-thread
+// twiddle after pass A: p0 * b^k2.  Out: x[j] = X[k2 + 16 (8h + j)],
+// y[j] = X[k2 + 16 (16 + 8h + j)], (k2, h) = (lane >> 1, lane & 1).
+template <int SIGN>
+__device__ __forceinline__ void dft512(double2 (&a)[16], int lane, double2 p0, double2 b,
+                                       double2* scratch, double2 (&x)[8], double2 (&y)[8]) {
+  dft16<SIGN>(a);
+  {
+    double2 p = p0;
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+      scratch[lane * 17 + k2] = cmul(a[brev4(k2)], p);
+      if (k2 < 15) p = cmul(p, b);
+    }
+  }
+  __syncwarp();
+  const int k2 = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = scratch[(2 * m + h) * 17 + k2];
+  dft16<SIGN>(a);
+  // odd column: times w32^(SIGN k), k < 16
+  if (h) {
+#pragma unroll
+    for (int k = 1; k < 16; ++k) a[brev4(k)] = rot<SIGN>(a[brev4(k)], 4 * k);
+  }
+  // exchange: h = 0 keeps E[0..7] and gets O'[0..7]; h = 1 keeps O'[8..15] and gets E[8..15]
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double2 lo = a[brev4(j)], hi = a[brev4(8 + j)];
+    const double2 send = h ? lo : hi, keep = h ? hi : lo;
+    double2 r;
+    r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+    r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+    const double2 e = h ? r : keep, o = h ? keep : r;
+    x[j] = cadd(e, o);
+    y[j] = csub(e, o);
+  }
+  __syncwarp();  // scratch reads done before the caller reuses the row
+}
+
+// Forward transform of a real polynomial given as (re[m], im[m]) = (a_n,
+// a_{n+512}), n = lane + 32 m (m < 16).  Writes X[k] to row[k] (natural order).
+__device__ __forceinline__ void forward(const double (&re)[16], const double (&im)[16], int lane,
+                                        double2 z_lane, double2 w_lane, double2* row) {
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = rot<1>(make_double2(re[m], im[m]), 2 * m);  // w64^m
+  double2 x[8], y[8];
+  dft512<1>(a, lane, z_lane, w_lane, row, x, y);
+  const int k2 = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    row[k2 + 16 * (8 * h + j)] = x[j];
+    row[k2 + 16 * (16 + 8 * h + j)] = y[j];
+  }
+}
+
+// Inverse transform of row[k] (natural order, 1/512 already folded in):
+// out_re[j], out_im[j] for the two groups (g = 0, 1) at positions
+// n = k2 + 16 (16 g + 8 h + j): a_n = re, a_{n+512} = im.
+__device__ __forceinline__ void inverse(const double2* row_in, int lane, double2 b_inv,
+                                        double2* row, double2 (&x)[8], double2 (&y)[8]) {
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = row_in[lane + 32 * m];
+  __syncwarp();
+  dft512<-1>(a, lane, make_double2(1.0, 0.0), b_inv, row, x, y);
+  const int h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {  // untwist zeta^(-16 k1) = conj(W128[k1])
+    x[j] = cmulc(x[j], c_w128[8 * h + j]);
+    y[j] = cmulc(y[j], c_w128[16 + 8 * h + j]);
+  }
+}
+
+// exact small integer -> double (|v| < 2^31) without the conversion unit
+__device__ __forceinline__ double i2d(int32_t v) {
+  return __hiloint2double(0x43300000, (int)((uint32_t)v ^ 0x80000000u)) - 4503601774854144.0;
+}
+// round(v) mod 2^32 for |v| < 2^51
+__device__ __forceinline__ uint32_t d2u_round(double v) {
+  return (uint32_t)__double2loint(v + 6755399441055744.0);
+}
+
+// per-thread twiddle bases, table [3][32] built once (bases_kernel):
+// [0][lane] = zeta^lane (forward p0), [1][lane] = w512^lane (forward b),
+// [2][lane] = exp(-i pi (4 lane + 1) / 1024) (inverse b)
+__device__ __forceinline__ void make_bases(int lane, double2* tab) {
+  double s, c;
+  sincospi(lane / 1024.0, &s, &c);
+  tab[lane] = make_double2(c, s);
+  sincospi(lane / 256.0, &s, &c);
+  tab[32 + lane] = make_double2(c, s);
+  sincospi(-(4 * lane + 1) / 1024.0, &s, &c);
+  tab[64 + lane] = make_double2(c, s);
+}
+
+}  // namespace fft

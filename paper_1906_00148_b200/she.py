@@ -87,6 +87,9 @@ def lib() -> ctypes.CDLL:
                                 ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
             "she_bench_modmul_peak": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+            "she_bench_fp64_peak": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+            "she_ctx_br_engine": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
             "she_conv_shift_acc": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
                                    + [_vp, ctypes.POINTER(ctypes.c_int), _vp], ctypes.c_int),
             "she_fc_shift_acc": ([_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
@@ -281,6 +284,20 @@ def modmul_peak(device: int = 0) -> tuple[float, float]:
     r, ms = ctypes.c_double(), ctypes.c_double()
     _check(lib().she_bench_modmul_peak(device, ctypes.byref(r), ctypes.byref(ms)))
     return r.value, ms.value
+
+
+def fp64_peak(device: int = 0) -> tuple[float, float]:
+    """K7: measured FP64 instructions/s on all SMs (and the kernel's ms)."""
+    r, ms = ctypes.c_double(), ctypes.c_double()
+    _check(lib().she_bench_fp64_peak(device, ctypes.byref(r), ctypes.byref(ms)))
+    return r.value, ms.value
+
+
+def br_engine(ctx: Context) -> int:
+    """G > 0: FP64 FFT blind rotation with G lanes per CTA; 0: Goldilocks NTT."""
+    g = ctypes.c_int()
+    _check(lib().she_ctx_br_engine(ctx.handle, ctypes.byref(g)))
+    return g.value
 
 
 def she_gate_batch(ctx: Context, op: int, a, b, c, out, stream=None) -> None:

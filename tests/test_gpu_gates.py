@@ -285,6 +285,35 @@ def test_config1_full_parity_vs_oracle_digests(env1, config1_outputs):
     assert np.array_equal(she.she_decrypt_bits(env1.sk, out), want)
 
 
+@pytest.mark.parametrize("engine", ["ntt", "fft3"])
+def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, monkeypatch, engine):
+    """The default context of N = 1024 runs the FP64 FFT engine with 4 lanes per
+    CTA; the Goldilocks NTT engine (SHE_BR_ENGINE=ntt) and the 3-lane FFT shape
+    must give the same ciphertexts bit for bit (both products are exact,
+    DESIGN.md §4.2b): all 4096 config-1 gates against the oracle digests."""
+    assert she.br_engine(env1.ctx) == 4
+    assert she.br_engine(env0_ctx()) == 0  # N = 256 has no FFT engine
+    monkeypatch.setenv("SHE_BR_ENGINE", engine)
+    P = env1.P
+    ctx = she.Context(P, env1.ck, device=0)
+    assert she.br_engine(ctx) == (0 if engine == "ntt" else 3)
+    ops, bits, (a, b, c), _ = config1_outputs
+    out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
+    she.she_gate_batch_ops(ctx, dev(np.asarray(ops, np.uint8)), dev(a), dev(b), dev(c), out)
+    torch.cuda.synchronize()
+    got = host(out)
+    rows = read_digests(1)
+    bad = [g for g, op, d, bit in rows if digest(got[g, : P.n + 1]) != d]
+    assert not bad, f"{engine}: {len(bad)} gates differ from the oracle, first {bad[:8]}"
+    ctx.close()
+
+
+def env0_ctx():
+    if 0 not in _envs:
+        _envs[0] = Env(0)
+    return _envs[0].ctx
+
+
 def test_config1_sampled_live_oracle(env1, config1_outputs):
     ops, bits, (a, b, c), out = config1_outputs
     rng = np.random.default_rng(si.sample_seed(1))

@@ -13,7 +13,7 @@ timeout 600 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
     --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launches_$TAG.log 2>&1
 echo "ncu launches exit $?" >> gpurun_out/ncu_launches_$TAG.log
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:br_kernel -s 1 -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"br_(fft_)?kernel" -s 1 -c 1 \
     -o gpurun_out/prof_br_$TAG -f $CMD > gpurun_out/ncu_br_$TAG.log 2>&1
 echo "ncu br exit $?" >> gpurun_out/ncu_br_$TAG.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ks2_kernel -s 1 -c 1 \
