@@ -409,13 +409,17 @@ __global__ void __launch_bounds__(128 * G, 1) br_fft_kernel(BRFArgs args) {
         uint32_t* acc = me.acc + (w >> 1) * N;
         const int sh = (w & 1) ? 0 : 16;
         const int k2 = lane >> 1, hh = lane & 1;
+        // the pair (hh = 0, 1) of a column k2 hits the same bank for the same
+        // j: the odd thread takes j ^ 1 (register selects, no local memory)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int n_x = k2 + 16 * (8 * hh + j), n_y = k2 + 16 * (16 + 8 * hh + j);
-          atomicAdd(acc + n_x, fft::d2u_round(x[j].x) << sh);
-          atomicAdd(acc + n_x + M, fft::d2u_round(x[j].y) << sh);
-          atomicAdd(acc + n_y, fft::d2u_round(y[j].x) << sh);
-          atomicAdd(acc + n_y + M, fft::d2u_round(y[j].y) << sh);
+          const int jj = j ^ hh;
+          const double2 xv = hh ? x[j ^ 1] : x[j], yv = hh ? y[j ^ 1] : y[j];
+          const int n_x = k2 + 16 * (8 * hh + jj), n_y = k2 + 16 * (16 + 8 * hh + jj);
+          atomicAdd(acc + n_x, fft::d2u_round(xv.x) << sh);
+          atomicAdd(acc + n_x + M, fft::d2u_round(xv.y) << sh);
+          atomicAdd(acc + n_y, fft::d2u_round(yv.x) << sh);
+          atomicAdd(acc + n_y + M, fft::d2u_round(yv.y) << sh);
         }
         lane_sync(1 + g);
       }
@@ -950,6 +954,8 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
                             (int)(3 * FLane::bytes(p.n))));
     CK(cudaFuncSetAttribute(br_fft_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(4 * FLane::bytes(p.n))));
+    CK(cudaFuncSetAttribute(br_fft_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(5 * FLane::bytes(p.n))));
   }
   cudaFree(d_bk32);
 #define SHE_BR_SMEM(G, B)                                                            \
@@ -1069,8 +1075,9 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     if (ctx->timing) mark(ctx, stream);
     st = fail(SHE_ERR_STATE, "no blind-rotation kernel for config %dx%d", ctx->br_g, ctx->br_b);
     if (ctx->bkf && S::N == fft::kN) {
-      st = ctx->fft_g == 3 ? launch_br_fft<3>(ctx, a, 2 * cnt, stream)
-                           : launch_br_fft<4>(ctx, a, 2 * cnt, stream);
+      st = ctx->fft_g == 3   ? launch_br_fft<3>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_g == 5 ? launch_br_fft<5>(ctx, a, 2 * cnt, stream)
+                             : launch_br_fft<4>(ctx, a, 2 * cnt, stream);
     } else {
 #define SHE_BR_LAUNCH(G, B) \
     if (ctx->br_g == G && ctx->br_b == B) st = launch_br<S, G, B>(ctx, a, 2 * cnt, stream);
@@ -1146,10 +1153,11 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
   if (const char* e = getenv("SHE_BR_ENGINE")) {
     if (strcmp(e, "fft") == 0 || strcmp(e, "fft4") == 0) ctx->fft_g = 4;
     else if (strcmp(e, "fft3") == 0) ctx->fft_g = 3;
+    else if (strcmp(e, "fft5") == 0) ctx->fft_g = 5;
     else if (strcmp(e, "ntt") == 0) ctx->fft_g = 0;
     else {
       delete ctx;
-      return fail(SHE_ERR_ARG, "SHE_BR_ENGINE=%s: expected fft, fft3, fft4 or ntt", e);
+      return fail(SHE_ERR_ARG, "SHE_BR_ENGINE=%s: expected fft, fft3, fft4, fft5 or ntt", e);
     }
   }
   if (p->N != fft::kN) ctx->fft_g = 0;

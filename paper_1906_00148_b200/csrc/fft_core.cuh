@@ -28,7 +28,19 @@
 
 namespace fft {
 
-constexpr int kN = 1024, kM = 512, kRow = 32 * 17;  // complex per scratch row
+constexpr int kN = 1024, kM = 512, kRow = 512;  // complex per scratch row
+
+// Shared-memory swizzles (16-byte accesses are served 8 threads per
+// wavefront; each group of 8 must hit 8 distinct 16-byte bank groups):
+// transpose slot of (n1, k2): row n1, column k2 ^ s(n1) -- pass A writes
+// (k2 fixed, 8 consecutive n1) and pass B reads (n1 = 2m + h, k2 = t >> 1)
+// both spread over the 8 groups; frequency k is kept at position
+// k ^ (bit 7 of k) << 2 -- the forward's stores (k = k2 + 128 h + 16 j) and
+// the inverse's loads (k = lane + 32 m) are conflict-free.
+__device__ __forceinline__ int tslot(int n1, int k2) {
+  return n1 * 16 + (k2 ^ (((n1 & 1) << 2) | ((n1 >> 1) & 3)));
+}
+__device__ __forceinline__ int fpos(int k) { return k ^ (((k >> 7) & 1) << 2); }
 
 // W128[k] = exp(2 pi i k / 128)
 __constant__ double2 c_w128[128] = {
@@ -216,14 +228,14 @@ __device__ __forceinline__ void dft512(double2 (&a)[16], int lane, double2 p0, d
     double2 p = p0;
 #pragma unroll
     for (int k2 = 0; k2 < 16; ++k2) {
-      scratch[lane * 17 + k2] = cmul(a[brev4(k2)], p);
+      scratch[tslot(lane, k2)] = cmul(a[brev4(k2)], p);
       if (k2 < 15) p = cmul(p, b);
     }
   }
   __syncwarp();
   const int k2 = lane >> 1, h = lane & 1;
 #pragma unroll
-  for (int m = 0; m < 16; ++m) a[m] = scratch[(2 * m + h) * 17 + k2];
+  for (int m = 0; m < 16; ++m) a[m] = scratch[tslot(2 * m + h, k2)];
   dft16<SIGN>(a);
   // odd column: times w32^(SIGN k), k < 16
   if (h) {
@@ -246,7 +258,7 @@ __device__ __forceinline__ void dft512(double2 (&a)[16], int lane, double2 p0, d
 }
 
 // Forward transform of a real polynomial given as (re[m], im[m]) = (a_n,
-// a_{n+512}), n = lane + 32 m (m < 16).  Writes X[k] to row[k] (natural order).
+// a_{n+512}), n = lane + 32 m (m < 16).  Writes X[k] to row[fpos(k)].
 __device__ __forceinline__ void forward(const double (&re)[16], const double (&im)[16], int lane,
                                         double2 z_lane, double2 w_lane, double2* row) {
   double2 a[16];
@@ -257,19 +269,19 @@ __device__ __forceinline__ void forward(const double (&re)[16], const double (&i
   const int k2 = lane >> 1, h = lane & 1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    row[k2 + 16 * (8 * h + j)] = x[j];
-    row[k2 + 16 * (16 + 8 * h + j)] = y[j];
+    row[fpos(k2 + 16 * (8 * h + j))] = x[j];
+    row[fpos(k2 + 16 * (16 + 8 * h + j))] = y[j];
   }
 }
 
-// Inverse transform of row[k] (natural order, 1/512 already folded in):
+// Inverse transform of X[k] = row[fpos(k)] (1/512 already folded in):
 // out_re[j], out_im[j] for the two groups (g = 0, 1) at positions
 // n = k2 + 16 (16 g + 8 h + j): a_n = re, a_{n+512} = im.
 __device__ __forceinline__ void inverse(const double2* row_in, int lane, double2 b_inv,
                                         double2* row, double2 (&x)[8], double2 (&y)[8]) {
   double2 a[16];
 #pragma unroll
-  for (int m = 0; m < 16; ++m) a[m] = row_in[lane + 32 * m];
+  for (int m = 0; m < 16; ++m) a[m] = row_in[fpos(lane + 32 * m)];
   __syncwarp();
   dft512<-1>(a, lane, make_double2(1.0, 0.0), b_inv, row, x, y);
   const int h = lane & 1;
