@@ -305,12 +305,13 @@ struct FLane {
   __device__ double2* row(int r) const { return rows + (size_t)r * fft::kRow; }
 };
 
+constexpr size_t kFftTables = 2 * 512 * sizeof(double2);  // pass-A twiddles, fwd + inv
+
 struct BRFArgs {
   GateSrc src;
   const uint32_t* lanes;
   const uint32_t* nlanes;
   const double2* bkf;  // [n][16][512]: plane (w * 2 + o) * 2 + half
-  const double2* bases;  // [3][32] per-lane twiddle bases (fft::make_bases)
   uint32_t* ext;
   uint32_t ext_stride;
   br::Geometry geo;
@@ -329,7 +330,10 @@ __global__ void __launch_bounds__(128 * G, 1) br_fft_kernel(BRFArgs args) {
   const size_t lane_bytes = FLane::bytes(n);
   FLane me(smem + (size_t)g * lane_bytes);
   const uint32_t total = *args.nlanes;
-  const double2* bases = args.bases;
+  double2* tw_fwd = reinterpret_cast<double2*>(smem + (size_t)G * lane_bytes);
+  double2* tw_inv = tw_fwd + 512;
+  fft::make_tables(tid, T, tw_fwd, tw_inv);
+  __syncthreads();
 
   const uint32_t first = (uint32_t)(((uint64_t)blockIdx.x * total) / gridDim.x);
   const uint32_t last = (uint32_t)(((uint64_t)(blockIdx.x + 1) * total) / gridDim.x);
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(128 * G, 1) br_fft_kernel(BRFArgs args) {
           re[m] = fft::i2d(d[m]);
           im[m] = fft::i2d(d[m + 16]);
         }
-        fft::forward(re, im, lane, __ldg(bases + lane), __ldg(bases + 32 + lane), me.row(w));
+        fft::forward(re, im, lane, tw_fwd, me.row(w));
       }
       __syncthreads();
       {  // pointwise: frequency k, all lanes of the CTA, BK_i planes read once
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(128 * G, 1) br_fft_kernel(BRFArgs args) {
       __syncthreads();
       if (on) {  // inverse of output (o, half) = (w >> 1, w & 1), added into ACC_o
         double2 x[8], y[8];
-        fft::inverse(me.row(w), lane, __ldg(bases + 64 + lane), me.row(w), x, y);
+        fft::inverse(me.row(w), lane, tw_inv, me.row(w), x, y);
         uint32_t* acc = me.acc + (w >> 1) * N;
         const int sh = (w & 1) ? 0 : 16;
         const int k2 = lane >> 1, hh = lane & 1;
@@ -441,15 +445,14 @@ __global__ void __launch_bounds__(128 * G, 1) br_fft_kernel(BRFArgs args) {
 
 // K1 for the FP64 engine: BK poly (i, w, o) -> two planes (halves), forward
 // FFT, 1/512 folded.  One warp per (poly, half).
-__global__ void fft_bases_kernel(double2* tab) { fft::make_bases(threadIdx.x, tab); }
-
-__global__ void bk_fft_kernel(const uint32_t* bk, const double2* bases, double2* out,
-                              uint32_t polys) {
+__global__ void bk_fft_kernel(const uint32_t* bk, double2* out, uint32_t polys) {
   __shared__ double2 row[fft::kRow];
+  __shared__ double2 tw[2 * 512];
   const uint32_t item = blockIdx.x, poly = item >> 1, half = item & 1;
   if (poly >= polys) return;
   const int lane = threadIdx.x;
-  const double2 z = bases[lane], wl = bases[32 + lane];
+  fft::make_tables(lane, 32, tw, tw + 512);
+  __syncwarp();
   const uint32_t* b = bk + (size_t)poly * fft::kN;
   double re[16], im[16];
 #pragma unroll
@@ -459,7 +462,7 @@ __global__ void bk_fft_kernel(const uint32_t* bk, const double2* bases, double2*
     re[m] = half ? (double)l0 : (double)((v0 - l0) >> 16);
     im[m] = half ? (double)l1 : (double)((v1 - l1) >> 16);
   }
-  fft::forward(re, im, lane, z, wl, row);
+  fft::forward(re, im, lane, tw, row);
   __syncwarp();
   // storage: [i][plane][512], plane = (w * 2 + o) * 2 + half, poly = i * 8 + w * 2 + o
   const uint32_t i = poly >> 3, wo = poly & 7;
@@ -867,7 +870,6 @@ struct she_ctx {
   // (SHE_BR_ENGINE=fft | fft3 | fft4 | ntt)
   int fft_g = 4;
   double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain
-  double2* fft_bases = nullptr;  // [3][32]
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
   // staging for the host-buffer API
   uint8_t* h_ops = nullptr;
@@ -945,17 +947,15 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
   CK(cudaDeviceSynchronize());
   if (ctx->fft_g && S::N == fft::kN) {
     CK(cudaMalloc(&ctx->bkf, (size_t)p.n * 16 * fft::kM * sizeof(double2)));
-    CK(cudaMalloc(&ctx->fft_bases, 96 * sizeof(double2)));
-    fft_bases_kernel<<<1, 32>>>(ctx->fft_bases);
-    bk_fft_kernel<<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->fft_bases, ctx->bkf, (uint32_t)polys);
+    bk_fft_kernel<<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkf, (uint32_t)polys);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     CK(cudaFuncSetAttribute(br_fft_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(3 * FLane::bytes(p.n))));
+                            (int)(3 * FLane::bytes(p.n) + kFftTables)));
     CK(cudaFuncSetAttribute(br_fft_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(4 * FLane::bytes(p.n))));
+                            (int)(4 * FLane::bytes(p.n) + kFftTables)));
     CK(cudaFuncSetAttribute(br_fft_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(5 * FLane::bytes(p.n))));
+                            (int)(5 * FLane::bytes(p.n) + kFftTables)));
   }
   cudaFree(d_bk32);
 #define SHE_BR_SMEM(G, B)                                                            \
@@ -1030,12 +1030,11 @@ she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaSt
   f.lanes = a.lanes;
   f.nlanes = a.nlanes;
   f.bkf = ctx->bkf;
-  f.bases = ctx->fft_bases;
   f.ext = a.ext;
   f.ext_stride = a.ext_stride;
   f.geo = a.geo;
   const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms));
-  br_fft_kernel<G><<<grid, 128 * G, G * FLane::bytes(ctx->p.n), stream>>>(f);
+  br_fft_kernel<G><<<grid, 128 * G, G * FLane::bytes(ctx->p.n) + kFftTables, stream>>>(f);
   CK(cudaGetLastError());
   return SHE_OK;
 }
@@ -1215,7 +1214,7 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaDeviceSynchronize();
   cudaFree(ctx->bk);
   cudaFree(ctx->bkf);
-  cudaFree(ctx->fft_bases);
+
   cudaFree(ctx->ksk);
   cudaFree(ctx->tw);
   cudaFree(ctx->itw);

@@ -218,19 +218,17 @@ __device__ __forceinline__ void dft16(double2 (&a)[16]) {
 
 // Pass A + transpose + pass B of one 512-point DFT (direction SIGN) on warp-
 // private scratch (kRow complex).  In: a[n2] = point lane + 32 n2.  Per-thread
-// twiddle after pass A: p0 * b^k2.  Out: x[j] = X[k2 + 16 (8h + j)],
-// y[j] = X[k2 + 16 (16 + 8h + j)], (k2, h) = (lane >> 1, lane & 1).
+// twiddle after pass A: tw[k2 * 32 + lane] (a shared table, see make_tables).
+// Out: x[j] = X[k2 + 16 (8h + j)], y[j] = X[k2 + 16 (16 + 8h + j)],
+// (k2, h) = (lane >> 1, lane & 1).
 template <int SIGN>
-__device__ __forceinline__ void dft512(double2 (&a)[16], int lane, double2 p0, double2 b,
+__device__ __forceinline__ void dft512(double2 (&a)[16], int lane, const double2* tw,
                                        double2* scratch, double2 (&x)[8], double2 (&y)[8]) {
   dft16<SIGN>(a);
-  {
-    double2 p = p0;
 #pragma unroll
-    for (int k2 = 0; k2 < 16; ++k2) {
-      scratch[tslot(lane, k2)] = cmul(a[brev4(k2)], p);
-      if (k2 < 15) p = cmul(p, b);
-    }
+  for (int k2 = 0; k2 < 16; ++k2) {
+    const double2 p = tw[k2 * 32 + lane];
+    scratch[tslot(lane, k2)] = k2 == 0 && SIGN < 0 ? a[0] : cmul(a[brev4(k2)], p);
   }
   __syncwarp();
   const int k2 = lane >> 1, h = lane & 1;
@@ -260,12 +258,12 @@ __device__ __forceinline__ void dft512(double2 (&a)[16], int lane, double2 p0, d
 // Forward transform of a real polynomial given as (re[m], im[m]) = (a_n,
 // a_{n+512}), n = lane + 32 m (m < 16).  Writes X[k] to row[fpos(k)].
 __device__ __forceinline__ void forward(const double (&re)[16], const double (&im)[16], int lane,
-                                        double2 z_lane, double2 w_lane, double2* row) {
+                                        const double2* tw_fwd, double2* row) {
   double2 a[16];
 #pragma unroll
   for (int m = 0; m < 16; ++m) a[m] = rot<1>(make_double2(re[m], im[m]), 2 * m);  // w64^m
   double2 x[8], y[8];
-  dft512<1>(a, lane, z_lane, w_lane, row, x, y);
+  dft512<1>(a, lane, tw_fwd, row, x, y);
   const int k2 = lane >> 1, h = lane & 1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -277,13 +275,13 @@ __device__ __forceinline__ void forward(const double (&re)[16], const double (&i
 // Inverse transform of X[k] = row[fpos(k)] (1/512 already folded in):
 // out_re[j], out_im[j] for the two groups (g = 0, 1) at positions
 // n = k2 + 16 (16 g + 8 h + j): a_n = re, a_{n+512} = im.
-__device__ __forceinline__ void inverse(const double2* row_in, int lane, double2 b_inv,
+__device__ __forceinline__ void inverse(const double2* row_in, int lane, const double2* tw_inv,
                                         double2* row, double2 (&x)[8], double2 (&y)[8]) {
   double2 a[16];
 #pragma unroll
   for (int m = 0; m < 16; ++m) a[m] = row_in[fpos(lane + 32 * m)];
   __syncwarp();
-  dft512<-1>(a, lane, make_double2(1.0, 0.0), b_inv, row, x, y);
+  dft512<-1>(a, lane, tw_inv, row, x, y);
   const int h = lane & 1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {  // untwist zeta^(-16 k1) = conj(W128[k1])
@@ -301,17 +299,21 @@ __device__ __forceinline__ uint32_t d2u_round(double v) {
   return (uint32_t)__double2loint(v + 6755399441055744.0);
 }
 
-// per-thread twiddle bases, table [3][32] built once (bases_kernel):
-// [0][lane] = zeta^lane (forward p0), [1][lane] = w512^lane (forward b),
-// [2][lane] = exp(-i pi (4 lane + 1) / 1024) (inverse b)
-__device__ __forceinline__ void make_bases(int lane, double2* tab) {
-  double s, c;
-  sincospi(lane / 1024.0, &s, &c);
-  tab[lane] = make_double2(c, s);
-  sincospi(lane / 256.0, &s, &c);
-  tab[32 + lane] = make_double2(c, s);
-  sincospi(-(4 * lane + 1) / 1024.0, &s, &c);
-  tab[64 + lane] = make_double2(c, s);
+// Pass-A twiddle tables [16][32] (k2, lane), each entry from sincospi:
+//   forward  zeta^lane w512^(lane k2) = exp(i pi lane (1 + 4 k2) / 1024)
+//            (the twist zeta^n = zeta^lane w64^n2 of the folding, its
+//            thread-constant factor moved behind the linear pass A);
+//   inverse  w512^(-lane k2) zeta^(-k2) = exp(-i pi k2 (4 lane + 1) / 1024)
+//            (the untwist's zeta^(-k2) factor of output n = k2 + 16 k1).
+__device__ __forceinline__ void make_tables(int t, int nthreads, double2* fwd, double2* inv) {
+  for (int e = t; e < 512; e += nthreads) {
+    const int k2 = e >> 5, lane = e & 31;
+    double s, c;
+    sincospi(lane * (1 + 4 * k2) / 1024.0, &s, &c);
+    fwd[e] = make_double2(c, s);
+    sincospi(-k2 * (4 * lane + 1) / 1024.0, &s, &c);
+    inv[e] = make_double2(c, s);
+  }
 }
 
 }  // namespace fft
