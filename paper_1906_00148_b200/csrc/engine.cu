@@ -317,8 +317,8 @@ struct BRFArgs {
   br::Geometry geo;
 };
 
-template <int G>
-__global__ void __launch_bounds__(128 * G, 1) br_fft_kernel(BRFArgs args) {
+template <int G, int B = 1>
+__global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
   using S = ntt::Shape<1024>;
   constexpr int N = fft::kN, M = fft::kM, T = 128 * G;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -956,6 +956,8 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
                             (int)(4 * FLane::bytes(p.n) + kFftTables)));
     CK(cudaFuncSetAttribute(br_fft_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(5 * FLane::bytes(p.n) + kFftTables)));
+    CK(cudaFuncSetAttribute(br_fft_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(2 * FLane::bytes(p.n) + kFftTables)));
   }
   cudaFree(d_bk32);
 #define SHE_BR_SMEM(G, B)                                                            \
@@ -1023,7 +1025,7 @@ she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream
   return SHE_OK;
 }
 
-template <int G>
+template <int G, int B = 1>
 she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
   BRFArgs f;
   f.src = a.src;
@@ -1033,8 +1035,9 @@ she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaSt
   f.ext = a.ext;
   f.ext_stride = a.ext_stride;
   f.geo = a.geo;
-  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms));
-  br_fft_kernel<G><<<grid, 128 * G, G * FLane::bytes(ctx->p.n) + kFftTables, stream>>>(f);
+  const unsigned grid =
+      (unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms * B));
+  br_fft_kernel<G, B><<<grid, 128 * G, G * FLane::bytes(ctx->p.n) + kFftTables, stream>>>(f);
   CK(cudaGetLastError());
   return SHE_OK;
 }
@@ -1076,6 +1079,7 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     if (ctx->bkf && S::N == fft::kN) {
       st = ctx->fft_g == 3   ? launch_br_fft<3>(ctx, a, 2 * cnt, stream)
            : ctx->fft_g == 5 ? launch_br_fft<5>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_g == 2 ? launch_br_fft<2, 2>(ctx, a, 2 * cnt, stream)
                              : launch_br_fft<4>(ctx, a, 2 * cnt, stream);
     } else {
 #define SHE_BR_LAUNCH(G, B) \
@@ -1153,10 +1157,11 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
     if (strcmp(e, "fft") == 0 || strcmp(e, "fft4") == 0) ctx->fft_g = 4;
     else if (strcmp(e, "fft3") == 0) ctx->fft_g = 3;
     else if (strcmp(e, "fft5") == 0) ctx->fft_g = 5;
+    else if (strcmp(e, "fft2x2") == 0) ctx->fft_g = 2;
     else if (strcmp(e, "ntt") == 0) ctx->fft_g = 0;
     else {
       delete ctx;
-      return fail(SHE_ERR_ARG, "SHE_BR_ENGINE=%s: expected fft, fft3, fft4, fft5 or ntt", e);
+      return fail(SHE_ERR_ARG, "SHE_BR_ENGINE=%s: expected fft, fft2x2, fft3, fft4, fft5 or ntt", e);
     }
   }
   if (p->N != fft::kN) ctx->fft_g = 0;
