@@ -378,13 +378,18 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
         }
         fft::forward(re, im, lane, tw_fwd, me.row(w));
       }
+      // BK_i planes of this thread's first frequency (k = tid) are requested
+      // before the barrier, so their L2 latency overlaps the wait for the
+      // slowest warp's forward transform
+      const double2* bki = args.bkf + (size_t)i * 16 * M;
+      double2 bpre[16];
+      if (tid < M) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) bpre[q] = __ldg(bki + (size_t)q * M + tid);
+      }
       __syncthreads();
       {  // pointwise: frequency k, all lanes of the CTA, BK_i planes read once
-        const double2* bki = args.bkf + (size_t)i * 16 * M;
-        for (int k = tid; k < M; k += T) {
-          double2 b[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) b[q] = __ldg(bki + (size_t)q * M + k);
+        auto pointwise = [&](int k, const double2 (&b)[16]) {
 #pragma unroll
           for (int gg = 0; gg < G; ++gg)
             if (base + gg < last) {
@@ -404,6 +409,13 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
                 other.row(q)[k] = c;
               }
             }
+        };
+        if (tid < M) pointwise(tid, bpre);
+        for (int k = tid + T; k < M; k += T) {
+          double2 b[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) b[q] = __ldg(bki + (size_t)q * M + k);
+          pointwise(k, b);
         }
       }
       __syncthreads();

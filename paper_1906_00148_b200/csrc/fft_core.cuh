@@ -235,12 +235,10 @@ __device__ __forceinline__ void dft512(double2 (&a)[16], int lane, const double2
 #pragma unroll
   for (int m = 0; m < 16; ++m) a[m] = scratch[tslot(2 * m + h, k2)];
   dft16<SIGN>(a);
-  // odd column: times w32^(SIGN k), k < 16
-  if (h) {
-#pragma unroll
-    for (int k = 1; k < 16; ++k) a[brev4(k)] = rot<SIGN>(a[brev4(k)], 4 * k);
-  }
-  // exchange: h = 0 keeps E[0..7] and gets O'[0..7]; h = 1 keeps O'[8..15] and gets E[8..15]
+  // exchange: h = 0 keeps E[0..7] and gets O[0..7]; h = 1 keeps O[8..15] and
+  // gets E[8..15].  The odd-column twiddle w32^(SIGN k) is applied after the
+  // exchange, split between the pair (k = 8h + j = w32^j times i^h), so both
+  // threads of a pair do 7 complex products instead of one doing 14.
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const double2 lo = a[brev4(j)], hi = a[brev4(8 + j)];
@@ -248,7 +246,9 @@ __device__ __forceinline__ void dft512(double2 (&a)[16], int lane, const double2
     double2 r;
     r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
     r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
-    const double2 e = h ? r : keep, o = h ? keep : r;
+    const double2 e = h ? r : keep;
+    double2 o = rot<SIGN>(h ? keep : r, 4 * j);
+    if (h) o = SIGN > 0 ? make_double2(-o.y, o.x) : make_double2(o.y, -o.x);
     x[j] = cadd(e, o);
     y[j] = csub(e, o);
   }
