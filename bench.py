@@ -42,10 +42,10 @@ UNIT = "gates/s"
 CFG = 1
 COUNT = 4096
 # FP64 engine (N = 1024): FP64 instructions (DADD, DMUL, DFMA
-# one each) per CMux of one lane: 4 forward + 4 inverse 512-point FFTs x 17664
+# one each) per CMux of one lane: 4 forward + 4 inverse 512-point FFTs x 17920
 # (passes A and B, folding twist, int<->double conversions) + pointwise
-# 512 x 4 x 16; ncu's DADD + DMUL + DFMA count agrees to 0.3 %
-FP64_OPS_PER_CMUX = 8 * 17_664 + 512 * 4 * 16
+# 512 x 4 x 16 = 176,128; ncu's DADD + DMUL + DFMA count: 176,129
+FP64_OPS_PER_CMUX = 8 * 17_920 + 512 * 4 * 16
 MODMUL_PER_LANE = {1024: 19_456_000, 256: 1_048_576}  # n[(k+1)l+(k+1)](N/2)log2N + n(k+1)l(k+1)N
 WORKLOAD = ("config1: 4096 independent bootstrapped gates, ops uniform over "
             "NAND/AND/OR/XOR/XNOR/MUX, uniform input bits; TFHE N=1024 k=1 n=500 "
