@@ -129,11 +129,18 @@ she_status she_decrypt_bits_gpu(const she_secret_key* sk, const uint32_t* in, si
 
 /* ---- server side (device) ------------------------------------------------ */
 
-/* Create a context on CUDA `device`: uploads BK and KSK, transforms BK into the
- * Goldilocks NTT domain (with N^-1 folded in) and keeps it resident (L2
- * persisting window).  rank/world describe the multi-GPU group this context
- * belongs to (world = 1 for single GPU; the exchange between ranks is done by
- * the caller's process group). */
+/* Create a context on CUDA `device`: uploads BK and KSK and transforms BK for
+ * the blind-rotation engine: for N = 1024 (default) into the FP64 FFT domain
+ * (each torus32 coefficient split into 16-bit halves, 1/512 folded in; 65.5 MB
+ * at the default parameters; the product is exact), for
+ * N = 256 or with the environment variable SHE_BR_ENGINE=ntt into the
+ * Goldilocks NTT domain (N^-1 folded in).  SHE_BR_ENGINE=fft3|fft4|fft5|fft2x2
+ * select the FFT kernel's lanes per CTA (default fft4); SHE_BR_CFG=GxB the NTT
+ * kernel's shape; SHE_KS_KERNEL=legacy the general key-switch kernel.  An
+ * unknown value is SHE_ERR_ARG.  BK is kept resident (L2 persisting window).
+ * rank/world describe the multi-GPU group this context belongs to (world = 1
+ * for single GPU; the exchange between ranks is done by the caller's process
+ * group). */
 she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int device, int rank,
                           int world, she_ctx** ctx);
 she_status she_ctx_destroy(she_ctx* ctx);
