@@ -1,3 +1,7 @@
+#!/bin/bash
+# Round profile of the FFT engine: GPU tests, bench (+ net), ncu launch list, one ncu --set full
+# capture each of the BR and KS kernels, FP64 instruction counts, and the three nets.
+#   gpurun --timeout 3000 -- "bash tools/gpu_fft_profile.sh TAG"
 bash tools/gpu_tests.sh $1
 bash tools/gpu_profile.sh $1
 CMD="python bench.py --steps 2 --warmup 1 --no-net"

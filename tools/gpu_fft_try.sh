@@ -1,3 +1,4 @@
+#!/bin/bash
 # FFT engine A/B: gate parity tests, then bench.py --no-net per shape
 mkdir -p gpurun_out
 TAG=${1:-t}
