@@ -52,6 +52,11 @@ WORKLOAD = ("config1: 4096 independent bootstrapped gates, ops uniform over "
             "Bg=2^10 l=2 ks 2^2x8 alpha_lwe=2.44e-5 alpha_bk=3.73e-9 (torus32)")
 
 
+def set_count(n: int) -> None:
+    global COUNT
+    COUNT = n
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -431,6 +436,16 @@ def batch_sweep(ctx, sk, P, sizes=(148, 740, 1480, 4096, 8192, 16384, 32768)):
     return res
 
 
+def engine_options(args) -> dict:
+    """she_ctx_options from the command line (all engines are exact; A/B only)."""
+    opts = {}
+    if args.engine != "default":
+        opts["engine"] = args.engine
+    if args.fft_lanes:
+        opts["fft_lanes"] = args.fft_lanes
+    return opts
+
+
 def run_she(args):
     import torch
     import torch.distributed as dist
@@ -450,7 +465,7 @@ def run_she(args):
     torch.cuda.set_device(local)
     P = si.CONFIG_PARAMS[CFG]
     sk, ck = she.she_keygen(P, si.key_seed(CFG))
-    ctx = she.Context(P, ck, device=local, rank=rank, world=world)
+    ctx = she.Context(P, ck, device=local, rank=rank, world=world, **engine_options(args))
     ops = si.gate_ops(CFG, COUNT)
     bits = si.gate_input_bits(CFG, COUNT)
     # every rank evaluates its own batch: distinct ciphertexts (ordinal offset by rank)
@@ -459,7 +474,7 @@ def run_she(args):
     lanes = si.br_lanes(ops)
     stride = P.stride
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).cuda()
-    d_ops = dev(ops.astype(np.uint8))
+    d_ops = torch.from_numpy(ops.astype(np.uint8)).cuda()
     d_a, d_b, d_c = (dev(cts[:, j].copy()) for j in range(3))
     d_out = torch.empty((COUNT, stride), dtype=torch.int32, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -684,7 +699,14 @@ def main():
                     help="also time a DSHE-style deeper net with batch norm (NEXT-3)")
     ap.add_argument("--sweep", action="store_true",
                     help="also report gates/s against the batch size")
+    ap.add_argument("--engine", default="default", choices=["default", "fft", "ntt"],
+                    help="blind-rotation engine (she_ctx_options; A/B measurements only)")
+    ap.add_argument("--fft-lanes", type=int, default=0,
+                    help="FFT engine lanes per CTA (she_ctx_options.fft_lanes)")
+    ap.add_argument("--count", type=int, default=COUNT,
+                    help="gates per step (default: config 1's 4096; other values are A/B only)")
     args = ap.parse_args()
+    set_count(args.count)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -61,8 +61,10 @@ typedef enum {
 } she_op;
 
 /* TFHE gate-bootstrapping parameters (BASELINE.json configs).  Supported:
- * k = 1; N in {256, 1024}; n <= 1024; l * bg_bits <= 32; ks_t * ks_base_bits
- * <= 32; exactness (k+1) l N (Bg/2) 2^31 < (p-1)/2 for p = 2^64 - 2^32 + 1. */
+ * k = 1; N in {256, 1024}; 1 <= n <= 511 (an LWE slot of n + 1 words padded
+ * to 32 fits the key-switch kernels); l = 2; l * bg_bits < 32; ks_base_bits =
+ * 2, ks_t * ks_base_bits < 32; exactness (k+1) l N (Bg/2) 2^31 < (p-1)/2 for
+ * p = 2^64 - 2^32 + 1.  Anything else is SHE_ERR_PARAMS. */
 typedef struct {
   uint32_t N, k, n, bg_bits, l, ks_base_bits, ks_t;
   double alpha_lwe, alpha_bk;
@@ -129,18 +131,42 @@ she_status she_decrypt_bits_gpu(const she_secret_key* sk, const uint32_t* in, si
 
 /* ---- server side (device) ------------------------------------------------ */
 
+/* Engine selection of a context (she_ctx_create_ex).  Every engine and shape
+ * computes the same ciphertexts bit for bit (all are exact); they differ only
+ * in speed.  Zero-initialised = the defaults. */
+typedef struct {
+  int br_engine;  /* 0 = default: the FP64 FFT engine for N = 1024 and bg_bits
+                     <= 12, else the Goldilocks NTT engine;
+                     1 = FFT (SHE_ERR_ARG where it does not apply); 2 = NTT */
+  int fft_lanes;  /* FFT engine: blind-rotation lanes per CTA, 0 = default (4);
+                     2 (two CTAs per SM), 3, 4 or 5 */
+  int ntt_lanes;  /* NTT engine: lanes per CTA x CTAs per SM, 0 = default 5 x 1; */
+  int ntt_ctas;   /*   the instantiated shapes are 5x1, 4x1, 3x1, 2x2, 1x4      */
+  int ks_kernel;  /* 0 = default (ks2_kernel for base 4, t = 8), 1 = the general
+                     ks_kernel (any base-4 decomposition) */
+  int reserved[7];/* must be 0 */
+} she_ctx_options;
+
 /* Create a context on CUDA `device`: uploads BK and KSK and transforms BK for
- * the blind-rotation engine: for N = 1024 (default) into the FP64 FFT domain
- * (each torus32 coefficient split into 16-bit halves, 1/512 folded in; 65.5 MB
- * at the default parameters; the product is exact), for
- * N = 256 or with the environment variable SHE_BR_ENGINE=ntt into the
- * Goldilocks NTT domain (N^-1 folded in).  SHE_BR_ENGINE=fft3|fft4|fft5|fft2x2
- * select the FFT kernel's lanes per CTA (default fft4); SHE_BR_CFG=GxB the NTT
- * kernel's shape; SHE_KS_KERNEL=legacy the general key-switch kernel.  An
- * unknown value is SHE_ERR_ARG.  BK is kept resident (L2 persisting window).
- * rank/world describe the multi-GPU group this context belongs to (world = 1
- * for single GPU; the exchange between ranks is done by the caller's process
- * group). */
+ * the blind-rotation engine that `opt` selects (NULL = defaults): for the FFT
+ * engine into the FP64 FFT domain (each torus32 coefficient split into 16-bit
+ * halves, 1/512 folded in; 65.5 MB at the default parameters; the product is
+ * exact), for the NTT engine into the Goldilocks NTT domain
+ * (N^-1 folded in; 32.8 MB).  Only the selected engine's BK is built.  The
+ * BK in use gets an L2 persisting access-policy window on the blind-rotation
+ * launches when the device allows one (cudaLimitPersistingL2CacheSize).
+ * Unknown or inapplicable option values are SHE_ERR_ARG.  rank/world describe
+ * the multi-GPU group this context belongs to (world = 1 for single GPU; the
+ * exchange between ranks is done by the caller's process group).
+ *
+ * Threading and streams: a context's scratch (extracted samples, lane list,
+ * wire table, host staging) is shared by all its calls, which are serialised
+ * by a mutex on the host but ordered only on the stream each call is given.
+ * Use one context from one stream at a time (or synchronise between streams);
+ * calls on two streams that overlap on the device race on the scratch. */
+she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int device, int rank,
+                             int world, const she_ctx_options* opt, she_ctx** ctx);
+/* she_ctx_create_ex with the default options. */
 she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int device, int rank,
                           int world, she_ctx** ctx);
 she_status she_ctx_destroy(she_ctx* ctx);
@@ -165,7 +191,7 @@ she_status she_bench_fp64_peak(int device, double* ops_per_s, double* ms);
 
 /* Blind-rotation engine of a context: *fft_lanes = G > 0 for the FP64 FFT
  * engine (br_fft_kernel, G lanes per CTA; the default for N = 1024), 0 for the
- * Goldilocks NTT engine (br_kernel; N = 256, or SHE_BR_ENGINE=ntt).  Both are
+ * Goldilocks NTT engine (br_kernel; N = 256, or br_engine = 2).  Both are
  * exact, so the outputs are bit-identical. */
 she_status she_ctx_br_engine(const she_ctx* ctx, int* fft_lanes);
 
@@ -176,6 +202,21 @@ she_status she_ctx_br_engine(const she_ctx* ctx, int* fft_lanes);
  * shl_le(a, s) for s = 0..95.  Results are lazy residues (the *_le ones <= p). */
 she_status she_field_selftest(int device, const uint64_t* a, const uint64_t* b, const uint32_t* c,
                               size_t n, uint64_t* out);
+
+/* Test instrumentation: the FP64 engine's CMux product on caller-given inputs,
+ * through the exact device code of br_fft_kernel (BK split into 16-bit halves
+ * and transformed by the engine's setup kernel; forward FFT of the digit rows,
+ * pointwise sum, inverse FFT, rounding, hi/lo recombination),
+ * so that the exactness reading is pinned on the kernel that runs, not on a
+ * model of it.  N = 1024 only.  HOST buffers:
+ *   digits int32[count][4][1024]      digit rows r = c*l + j, |d| <= 2^11
+ *   bk     uint32[count][4][2][1024]  torus32 BK rows (r, output o)
+ *   out    uint32[count][2][1024]     out[c][o] = sum_r digits[c][r] * bk[c][r][o]
+ *                                     mod (X^1024 + 1), mod 2^32
+ * *worst_distance (may be NULL) = max over all cases of |v - rint(v)| for every
+ * value before rounding (exactness needs < 1/2).  count <= 65535. */
+she_status she_fft_product_selftest(int device, const int32_t* digits, const uint32_t* bk,
+                                    size_t count, uint32_t* out, double* worst_distance);
 
 /* Bootstrapped gates, all with the same op (north_star signature).  a, b, c,
  * out: device, count slots each (c read only for MUX, b not read for

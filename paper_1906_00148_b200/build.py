@@ -18,7 +18,6 @@ EMU = os.path.join(HERE, "libshe_hostemu.so")
 
 CUDA_SOURCES = ["engine.cu"]
 CXX_SOURCES = ["client.cpp", "scheduler.cpp"]
-HEADERS = ["gl64.cuh", "ntt.cuh", "bootstrap_core.cuh", "common.h", "keys.h", "scheduler.h"]
 
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -28,7 +27,9 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "--expt-relaxed
 
 
 def _inputs():
-    files = [os.path.join(CSRC, f) for f in CUDA_SOURCES + CXX_SOURCES + HEADERS]
+    # every source and header under csrc/ (a new header is covered automatically)
+    files = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))
+             if f.endswith((".cu", ".cuh", ".h", ".cpp", ".hpp"))]
     files.append(os.path.join(os.path.dirname(HERE), "include", "she.h"))
     files.append(os.path.join(os.path.dirname(HERE), "she_inputs", "she_rng.h"))
     files.append(os.path.abspath(__file__))

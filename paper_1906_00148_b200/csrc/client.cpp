@@ -4,8 +4,9 @@
 //
 // Randomness comes from the shared seeded generator she_inputs/she_rng.h
 // (masks, Gaussian noise, key bits); the arithmetic here is this library's
-// own (the oracle has an independent implementation; tests/test_client.py
-// checks the two produce identical key and ciphertext bytes).
+// own (the oracle has an independent implementation;
+// tests/test_client_and_emu.py checks the two produce identical key and
+// ciphertext bytes).
 #include <omp.h>
 #include <stdint.h>
 #include <string.h>

@@ -28,7 +28,9 @@ inline she_status check_params(const she_params* p) {
   if (!p) return fail(SHE_ERR_ARG, "params is NULL");
   if (p->k != 1) return fail(SHE_ERR_PARAMS, "k=%u unsupported (k=1 only)", p->k);
   if (p->N != 256 && p->N != 1024) return fail(SHE_ERR_PARAMS, "N=%u unsupported", p->N);
-  if (p->n == 0 || p->n > 1024) return fail(SHE_ERR_PARAMS, "n=%u unsupported", p->n);
+  // an LWE slot (n + 1 words padded to 32) must fit the key-switch kernels'
+  // 512 threads / 2 x 256 words per gate: n <= 511
+  if (p->n == 0 || p->n > 511) return fail(SHE_ERR_PARAMS, "n=%u unsupported (1..511)", p->n);
   if (p->l != 2) return fail(SHE_ERR_PARAMS, "l=%u unsupported (l=2: 4 rows = 4 warps)", p->l);
   if (p->bg_bits == 0 || p->l * p->bg_bits >= 32)
     return fail(SHE_ERR_PARAMS, "l*bg_bits=%u must be < 32", p->l * p->bg_bits);

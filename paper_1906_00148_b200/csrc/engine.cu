@@ -307,6 +307,76 @@ struct FLane {
 
 constexpr size_t kFftTables = 2 * 512 * sizeof(double2);  // pass-A twiddles, fwd + inv
 
+// The CMux product steps of the FP64 engine, shared by br_fft_kernel and the
+// device product self-test (she_fft_product_selftest) so that the test runs
+// exactly the arithmetic the blind rotation runs.
+//
+// Forward FFT of one digit row (32 digits per thread: coefficient lane + 32 m).
+__device__ __forceinline__ void fbr_forward_digits(const int32_t (&d)[32], int lane,
+                                                   const double2* tw_fwd, double2* row) {
+  double re[16], im[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    re[m] = fft::i2d(d[m]);
+    im[m] = fft::i2d(d[m + 16]);
+  }
+  fft::forward(re, im, lane, tw_fwd, row);
+}
+
+// Pointwise sum at frequency k of one lane: rows r = 0..3 hold the digit
+// spectra on entry and the products (o, half) = (q >> 1, q & 1) on exit;
+// b[r * 4 + q] = BK_i plane (r, o, half) at k (1/512 folded in).
+__device__ __forceinline__ void fbr_pointwise(double2* row0, int k, const double2 (&b)[16]) {
+  double2 a[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) a[r] = row0[r * fft::kRow + k];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // q = o * 2 + half
+    double2 c = fft::cmul(a[0], b[q]);
+#pragma unroll
+    for (int r = 1; r < 4; ++r) {
+      const double2 bb = b[r * 4 + q];
+      c.x = fma(a[r].x, bb.x, fma(-a[r].y, bb.y, c.x));
+      c.y = fma(a[r].x, bb.y, fma(a[r].y, bb.x, c.y));
+    }
+    row0[q * fft::kRow + k] = c;
+  }
+}
+
+// Inverse FFT of product row w = (o, half), rounded to the exact integer and
+// added into ACC_o (hi half shifted by 16; torus32 wrap).  TRACK: also the
+// largest distance of a pre-rounding value to its integer (self-test only).
+template <bool TRACK>
+__device__ __forceinline__ void fbr_inverse_acc(double2* row, int lane, const double2* tw_inv,
+                                                uint32_t* acc_o, int w,
+                                                unsigned long long* worst) {
+  constexpr int M = fft::kM;
+  double2 x[8], y[8];
+  fft::inverse(row, lane, tw_inv, row, x, y);
+  const int sh = (w & 1) ? 0 : 16;
+  const int k2 = lane >> 1, hh = lane & 1;
+  double dmax = 0.0;
+  // the pair (hh = 0, 1) of a column k2 hits the same bank for the same j:
+  // the odd thread takes j ^ 1 (register selects, no local memory)
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int jj = j ^ hh;
+    const double2 xv = hh ? x[j ^ 1] : x[j], yv = hh ? y[j ^ 1] : y[j];
+    const int n_x = k2 + 16 * (8 * hh + jj), n_y = k2 + 16 * (16 + 8 * hh + jj);
+    if (TRACK) {
+      dmax = fmax(dmax, fabs(xv.x - rint(xv.x)));
+      dmax = fmax(dmax, fabs(xv.y - rint(xv.y)));
+      dmax = fmax(dmax, fabs(yv.x - rint(yv.x)));
+      dmax = fmax(dmax, fabs(yv.y - rint(yv.y)));
+    }
+    atomicAdd(acc_o + n_x, fft::d2u_round(xv.x) << sh);
+    atomicAdd(acc_o + n_x + M, fft::d2u_round(xv.y) << sh);
+    atomicAdd(acc_o + n_y, fft::d2u_round(yv.x) << sh);
+    atomicAdd(acc_o + n_y + M, fft::d2u_round(yv.y) << sh);
+  }
+  if (TRACK) atomicMax(worst, (unsigned long long)__double_as_longlong(dmax));
+}
+
 struct BRFArgs {
   GateSrc src;
   const uint32_t* lanes;
@@ -370,13 +440,7 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
       if (on) {  // forward FFT of digit row w
         int32_t d[32];
         br::load_digits<S>(geo, w, lane, me.acc, me.abar[i], d);
-        double re[16], im[16];
-#pragma unroll
-        for (int m = 0; m < 16; ++m) {
-          re[m] = fft::i2d(d[m]);
-          im[m] = fft::i2d(d[m + 16]);
-        }
-        fft::forward(re, im, lane, tw_fwd, me.row(w));
+        fbr_forward_digits(d, lane, tw_fwd, me.row(w));
       }
       // BK_i planes of this thread's first frequency (k = tid) are requested
       // before the barrier, so their L2 latency overlaps the wait for the
@@ -392,23 +456,7 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
         auto pointwise = [&](int k, const double2 (&b)[16]) {
 #pragma unroll
           for (int gg = 0; gg < G; ++gg)
-            if (base + gg < last) {
-              FLane other(smem + (size_t)gg * lane_bytes);
-              double2 a[4];
-#pragma unroll
-              for (int r = 0; r < 4; ++r) a[r] = other.row(r)[k];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {  // q = o * 2 + half
-                double2 c = fft::cmul(a[0], b[q]);
-#pragma unroll
-                for (int r = 1; r < 4; ++r) {
-                  const double2 bb = b[r * 4 + q];
-                  c.x = fma(a[r].x, bb.x, fma(-a[r].y, bb.y, c.x));
-                  c.y = fma(a[r].x, bb.y, fma(a[r].y, bb.x, c.y));
-                }
-                other.row(q)[k] = c;
-              }
-            }
+            if (base + gg < last) fbr_pointwise(FLane(smem + (size_t)gg * lane_bytes).row(0), k, b);
         };
         if (tid < M) pointwise(tid, bpre);
         for (int k = tid + T; k < M; k += T) {
@@ -420,23 +468,7 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
       }
       __syncthreads();
       if (on) {  // inverse of output (o, half) = (w >> 1, w & 1), added into ACC_o
-        double2 x[8], y[8];
-        fft::inverse(me.row(w), lane, tw_inv, me.row(w), x, y);
-        uint32_t* acc = me.acc + (w >> 1) * N;
-        const int sh = (w & 1) ? 0 : 16;
-        const int k2 = lane >> 1, hh = lane & 1;
-        // the pair (hh = 0, 1) of a column k2 hits the same bank for the same
-        // j: the odd thread takes j ^ 1 (register selects, no local memory)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int jj = j ^ hh;
-          const double2 xv = hh ? x[j ^ 1] : x[j], yv = hh ? y[j ^ 1] : y[j];
-          const int n_x = k2 + 16 * (8 * hh + jj), n_y = k2 + 16 * (16 + 8 * hh + jj);
-          atomicAdd(acc + n_x, fft::d2u_round(xv.x) << sh);
-          atomicAdd(acc + n_x + M, fft::d2u_round(xv.y) << sh);
-          atomicAdd(acc + n_y, fft::d2u_round(yv.x) << sh);
-          atomicAdd(acc + n_y + M, fft::d2u_round(yv.y) << sh);
-        }
+        fbr_inverse_acc<false>(me.row(w), lane, tw_inv, me.acc + (w >> 1) * N, w, nullptr);
         lane_sync(1 + g);
       }
     }
@@ -483,6 +515,46 @@ __global__ void bk_fft_kernel(const uint32_t* bk, double2* out, uint32_t polys) 
     const double2 v = row[k];
     o[k] = make_double2(v.x * (1.0 / 512), v.y * (1.0 / 512));
   }
+}
+
+// Test instrumentation (she_fft_product_selftest): case c computes
+//   out[c][o] = sum_{r<4} digits[c][r] * BK_c[r][o]  mod (X^N + 1), mod 2^32
+// with the FP64 engine's own steps (fbr_forward_digits, fbr_pointwise on the
+// FFT-domain BK made by bk_fft_kernel, fbr_inverse_acc), one CTA of 4 warps per
+// case (warp w = digit row w, then output row w), and the largest distance of
+// a pre-rounding value to its integer.
+__global__ void __launch_bounds__(128) fft_selftest_kernel(const int32_t* digits,
+                                                           const double2* bkf, uint32_t* out,
+                                                           unsigned long long* worst) {
+  constexpr int N = fft::kN, M = fft::kM;
+  extern __shared__ __align__(16) uint8_t smem[];  // kFftSelftestSmem bytes
+  double2* rows = reinterpret_cast<double2*>(smem);
+  double2* tw = rows + 4 * fft::kRow;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(tw + 2 * 512);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const size_t c = blockIdx.x;
+  fft::make_tables(tid, 128, tw, tw + 512);
+  for (int m = tid; m < 2 * N; m += 128) acc[m] = 0;
+  __syncthreads();
+  {
+    const int32_t* d = digits + (c * 4 + w) * N;
+    int32_t dd[32];
+#pragma unroll
+    for (int j2 = 0; j2 < 32; ++j2) dd[j2] = d[lane + 32 * j2];
+    fbr_forward_digits(dd, lane, tw, rows + w * fft::kRow);
+  }
+  __syncthreads();
+  const double2* bki = bkf + c * 16 * M;
+  for (int k = tid; k < M; k += 128) {
+    double2 b[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) b[q] = bki[(size_t)q * M + k];
+    fbr_pointwise(rows, k, b);
+  }
+  __syncthreads();
+  fbr_inverse_acc<true>(rows + w * fft::kRow, lane, tw + 512, acc + (w >> 1) * N, w, worst);
+  __syncthreads();
+  for (int m = tid; m < 2 * N; m += 128) out[c * 2 * N + m] = acc[m];
 }
 
 // Compact lane list of a gate batch: gate g contributes lane (g, 0) if it is
@@ -663,7 +735,7 @@ __global__ void __launch_bounds__(kKs2T, 2) ks2_kernel(KSArgs args) {
     acc[q][1] = (k + kKs2T == n) ? bprime[q] : 0u;
   }
 
-  const bool hb = k + kKs2T < stride;  // second word exists (stride 512 at C1, 160 at C0)
+  const bool ha = k < stride, hb = k + kKs2T < stride;  // words k, k + 256 exist (stride 512 / 160)
   for (uint32_t i0 = 0; i0 < N; i0 += CH) {
     __syncthreads();
     for (uint32_t idx = k; idx < (uint32_t)G * CH; idx += kKs2T) {
@@ -687,8 +759,12 @@ __global__ void __launch_bounds__(kKs2T, 2) ks2_kernel(KSArgs args) {
 #pragma unroll
       for (int j = 0; j < T; ++j) {
         const uint32_t* r = rows + (size_t)(3 * j) * stride;
-        const uint32_t k1a = __ldg(r), k2a = __ldg(r + stride), n3a = __ldg(r + 2 * stride);
-        uint32_t k1b = 0, k2b = 0, n3b = 0;
+        uint32_t k1a = 0, k2a = 0, n3a = 0, k1b = 0, k2b = 0, n3b = 0;
+        if (ha) {  // stride 160 at C0: threads past the row read nothing
+          k1a = __ldg(r);
+          k2a = __ldg(r + stride);
+          n3a = __ldg(r + 2 * stride);
+        }
         if (hb) {
           k1b = __ldg(r + kKs2T);
           k2b = __ldg(r + stride + kKs2T);
@@ -888,6 +964,8 @@ struct she_ctx {
   uint32_t* h_io = nullptr;
   size_t h_cap = 0;
   bool persist = false;
+  size_t window_bytes = 0;  // access-policy window over the engine's BK
+  float window_hit = 1.0f;
   std::mutex mu;
   // wire table + program buffers of the layer scheduler
   uint32_t* table = nullptr;
@@ -942,23 +1020,26 @@ template <class S>
 she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
   const she_params& p = ctx->p;
   const size_t polys = (size_t)p.n * 2 * p.l * 2;
-  ctx->bk_bytes = polys * p.N * sizeof(uint64_t);
-  CK(cudaMalloc(&ctx->bk, ctx->bk_bytes));
-  CK(cudaMalloc(&ctx->tw, sizeof(uint64_t) * S::L * S::L));
-  CK(cudaMalloc(&ctx->itw, sizeof(uint64_t) * S::L * S::L));
-  std::vector<uint64_t> tw(S::L * S::L), itw(S::L * S::L);
-  ntt::make_twists(S::N, S::L, S::SH, tw.data(), itw.data());
-  CK(cudaMemcpy(ctx->tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->itw, itw.data(), itw.size() * 8, cudaMemcpyHostToDevice));
   uint32_t* d_bk32 = nullptr;
   CK(cudaMalloc(&d_bk32, polys * p.N * 4));
   CK(cudaMemcpy(d_bk32, ck->bk.data(), polys * p.N * 4, cudaMemcpyHostToDevice));
-  const uint64_t ninv = gl::pow(p.N, gl::P - 2);
-  bk_transform_kernel<S><<<(unsigned)polys, 32>>>(d_bk32, ctx->bk, ctx->tw, ninv, (uint32_t)polys);
-  CK(cudaGetLastError());
-  CK(cudaDeviceSynchronize());
-  if (ctx->fft_g && S::N == fft::kN) {
-    CK(cudaMalloc(&ctx->bkf, (size_t)p.n * 16 * fft::kM * sizeof(double2)));
+  if (!ctx->fft_g) {  // NTT engine: BK in the Goldilocks NTT domain
+    ctx->bk_bytes = polys * p.N * sizeof(uint64_t);
+    CK(cudaMalloc(&ctx->bk, ctx->bk_bytes));
+    CK(cudaMalloc(&ctx->tw, sizeof(uint64_t) * S::L * S::L));
+    CK(cudaMalloc(&ctx->itw, sizeof(uint64_t) * S::L * S::L));
+    std::vector<uint64_t> tw(S::L * S::L), itw(S::L * S::L);
+    ntt::make_twists(S::N, S::L, S::SH, tw.data(), itw.data());
+    CK(cudaMemcpy(ctx->tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->itw, itw.data(), itw.size() * 8, cudaMemcpyHostToDevice));
+    const uint64_t ninv = gl::pow(p.N, gl::P - 2);
+    bk_transform_kernel<S><<<(unsigned)polys, 32>>>(d_bk32, ctx->bk, ctx->tw, ninv, (uint32_t)polys);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+  }
+  if (ctx->fft_g && S::N == fft::kN) {  // FFT engine: BK halves in the FFT domain
+    ctx->bk_bytes = (size_t)p.n * 16 * fft::kM * sizeof(double2);
+    CK(cudaMalloc(&ctx->bkf, ctx->bk_bytes));
     bk_fft_kernel<<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkf, (uint32_t)polys);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
@@ -1026,8 +1107,8 @@ she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream
   if (ctx->persist) {
     attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
     attr[0].val.accessPolicyWindow.base_ptr = ctx->bk;
-    attr[0].val.accessPolicyWindow.num_bytes = ctx->bk_bytes;
-    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[0].val.accessPolicyWindow.num_bytes = ctx->window_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = ctx->window_hit;
     attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.attrs = attr;
@@ -1047,10 +1128,23 @@ she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaSt
   f.ext = a.ext;
   f.ext_stride = a.ext_stride;
   f.geo = a.geo;
-  const unsigned grid =
-      (unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms * B));
-  br_fft_kernel<G, B><<<grid, 128 * G, G * FLane::bytes(ctx->p.n) + kFftTables, stream>>>(f);
-  CK(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms * B)));
+  cfg.blockDim = dim3(128 * G);
+  cfg.dynamicSmemBytes = G * FLane::bytes(ctx->p.n) + kFftTables;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (ctx->persist) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = ctx->bkf;
+    attr[0].val.accessPolicyWindow.num_bytes = ctx->window_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = ctx->window_hit;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  CK(cudaLaunchKernelEx(&cfg, br_fft_kernel<G, B>, f));
   return SHE_OK;
 }
 
@@ -1134,12 +1228,41 @@ extern "C" {
 
 she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int device, int rank,
                           int world, she_ctx** out) {
+  return she_ctx_create_ex(p, ck, device, rank, world, nullptr, out);
+}
+
+she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int device, int rank,
+                             int world, const she_ctx_options* opt, she_ctx** out) {
   she_status st = check_params(p);
   if (st != SHE_OK) return st;
   if (!ck || !out) return fail(SHE_ERR_ARG, "NULL argument");
   if (memcmp(&ck->p, p, sizeof(she_params)) != 0)
     return fail(SHE_ERR_PARAMS, "cloud key was made for other parameters");
   if (world < 1 || rank < 0 || rank >= world) return fail(SHE_ERR_ARG, "bad rank/world");
+  she_ctx_options o = {};
+  if (opt) o = *opt;
+  for (int r : o.reserved)
+    if (r != 0) return fail(SHE_ERR_ARG, "she_ctx_options.reserved must be 0");
+  // the FFT engine is exact for N = 1024 while the digit bound keeps the
+  // round-off below 1/2 (Bg <= 2^12 leaves > 100x margin)
+  const bool fft_ok = p->N == fft::kN && p->bg_bits <= 12;
+  if (o.br_engine < 0 || o.br_engine > 2) return fail(SHE_ERR_ARG, "br_engine=%d", o.br_engine);
+  if (o.br_engine == 1 && !fft_ok)
+    return fail(SHE_ERR_ARG, "the FFT engine needs N = 1024 and bg_bits <= 12");
+  const bool use_fft = o.br_engine == 1 || (o.br_engine == 0 && fft_ok);
+  if (o.fft_lanes != 0 && o.fft_lanes != 2 && o.fft_lanes != 3 && o.fft_lanes != 4 &&
+      o.fft_lanes != 5)
+    return fail(SHE_ERR_ARG, "fft_lanes=%d: expected 0, 2, 3, 4 or 5", o.fft_lanes);
+  if (o.fft_lanes && !use_fft) return fail(SHE_ERR_ARG, "fft_lanes given for the NTT engine");
+  bool known = o.ntt_lanes == 0 && o.ntt_ctas == 0;
+#define SHE_BR_KNOWN(G, B) known = known || (o.ntt_lanes == G && o.ntt_ctas == B);
+  SHE_BR_CONFIGS(SHE_BR_KNOWN)
+#undef SHE_BR_KNOWN
+  if (!known)
+    return fail(SHE_ERR_ARG, "NTT shape %dx%d is not instantiated", o.ntt_lanes, o.ntt_ctas);
+  if ((o.ntt_lanes || o.ntt_ctas) && use_fft)
+    return fail(SHE_ERR_ARG, "ntt_lanes/ntt_ctas given for the FFT engine");
+  if (o.ks_kernel < 0 || o.ks_kernel > 1) return fail(SHE_ERR_ARG, "ks_kernel=%d", o.ks_kernel);
   CK(cudaSetDevice(device));
   she_ctx* ctx = new (std::nothrow) she_ctx;
   if (!ctx) return fail(SHE_ERR_OOM, "host allocation failed");
@@ -1151,32 +1274,11 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
   ctx->stride = (uint32_t)lwe_stride(*p);
   ctx->ext_stride = (p->N + 1 + 31) / 32 * 32;
   cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
-  if (const char* e = getenv("SHE_BR_CFG")) {
-    int g = 0, b = 0;
-    bool ok = sscanf(e, "%dx%d", &g, &b) == 2;
-    bool known = false;
-#define SHE_BR_KNOWN(G, B) known = known || (g == G && b == B);
-    SHE_BR_CONFIGS(SHE_BR_KNOWN)
-#undef SHE_BR_KNOWN
-    if (!ok || !known) {
-      delete ctx;
-      return fail(SHE_ERR_ARG, "SHE_BR_CFG=%s is not an instantiated GxB shape", e);
-    }
-    ctx->br_g = g;
-    ctx->br_b = b;
+  if (o.ntt_lanes) {
+    ctx->br_g = o.ntt_lanes;
+    ctx->br_b = o.ntt_ctas;
   }
-  if (const char* e = getenv("SHE_BR_ENGINE")) {
-    if (strcmp(e, "fft") == 0 || strcmp(e, "fft4") == 0) ctx->fft_g = 4;
-    else if (strcmp(e, "fft3") == 0) ctx->fft_g = 3;
-    else if (strcmp(e, "fft5") == 0) ctx->fft_g = 5;
-    else if (strcmp(e, "fft2x2") == 0) ctx->fft_g = 2;
-    else if (strcmp(e, "ntt") == 0) ctx->fft_g = 0;
-    else {
-      delete ctx;
-      return fail(SHE_ERR_ARG, "SHE_BR_ENGINE=%s: expected fft, fft2x2, fft3, fft4, fft5 or ntt", e);
-    }
-  }
-  if (p->N != fft::kN) ctx->fft_g = 0;
+  ctx->fft_g = use_fft ? (o.fft_lanes ? o.fft_lanes : 4) : 0;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
     she_ctx_destroy(ctx);
@@ -1192,11 +1294,9 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
         for (uint32_t v = 1; v < base; ++v)
           memcpy(&h[(((size_t)i * t + j) * 3 + (v - 1)) * ctx->stride],
                  &ck->ksk[(((size_t)i * t + j) * base + v) * (n + 1)], (n + 1) * 4);
-    // SHE_KS_KERNEL=legacy forces ks_kernel (the general-parameter path) so
-    // that the tests can pin it on the configs' parameters as well
-    const char* ksk_env = getenv("SHE_KS_KERNEL");
-    const bool legacy = ksk_env && strcmp(ksk_env, "legacy") == 0;
-    ctx->ks2 = !legacy && (t == 8 && base == 4 && ctx->stride <= 2 * (uint32_t)kKs2T);
+    // ks_kernel = 1 forces ks_kernel (the general-parameter path) so that the
+    // tests can pin it on the configs' parameters as well
+    ctx->ks2 = o.ks_kernel == 0 && (t == 8 && base == 4 && ctx->stride <= 2 * (uint32_t)kKs2T);
     if (ctx->ks2)  // third row -> K1 + K2 - K3 (mod 2^32), see ks2_kernel
       for (size_t r = 0; r < (size_t)N * t; ++r) {
         uint32_t* row = &h[r * 3 * ctx->stride];
@@ -1210,13 +1310,18 @@ she_status she_ctx_create(const she_params* p, const she_cloud_key* ck, int devi
       return cuda_fail(e, "KSK upload");
     }
   }
-  // keep the NTT-domain BK L2-resident (persisting window on the BR launches)
+  // keep the BK of the selected engine L2-resident (persisting window on the
+  // blind-rotation launches)
   {
     int maxp = 0;
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
     if (maxp > 0) {
+      int maxw = 0;
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device);
       size_t want = std::min((size_t)maxp, ctx->bk_bytes);
-      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+      ctx->window_bytes = std::min((size_t)std::max(maxw, 0), ctx->bk_bytes);
+      ctx->window_hit = ctx->window_bytes ? std::min(1.0f, (float)want / ctx->window_bytes) : 0.f;
+      if (ctx->window_bytes && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
         ctx->persist = true;
     }
     cudaGetLastError();
@@ -1422,6 +1527,51 @@ she_status she_field_selftest(int device, const uint64_t* a, const uint64_t* b, 
   return st;
 }
 
+she_status she_fft_product_selftest(int device, const int32_t* digits, const uint32_t* bk,
+                                    size_t count, uint32_t* out, double* worst_distance) {
+  if (count == 0) return SHE_OK;
+  if (!digits || !bk || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  if (count > 65535) return fail(SHE_ERR_ARG, "count > 65535");
+  constexpr size_t N = fft::kN;
+  CK(cudaSetDevice(device));
+  int32_t* dd = nullptr;
+  uint32_t *db = nullptr, *dout = nullptr;
+  double2* dbkf = nullptr;
+  unsigned long long* dworst = nullptr;
+  she_status st = SHE_OK;
+  cudaError_t e = cudaMalloc(&dd, count * 4 * N * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&db, count * 8 * N * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, count * 2 * N * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dbkf, count * 16 * fft::kM * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&dworst, 8);
+  if (e == cudaSuccess) e = cudaMemset(dworst, 0, 8);
+  if (e == cudaSuccess) e = cudaMemcpy(dd, digits, count * 4 * N * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(db, bk, count * 8 * N * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {  // the setup transform of the engine (BK -> FFT domain, halves)
+    bk_fft_kernel<<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
+    e = cudaGetLastError();
+  }
+  constexpr size_t smem = (4 * fft::kRow + 2 * 512) * sizeof(double2) + 2 * N * 4;
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fft_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+  if (e == cudaSuccess) {
+    fft_selftest_kernel<<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, count * 2 * N * 4, cudaMemcpyDeviceToHost);
+  unsigned long long wbits = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&wbits, dworst, 8, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) st = cuda_fail(e, "fft product selftest");
+  else if (worst_distance) memcpy(worst_distance, &wbits, 8);
+  cudaFree(dd);
+  cudaFree(db);
+  cudaFree(dout);
+  cudaFree(dbkf);
+  cudaFree(dworst);
+  return st;
+}
+
 she_status she_ctx_synchronize(she_ctx* ctx) {
   if (!ctx) return fail(SHE_ERR_ARG, "NULL context");
   CK(cudaSetDevice(ctx->device));
@@ -1436,7 +1586,8 @@ static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
-static she_status gate_batch_common(she_ctx* ctx, const uint8_t* ops, int op, const uint32_t* a,
+// Caller holds ctx->mu.
+static she_status gate_batch_locked(she_ctx* ctx, const uint8_t* ops, int op, const uint32_t* a,
                                     const uint32_t* b, const uint32_t* c, uint32_t* out,
                                     size_t count, void* stream) {
   if (count == 0) return SHE_OK;
@@ -1449,7 +1600,6 @@ static she_status gate_batch_common(she_ctx* ctx, const uint8_t* ops, int op, co
   if (overlaps(out, bytes, a, bytes) || overlaps(out, bytes, b, bytes) ||
       overlaps(out, bytes, c, bytes))
     return fail(SHE_ERR_ARG, "out overlaps an input");
-  std::lock_guard<std::mutex> lk(ctx->mu);
   CK(cudaSetDevice(ctx->device));
   GateSrc s = {};
   s.ops = ops;
@@ -1461,6 +1611,15 @@ static she_status gate_batch_common(she_ctx* ctx, const uint8_t* ops, int op, co
   s.stride = ctx->stride;
   s.count = (uint32_t)count;
   return dispatch(ctx, s, (cudaStream_t)stream);
+}
+
+static she_status gate_batch_common(she_ctx* ctx, const uint8_t* ops, int op, const uint32_t* a,
+                                    const uint32_t* b, const uint32_t* c, uint32_t* out,
+                                    size_t count, void* stream) {
+  if (count == 0) return SHE_OK;
+  if (!ctx) return fail(SHE_ERR_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return gate_batch_locked(ctx, ops, op, a, b, c, out, count, stream);
 }
 
 she_status she_gate_batch(she_ctx* ctx, int op, const uint32_t* a, const uint32_t* b,
@@ -1483,9 +1642,11 @@ she_status she_gate_batch_ops_host(she_ctx* ctx, const uint8_t* ops, const uint3
   if (!ctx || !ops || !a || !b || !c || !out) return fail(SHE_ERR_ARG, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
   const size_t slots = count * ctx->stride;
+  // one lock over staging, evaluation and the copy back: the staging buffer
+  // h_io belongs to this call until the stream has been synchronised
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
   {
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CK(cudaSetDevice(ctx->device));
     if (ctx->h_cap < count) {
       cudaStreamSynchronize(st);
       cudaFree(ctx->h_ops);
@@ -1502,8 +1663,8 @@ she_status she_gate_batch_ops_host(she_ctx* ctx, const uint8_t* ops, const uint3
     CK(cudaMemcpyAsync(ctx->h_io + slots, b, slots * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(ctx->h_io + 2 * slots, c, slots * 4, cudaMemcpyHostToDevice, st));
   }
-  she_status s = she_gate_batch_ops(ctx, ctx->h_ops, ctx->h_io, ctx->h_io + slots,
-                                    ctx->h_io + 2 * slots, ctx->h_io + 3 * slots, count, stream);
+  she_status s = gate_batch_locked(ctx, ctx->h_ops, 0, ctx->h_io, ctx->h_io + slots,
+                                   ctx->h_io + 2 * slots, ctx->h_io + 3 * slots, count, stream);
   if (s != SHE_OK) return s;
   CK(cudaMemcpyAsync(out, ctx->h_io + 3 * slots, slots * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

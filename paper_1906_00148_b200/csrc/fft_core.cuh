@@ -19,9 +19,10 @@
 //           odd (h = 1) points n1 of column k2, then one radix-2 step across the
 //           thread pair (shfl.xor 1) gives X[k2 + 16 k1] for k1 = 8h + j and
 //           16 + 8h + j (j < 8).
-// One padded shared-memory transpose (17 complex per row: conflict-free both
+// One XOR-swizzled shared-memory transpose (tslot below: conflict-free both
 // ways) sits between the passes.  Constant twiddles come from the constant bank
-// (compile-time indices); per-thread twiddles by recurrence.
+// (compile-time indices); the per-thread pass-A twiddles from a shared table
+// filled with sincospi at kernel start (make_tables).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -11,7 +11,8 @@
 // 2^192 = 1: powers of two are "shift twiddles".
 //
 // All functions are __host__ __device__ so the exact same code is unit-tested
-// on the CPU (tests/test_ntt_host.py via libshe_host.so) and runs on sm_100a.
+// on the CPU (tests/test_client_and_emu.py via libshe_hostemu.so, built from
+// host_emu.cpp) and runs on sm_100a.
 #pragma once
 #include <stdint.h>
 

@@ -41,6 +41,20 @@ class she_params(ctypes.Structure):
         return cls(p.N, p.k, p.n, p.bg_bits, p.l, p.ks_base_bits, p.ks_t, p.alpha_lwe, p.alpha_bk)
 
 
+class she_ctx_options(ctypes.Structure):
+    """include/she.h she_ctx_options: engine selection (all engines are exact)."""
+    _fields_ = [("br_engine", ctypes.c_int), ("fft_lanes", ctypes.c_int),
+                ("ntt_lanes", ctypes.c_int), ("ntt_ctas", ctypes.c_int),
+                ("ks_kernel", ctypes.c_int), ("reserved", ctypes.c_int * 7)]
+
+    ENGINES = {"default": 0, "fft": 1, "ntt": 2}
+
+    @classmethod
+    def of(cls, engine="default", fft_lanes=0, ntt_shape=(0, 0), ks_kernel="default"):
+        return cls(cls.ENGINES[engine], fft_lanes, ntt_shape[0], ntt_shape[1],
+                   {"default": 0, "general": 1}[ks_kernel])
+
+
 class she_circuit_stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_uint64) for k in
                 ("gates", "br_lanes", "levels", "max_level_width", "min_level_width", "tiles")]
@@ -75,6 +89,8 @@ def lib() -> ctypes.CDLL:
             "she_decrypt_bits": ([_vp, _vp, _sz, _vp], ctypes.c_int),
             "she_ctx_create": ([P, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)],
                                ctypes.c_int),
+            "she_ctx_create_ex": ([P, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                   ctypes.POINTER(she_ctx_options), ctypes.POINTER(_vp)], ctypes.c_int),
             "she_ctx_destroy": ([_vp], ctypes.c_int),
             "she_ctx_synchronize": ([_vp], ctypes.c_int),
             "she_gate_batch": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
@@ -119,6 +135,8 @@ def lib() -> ctypes.CDLL:
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_field_selftest": ([ctypes.c_int, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_fft_product_selftest": ([ctypes.c_int, _vp, _vp, _sz, _vp,
+                                          ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
             "she_encrypt_noise": ([_vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
             "she_encrypt_bits_gpu": ([_vp, _vp, _vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp,
                                       ctypes.c_int, _vp], ctypes.c_int),
@@ -248,12 +266,16 @@ def she_decrypt_bits(sk: SecretKey, cts) -> np.ndarray:
 # ---- server side -------------------------------------------------------------
 
 class Context:
-    """she_ctx: device keys (BK in the NTT domain, KSK) on one CUDA device."""
+    """she_ctx: device keys (BK in the engine's transform domain, KSK) on one
+    CUDA device.  Keyword options (she_ctx_options): engine = "default" | "fft"
+    | "ntt", fft_lanes, ntt_shape = (G, B), ks_kernel = "default" | "general"."""
 
-    def __init__(self, params, ck: CloudKey, device: int = 0, rank: int = 0, world: int = 1):
+    def __init__(self, params, ck: CloudKey, device: int = 0, rank: int = 0, world: int = 1,
+                 **options):
         h = _vp()
-        _check(lib().she_ctx_create(ctypes.byref(she_params.of(params)), ck.handle, device, rank,
-                                    world, ctypes.byref(h)))
+        opt = she_ctx_options.of(**options)
+        _check(lib().she_ctx_create_ex(ctypes.byref(she_params.of(params)), ck.handle, device, rank,
+                                       world, ctypes.byref(opt), ctypes.byref(h)))
         self.handle, self.params, self.device = h.value, params, device
         self.stride = stride(params)
 
@@ -604,6 +626,21 @@ def field_selftest(device: int, a, b, c) -> np.ndarray:
     out = np.zeros((len(a), 104), dtype=np.uint64)
     _check(lib().she_field_selftest(device, _np_ptr(a), _np_ptr(b), _np_ptr(c), len(a), _np_ptr(out)))
     return out
+
+
+def fft_product_selftest(device: int, digits, bk):
+    """FP64-engine CMux product on given inputs (test instrumentation, she.h):
+    digits int32 [count][4][1024], bk uint32 [count][4][2][1024] ->
+    (out uint32 [count][2][1024], worst distance to an integer)."""
+    digits = np.ascontiguousarray(digits, dtype=np.int32)
+    bk = np.ascontiguousarray(bk, dtype=np.uint32)
+    count = digits.shape[0]
+    assert digits.shape == (count, 4, 1024) and bk.shape == (count, 4, 2, 1024)
+    out = np.zeros((count, 2, 1024), dtype=np.uint32)
+    worst = ctypes.c_double(0.0)
+    _check(lib().she_fft_product_selftest(device, _np_ptr(digits), _np_ptr(bk), count,
+                                          _np_ptr(out), ctypes.byref(worst)))
+    return out, worst.value
 
 
 # ---- client side on the GPU (she.h, NEXT-4) -----------------------------------

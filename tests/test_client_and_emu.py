@@ -184,3 +184,35 @@ def test_encrypt_noise_is_the_host_clients_noise(params):
     mu = np.where(bits == 1, 1 << 29, (1 << 32) - (1 << 29)).astype(np.uint64)
     ph = oracle.phases(params, K.s, cts).astype(np.uint64)
     assert np.array_equal((ph - mu) % (1 << 32), noise.astype(np.uint64))
+
+
+@pytest.mark.parametrize("opts, why", [
+    (dict(engine="fft"), "FFT engine at N = 256"),
+    (dict(engine="ntt", fft_lanes=3), "fft_lanes for the NTT engine"),
+    (dict(ntt_shape=(9, 9)), "uninstantiated NTT shape"),
+    (dict(fft_lanes=7), "unknown FFT lane count"),
+], ids=["fft-at-N256", "lanes-for-ntt", "shape-9x9", "lanes-7"])
+def test_ctx_options_rejected_before_any_device_work(opts, why):
+    """she_ctx_create_ex validates she_ctx_options on the host (SHE_ERR_ARG)
+    before it touches CUDA, so these run without a GPU."""
+    P = si.C0
+    _, ck = she.she_keygen(P, 5)
+    with pytest.raises(she.SheError) as e:
+        she.Context(P, ck, device=0, **opts)
+    assert e.value.status == -1, why
+
+
+def test_ctx_options_reserved_and_params_checked():
+    P = si.C0
+    _, ck = she.she_keygen(P, 5)
+    opt = she.she_ctx_options.of()
+    opt.reserved[3] = 1
+    h = ctypes.c_void_p()
+    st = she.lib().she_ctx_create_ex(ctypes.byref(she.she_params.of(P)), ck.handle, 0, 0, 1,
+                                     ctypes.byref(opt), ctypes.byref(h))
+    assert st == -1
+    import dataclasses
+    big = dataclasses.replace(P, n=600)
+    st = she.lib().she_ctx_create_ex(ctypes.byref(she.she_params.of(big)), ck.handle, 0, 0, 1,
+                                     None, ctypes.byref(h))
+    assert st == -2  # n > 511: SHE_ERR_PARAMS (include/she.h she_params)

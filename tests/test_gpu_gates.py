@@ -285,18 +285,21 @@ def test_config1_full_parity_vs_oracle_digests(env1, config1_outputs):
     assert np.array_equal(she.she_decrypt_bits(env1.sk, out), want)
 
 
-@pytest.mark.parametrize("engine", ["ntt", "fft3"])
-def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, monkeypatch, engine):
+ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3),
+               "fft2x2": dict(engine="fft", fft_lanes=2)}
+
+
+@pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2"])
+def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with 4 lanes per
-    CTA; the Goldilocks NTT engine (SHE_BR_ENGINE=ntt) and the 3-lane FFT shape
-    must give the same ciphertexts bit for bit (both products are exact,
-    DESIGN.md §4.2b): all 4096 config-1 gates against the oracle digests."""
+    CTA; the Goldilocks NTT engine (she_ctx_options.br_engine = 2) and the other
+    FFT shapes must give the same ciphertexts bit for bit (both products are
+    exact): all 4096 config-1 gates against the oracle digests."""
     assert she.br_engine(env1.ctx) == 4
     assert she.br_engine(env0_ctx()) == 0  # N = 256 has no FFT engine
-    monkeypatch.setenv("SHE_BR_ENGINE", engine)
     P = env1.P
-    ctx = she.Context(P, env1.ck, device=0)
-    assert she.br_engine(ctx) == (0 if engine == "ntt" else 3)
+    ctx = she.Context(P, env1.ck, device=0, **ENGINE_OPTS[engine])
+    assert she.br_engine(ctx) == {"ntt": 0, "fft3": 3, "fft2x2": 2}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
     she.she_gate_batch_ops(ctx, dev(np.asarray(ops, np.uint8)), dev(a), dev(b), dev(c), out)
@@ -386,14 +389,13 @@ def test_gpu_client_matches_host_client(cuda, cfg):
 
 
 
-def test_legacy_key_switch_kernel_c0(cuda, monkeypatch):
+def test_legacy_key_switch_kernel_c0(cuda):
     """ks_kernel (any base / t; used when the key-switching parameters are not
     base 4, t = 8) on the config-0 gates: bit-exact with the oracle too."""
-    monkeypatch.setenv("SHE_KS_KERNEL", "legacy")
     cfg, count = 0, 16
     P = si.CONFIG_PARAMS[cfg]
     sk, ck = she.she_keygen(P, si.key_seed(cfg))
-    ctx = she.Context(P, ck, device=0)
+    ctx = she.Context(P, ck, device=0, ks_kernel="general")
     ops = si.gate_ops(cfg, count)
     bits = si.gate_input_bits(cfg, count)
     cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0).reshape(count, 3, -1)
