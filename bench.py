@@ -11,9 +11,11 @@ NAND/AND/OR/XOR/XNOR/MUX, input bits uniform (she_inputs).
 Inputs are resident in HBM when the timed region starts; L2 is flushed
 (256 MiB write) between timed steps, outside the per-step CUDA-event pairs.
 
-N > 1 (torchrun): every rank runs its own 4096-gate batch (weak scaling, no
-data-path collective — the gates are independent); value = all ranks' gates
-/ max-over-ranks device time.
+N > 1 (torchrun, or `--gpus N` alone: bench.py then launches the N ranks
+itself): the 4096 gates are split across the ranks (4096/N each) and the
+output LWEs are all-gathered (NCCL) inside the step — strong scaling, value =
+4096 / max-over-ranks device time; the weak-scaled figure (every rank its own
+4096-gate batch, no collective) is reported beside it as "weak_scaled".
 
 --impl reference: the CPU oracle (oracle/, schoolbook TFHE) timed on this
 box's host cores on a bounded sample of the same workload, rank 0 only.
@@ -450,15 +452,22 @@ def run_she(args):
     import torch
     import torch.distributed as dist
     from paper_1906_00148_b200 import she
-
+    from paper_1906_00148_b200 import parallel
     from paper_1906_00148_b200.parallel import max_over_ranks
+
     world, rank, local = dist_env()
-    # SHE_BENCH_BACKEND=gloo + SHE_BENCH_DEVICE=0 run N ranks on one GPU: a
-    # functional check of the N > 1 code path only (timings meaningless).
+    # SHE_BENCH_BACKEND=gloo runs the N ranks with gloo collectives (CPU
+    # staging), e.g. several ranks on one GPU: a functional check of the N > 1
+    # code path (its timings say nothing about NVLink).
     backend = os.environ.get("SHE_BENCH_BACKEND", "nccl")
-    local = int(os.environ.get("SHE_BENCH_DEVICE", local))
+    ndev = max(1, torch.cuda.device_count())
+    local = int(os.environ.get("SHE_BENCH_DEVICE", local % ndev))
     if world > 1:
         if backend == "nccl":
+            # communicator set-up lines on stderr (the JSON line stays alone on stdout)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -468,81 +477,116 @@ def run_she(args):
     ctx = she.Context(P, ck, device=local, rank=rank, world=world, **engine_options(args))
     ops = si.gate_ops(CFG, COUNT)
     bits = si.gate_input_bits(CFG, COUNT)
-    # every rank evaluates its own batch: distinct ciphertexts (ordinal offset by rank)
-    cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(CFG), 3 * COUNT * rank)
-    cts = cts.reshape(COUNT, 3, -1)
-    lanes = si.br_lanes(ops)
     stride = P.stride
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).cuda()
+    # the config-1 batch, identical on every rank; rank r evaluates its shard
+    # [r*per, (r+1)*per) and the output LWEs are all-gathered (strong scaling)
+    cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(CFG), 0).reshape(COUNT, 3, -1)
+    lo, hi, per = parallel.shard(COUNT, rank, world)
+    lanes = si.br_lanes(ops)
+    lanes_rank = si.br_lanes(ops[lo:hi])
     d_ops = torch.from_numpy(ops.astype(np.uint8)).cuda()
     d_a, d_b, d_c = (dev(cts[:, j].copy()) for j in range(3))
-    d_out = torch.empty((COUNT, stride), dtype=torch.int32, device="cuda")
+    d_out = torch.zeros((parallel.padded_words(COUNT, world), stride), dtype=torch.int32,
+                        device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
     def step():
-        she.she_gate_batch_ops(ctx, d_ops, d_a, d_b, d_c, d_out, stream)
+        parallel.gate_batch_sharded(ctx, d_ops, d_a, d_b, d_c, d_out, rank, world, stream)
 
     peak, k6, derived, ipm, peak_src = roofline_peak(local, she.LIB_PATH, None)
     engine = she.br_engine(ctx)
     fp64_peak = she.fp64_peak(local)[0] if engine else None
 
+    def timed(fn, steps, kernel_timing=False):
+        """K steps bracketed by a barrier + synchronize, one CUDA-event pair per
+        step on the launch stream, L2 flushed between steps (outside the pairs);
+        returns the max over ranks of the summed device time (ms)."""
+        if kernel_timing:
+            ctx.enable_timing(True)
+            ctx.timing(reset=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        for k in range(steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            fn()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = None
+        if kernel_timing:
+            ctx.enable_timing(False)
+            t = ctx.timing(reset=True)
+        return max_over_ranks([sum(a.elapsed_time(b) for a, b in evs)], world)[0], t
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, per-step event pairs, L2 flushed between ----
-    ctx.enable_timing(True)
-    ctx.timing(reset=True)
+    # ---- timed region: the strong-scaled config-1 step ----
     clocks = ClockSampler(local)
     clocks.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    for k in range(args.steps):
-        flush.zero_()
-        evs[k][0].record(stream)
-        step()
-        evs[k][1].record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    dev_ms, t = timed(step, args.steps, kernel_timing=True)
     clk = clocks.stop()
-    ctx.enable_timing(False)
-    t = ctx.timing(reset=True)
-    dev_ms = max_over_ranks([sum(a.elapsed_time(b) for a, b in evs)], world)[0]
     ms_per_step = dev_ms / args.steps
-    value = world * COUNT * args.steps / (dev_ms * 1e-3)
+    value = COUNT * args.steps / (dev_ms * 1e-3)
+    gpu_out = d_out[:COUNT].cpu().numpy().view(np.uint32).copy()
 
-    # dominant kernel: the blind rotation (K2+K3)
+    # ---- weak scaling beside it: every rank its own 4096-gate batch ----
+    weak = None
+    if world > 1:
+        cts_w = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(CFG),
+                                     3 * COUNT * rank).reshape(COUNT, 3, -1)
+        w_a, w_b, w_c = (dev(cts_w[:, j].copy()) for j in range(3))
+        w_out = torch.zeros((COUNT, stride), dtype=torch.int32, device="cuda")
+        step_w = lambda: she.she_gate_batch_ops(ctx, d_ops, w_a, w_b, w_c, w_out, stream)
+        step_w()
+        w_ms, _ = timed(step_w, args.steps)
+        weak = {"value": round(world * COUNT * args.steps / (w_ms * 1e-3), 2), "unit": UNIT,
+                "gates_per_rank": COUNT, "ms_per_step": round(w_ms / args.steps, 3),
+                "note": "every rank evaluates its own 4096-gate batch (inputs encrypted at a "
+                        "rank-offset ordinal), no collective; value = all ranks' gates / "
+                        "max-over-ranks device time"}
+
+    # dominant kernel: the blind rotation (K2+K3), this rank's shard
     br_ms_per_launch = t["br_ms"] / max(1, t["br_launches"])
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
     common = {"kernel_ms_per_launch": round(br_ms_per_launch, 3),
               "kernel_share_of_step": round(t["br_ms"] / dev_ms, 4) if dev_ms else None,
-              "ks_kernel_ms_per_launch": round(t["ks_ms"] / max(1, t["ks_launches"]), 3)}
+              "ks_kernel_ms_per_launch": round(t["ks_ms"] / max(1, t["ks_launches"]), 3),
+              "lanes_per_launch": lanes_rank}
     if engine:  # FP64 FFT engine: bound by the FP64 pipe
-        fp64_ops = lanes * P.n * FP64_OPS_PER_CMUX
+        fp64_ops = lanes_rank * P.n * FP64_OPS_PER_CMUX
         achieved = fp64_ops / (br_ms_per_launch * 1e-3)
+        slots = sms * engine * (2 if engine == 2 else 1)  # fft2x2: 2 CTAs of 2 lanes per SM
+        rounds = -(-lanes_rank // slots)
         roof = {"bound": "fp64", "achieved": round(achieved / 1e12, 3),
                 "peak": round(fp64_peak / 1e12, 3), "unit": "T FP64-instr/s",
                 "frac": round(achieved / fp64_peak, 4), "traffic": read_profile_traffic("br_fft_kernel"),
                 "kernel": f"br_fft_kernel<{engine}> (gate prologue + blind rotation by exact FP64 "
                           "FFT + sample extract)",
-                "algorithmic_per_launch": f"{lanes} BR lanes x {P.n} CMux x {FP64_OPS_PER_CMUX} "
+                "algorithmic_per_launch": f"{lanes_rank} BR lanes x {P.n} CMux x {FP64_OPS_PER_CMUX} "
                                           "FP64 instr (DESIGN.md §4.2b)",
                 **common,
-                "peak_source": f"K7 measured {fp64_peak / 1e12:.2f} T DFMA/s on {torch.cuda.get_device_properties(local).multi_processor_count} SMs "
+                "wave_rounds": {"lanes": lanes_rank, "slots_per_round": slots, "rounds": rounds,
+                                "last_round_fill": round(lanes_rank / slots - (rounds - 1), 3)},
+                "peak_source": f"K7 measured {fp64_peak / 1e12:.2f} T DFMA/s on {sms} SMs "
                                "(nominal 64 FP64 lanes/SM/clk)",
-                "ntt_engine_equivalent": {"achieved_gmodmul_s": round(lanes * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3) / 1e9, 1),
+                "ntt_engine_equivalent": {"achieved_gmodmul_s": round(lanes_rank * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3) / 1e9, 1),
                                           "ntt_peak_gmodmul_s": round(peak / 1e9, 1)},
                 "ncu_profile": read_ncu_summary("br_fft_kernel")}
     else:
-        achieved = lanes * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3)
+        achieved = lanes_rank * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3)
         roof = {"bound": "alu", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
                 "unit": "Gmodmul/s", "frac": round(achieved / peak, 4), "traffic": read_profile_traffic(),
                 "kernel": "br_kernel (gate prologue + blind rotation + sample extract)",
-                "algorithmic_per_launch": f"{lanes} BR lanes x {MODMUL_PER_LANE[P.N]} modmul",
+                "algorithmic_per_launch": f"{lanes_rank} BR lanes x {MODMUL_PER_LANE[P.N]} modmul",
                 **common,
                 "peak_source": peak_src, "ncu_profile": read_ncu_summary()}
 
@@ -554,39 +598,57 @@ def run_she(args):
     for j in range(3):
         h_in[j][:] = cts[:, j]
     h_out = pin((COUNT, stride), torch.int32).view(np.uint32)
-    she.she_gate_batch_ops_host(ctx, h_ops, *h_in, h_out, stream)  # warm
+    if world == 1:  # the library's own host-buffer call
+        e2e_call = lambda: she.she_gate_batch_ops_host(ctx, h_ops, *h_in, h_out, stream)
+        h2d = COUNT + 3 * COUNT * stride * 4
+        api = "she_gate_batch_ops_host (libshe.so): H2D, gates, D2H, stream sync"
+    else:  # each rank copies its shard in, all-gather on the devices, full result out
+        stage = parallel.make_stage(COUNT, stride, world)
+        e2e_call = lambda: parallel.gate_batch_sharded_host(ctx, h_ops, *h_in, h_out, rank, world,
+                                                            stage)
+        h2d = (hi - lo) * (1 + 3 * stride * 4)
+        api = ("parallel.gate_batch_sharded_host: per-rank shard H2D, she_gate_batch_ops, "
+               f"{backend} all-gather, full result D2H")
+    e2e_call()  # warm
     e2e_s = []
-    if world > 1:
-        dist.barrier()
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        she.she_gate_batch_ops_host(ctx, h_ops, *h_in, h_out, stream)
+        e2e_call()
         e2e_s.append(time.perf_counter() - t0)
     e2e_total = max_over_ranks([sum(e2e_s)], world)[0]
-    # correctness spot check of the e2e output against the device path
-    assert np.array_equal(h_out, d_out.cpu().numpy().view(np.uint32)), "e2e output differs"
+    # correctness of this run: the e2e output equals the device path's, and
+    # every gate decrypts to its truth-table value
+    assert np.array_equal(h_out, gpu_out), "e2e output differs"
     dec = she.she_decrypt_bits(sk, h_out)
     want = np.array([si.truth(o, *b) for o, b in zip(ops, bits)])
     assert np.array_equal(dec, want), "decryption mismatch"
     decrypted = {"decrypted_compared": int(COUNT), "decrypted_mismatches": int(np.sum(dec != want))}
-    e2e = {"value": round(world * COUNT * args.steps / e2e_total, 2), "unit": UNIT,
-           "h2d_bytes_per_step": int(COUNT + 3 * COUNT * stride * 4),
-           "d2h_bytes_per_step": int(COUNT * stride * 4)}
+    e2e = {"value": round(COUNT * args.steps / e2e_total, 2), "unit": UNIT,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(COUNT * stride * 4),
+           "api": api}
 
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64" if engine else "u64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if engine else "u64",
             "data": "synthetic (seeded she_inputs; keys 1001, inputs 2001, ops 4001)",
-            "config": {"workload": WORKLOAD, "gates_per_rank": COUNT, "br_lanes_per_rank": lanes,
-                       "parallelism": f"gate-sharded x{world} (independent batches, no collective)",
+            "config": {"workload": WORKLOAD, "gates": COUNT, "br_lanes": lanes,
+                       "gates_per_rank": hi - lo, "br_lanes_per_rank": lanes_rank,
+                       "parallelism": (f"gate-sharded x{world}: {per} gates per rank, output LWEs "
+                                       f"all-gathered over {backend} inside the step"
+                                       if world > 1 else "1 GPU"),
                        "l2": "flushed between timed steps (256 MiB write), outside the event pairs"},
-            "br_lanes_per_s": round(world * lanes * args.steps / (dev_ms * 1e-3), 1),
+            "br_lanes_per_s": round(lanes * args.steps / (dev_ms * 1e-3), 1),
             "parity": decrypted,
             "roofline": roof, "clocks": clk, "e2e": e2e,
             "gpu_launches": int(t["br_launches"] + t["ks_launches"]),
             "k6_modmul_peak_per_s": round(k6, 1)}
+    if weak:
+        line["weak_scaled"] = weak
     if not args.no_net:
         line["net_latency"] = net_latency(ctx, sk, P, world, rank)
     if args.tcn:
@@ -707,6 +769,19 @@ def main():
                     help="gates per step (default: config 1's 4096; other values are A/B only)")
     args = ap.parse_args()
     set_count(args.count)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # no external launcher: run the N ranks ourselves (one process per GPU)
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={os.environ['WORLD_SIZE']} but --gpus {args.gpus}\n")
     if args.impl == "reference":
         run_reference(args)
     else:

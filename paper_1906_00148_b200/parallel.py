@@ -45,6 +45,49 @@ def gather_shards(buf, words: int, rank: int, world: int, group=None):
     return buf[:words]
 
 
+def gate_batch_sharded(ctx, ops, a, b, c, out, rank: int, world: int, stream=None, group=None):
+    """Config-1-style gate batch split across ranks (strong scaling, SURVEY.md
+    §8(e)): rank r evaluates gates [r*per, min(count, (r+1)*per)) of the batch
+    (per = ceil(count / world)) with she_gate_batch_ops and the output LWEs
+    are all-gathered into `out` (device, padded_words(count, world) rows;
+    rows [0, count) are the batch's outputs).  a, b, c, ops: the whole batch
+    (device; each rank reads only its shard).  Returns out[:count]."""
+    from . import she
+    count = a.shape[0]
+    lo, hi, _ = shard(count, rank, world)
+    if hi > lo:
+        she.she_gate_batch_ops(ctx, ops[lo:hi], a[lo:hi], b[lo:hi], c[lo:hi], out[lo:hi], stream)
+    return gather_shards(out, count, rank, world, group)
+
+
+def gate_batch_sharded_host(ctx, ops, a, b, c, out, rank: int, world: int, stage, group=None):
+    """The end-to-end multi-GPU call: HOST inputs (pinned numpy arrays of the
+    whole batch), each rank copies only its shard to the device, evaluates it,
+    the shards are all-gathered on the devices, and the full result is copied
+    back into the host array `out` (count x stride).  `stage` holds the
+    device buffers (dict from make_stage).  Synchronous."""
+    import torch
+    count = a.shape[0]
+    lo, hi, _ = shard(count, rank, world)
+    d_ops, d_in, d_out = stage["ops"], stage["in"], stage["out"]
+    d_ops[lo:hi].copy_(torch.from_numpy(ops[lo:hi]), non_blocking=True)
+    for j, h in enumerate((a, b, c)):
+        d_in[j][lo:hi].copy_(torch.from_numpy(h[lo:hi].view("int32")), non_blocking=True)
+    gate_batch_sharded(ctx, d_ops, d_in[0], d_in[1], d_in[2], d_out, rank, world, group=group)
+    torch.from_numpy(out.view("int32")).copy_(d_out[:count])
+    torch.cuda.synchronize()
+    return out
+
+
+def make_stage(count: int, stride: int, world: int, device="cuda"):
+    """Device buffers of gate_batch_sharded_host for a batch of `count` gates."""
+    import torch
+    rows = padded_words(count, world)
+    return {"ops": torch.zeros(count, dtype=torch.uint8, device=device),
+            "in": [torch.zeros((count, stride), dtype=torch.int32, device=device) for _ in range(3)],
+            "out": torch.zeros((rows, stride), dtype=torch.int32, device=device)}
+
+
 def max_over_ranks(values, world: int):
     """Element-wise max over ranks of a list of floats (device timings are
     reported as the max over ranks).  NCCL reduces on the GPU, gloo on the CPU."""

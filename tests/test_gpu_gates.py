@@ -368,8 +368,10 @@ def test_bad_arguments_raise(env1):
 @pytest.mark.parametrize("cfg", [0, 1])
 def test_gpu_client_matches_host_client(cuda, cfg):
     """Device encryption (masks drawn on the GPU from the shared counter-based
-    stream, host-drawn noise) is bit-identical to she_encrypt_bits; device
-    decryption equals the host decryption, including on bootstrapped outputs."""
+    stream, host-drawn noise) is bit-identical to the ORACLE's encryption
+    (oracle.encrypt from the oracle's own keygen of the same seed: an
+    independent implementation of R4) and to she_encrypt_bits; device
+    decryption equals the oracle's decryption and the host decryption."""
     P = si.CONFIG_PARAMS[cfg]
     sk, _ = she.she_keygen(P, si.key_seed(cfg))
     rng = np.random.default_rng(cfg + 50)
@@ -381,10 +383,14 @@ def test_gpu_client_matches_host_client(cuda, cfg):
     d_noise = torch.from_numpy(noise.view(np.int32)).cuda()
     d_ct = she.she_encrypt_bits_gpu(sk, d_bits, d_noise, 5151, 7)
     torch.cuda.synchronize()
+    K = oracle.keygen(P, si.key_seed(cfg))
+    ref = oracle.encrypt(P, K.s, bits, 5151, 7)
+    assert np.array_equal(host(d_ct), ref), "GPU encryption differs from oracle.encrypt"
     assert np.array_equal(host(d_ct), host_ct)
     back = she.she_decrypt_bits_gpu(sk, d_ct)
     torch.cuda.synchronize()
     assert np.array_equal(back.cpu().numpy(), bits)
+    assert np.array_equal(oracle.decrypt(P, K.s, host(d_ct)), bits)
     assert np.array_equal(she.she_decrypt_bits(sk, host_ct), bits)
 
 
