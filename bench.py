@@ -445,6 +445,10 @@ def engine_options(args) -> dict:
         opts["engine"] = args.engine
     if args.fft_lanes:
         opts["fft_lanes"] = args.fft_lanes
+    if args.fft_variant:
+        opts["fft_variant"] = args.fft_variant
+    if args.fft_groups:
+        opts["fft_groups"] = args.fft_groups
     return opts
 
 
@@ -765,6 +769,10 @@ def main():
                     help="blind-rotation engine (she_ctx_options; A/B measurements only)")
     ap.add_argument("--fft-lanes", type=int, default=0,
                     help="FFT engine lanes per CTA (she_ctx_options.fft_lanes)")
+    ap.add_argument("--fft-variant", type=int, default=0,
+                    help="FFT engine transform (she_ctx_options.fft_variant: 1 round-1, 2 v2)")
+    ap.add_argument("--fft-groups", type=int, default=0,
+                    help="FFT engine independent lane groups per CTA (she_ctx_options.fft_groups)")
     ap.add_argument("--count", type=int, default=COUNT,
                     help="gates per step (default: config 1's 4096; other values are A/B only)")
     args = ap.parse_args()

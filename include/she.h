@@ -144,7 +144,13 @@ typedef struct {
   int ntt_ctas;   /*   the instantiated shapes are 5x1, 4x1, 3x1, 2x2, 1x4      */
   int ks_kernel;  /* 0 = default (ks2_kernel for base 4, t = 8), 1 = the general
                      ks_kernel (any base-4 decomposition) */
-  int reserved[7];/* must be 0 */
+  int fft_variant;/* FFT engine transform: 0 = default (2), 1 = the round-1
+                     transform (16-entry twiddle tables, select-based pair
+                     exchange; 4 lanes per CTA only), 2 = v2 */
+  int fft_groups; /* FFT engine: independent lane groups per CTA, 0 = default
+                     (1); 2 = two groups of 2 lanes with their own pointwise
+                     step and barriers (4 lanes per CTA, variant 2) */
+  int reserved[5];/* must be 0 */
 } she_ctx_options;
 
 /* Create a context on CUDA `device`: uploads BK and KSK and transforms BK for
@@ -208,15 +214,17 @@ she_status she_field_selftest(int device, const uint64_t* a, const uint64_t* b, 
  * and transformed by the engine's setup kernel; forward FFT of the digit rows,
  * pointwise sum, inverse FFT, rounding, hi/lo recombination),
  * so that the exactness reading is pinned on the kernel that runs, not on a
- * model of it.  N = 1024 only.  HOST buffers:
+ * model of it.  variant: the transform (she_ctx_options.fft_variant; 0 =
+ * the default).  N = 1024 only.  HOST buffers:
  *   digits int32[count][4][1024]      digit rows r = c*l + j, |d| <= 2^11
  *   bk     uint32[count][4][2][1024]  torus32 BK rows (r, output o)
  *   out    uint32[count][2][1024]     out[c][o] = sum_r digits[c][r] * bk[c][r][o]
  *                                     mod (X^1024 + 1), mod 2^32
  * *worst_distance (may be NULL) = max over all cases of |v - rint(v)| for every
  * value before rounding (exactness needs < 1/2).  count <= 65535. */
-she_status she_fft_product_selftest(int device, const int32_t* digits, const uint32_t* bk,
-                                    size_t count, uint32_t* out, double* worst_distance);
+she_status she_fft_product_selftest(int device, int variant, const int32_t* digits,
+                                    const uint32_t* bk, size_t count, uint32_t* out,
+                                    double* worst_distance);
 
 /* Bootstrapped gates, all with the same op (north_star signature).  a, b, c,
  * out: device, count slots each (c read only for MUX, b not read for

@@ -305,13 +305,50 @@ struct FLane {
   __device__ double2* row(int r) const { return rows + (size_t)r * fft::kRow; }
 };
 
-constexpr size_t kFftTables = 2 * 512 * sizeof(double2);  // pass-A twiddles, fwd + inv
+// FFT variants of the FP64 engine (she_ctx_options.fft_variant): 1 = the
+// round-1 transform (16-entry pass-A twiddle tables, select-based pair
+// exchange), 2 = fft_core.cuh's v2 (9-entry tables, select-free exchange with
+// its scaling folded into the BK setup and the untwist).  Same products.
+template <int V>
+struct FftVar;
+template <>
+struct FftVar<1> {
+  static constexpr int kTab = 512;  // table entries per direction
+  __device__ static void tables(int t, int n, double2* f, double2* i) { fft::make_tables(t, n, f, i); }
+  __device__ static void forward(const double (&re)[16], const double (&im)[16], int lane,
+                                 const double2* tw, double2* row) {
+    fft::forward(re, im, lane, tw, row);
+  }
+  __device__ static void inverse(const double2* in, int lane, const double2* tw, double2* row,
+                                 double2 (&x)[8], double2 (&y)[8]) {
+    fft::inverse(in, lane, tw, row, x, y);
+  }
+  __device__ static double2 bk_correction(int) { return make_double2(1.0, 0.0); }
+};
+template <>
+struct FftVar<2> {
+  static constexpr int kTab = fft::kTw2 * 32;
+  __device__ static void tables(int t, int n, double2* f, double2* i) { fft::make_tables2(t, n, f, i); }
+  __device__ static void forward(const double (&re)[16], const double (&im)[16], int lane,
+                                 const double2* tw, double2* row) {
+    fft::forward_v2(re, im, lane, tw, row);
+  }
+  __device__ static void inverse(const double2* in, int lane, const double2* tw, double2* row,
+                                 double2 (&x)[8], double2 (&y)[8]) {
+    fft::inverse_v2(in, lane, tw, row, x, y);
+  }
+  __device__ static double2 bk_correction(int k) { return fft::v2_bk_correction(k); }
+};
+constexpr int kFftDefaultVariant = 2;
+template <int V>
+constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double2); }
 
 // The CMux product steps of the FP64 engine, shared by br_fft_kernel and the
 // device product self-test (she_fft_product_selftest) so that the test runs
 // exactly the arithmetic the blind rotation runs.
 //
 // Forward FFT of one digit row (32 digits per thread: coefficient lane + 32 m).
+template <int V>
 __device__ __forceinline__ void fbr_forward_digits(const int32_t (&d)[32], int lane,
                                                    const double2* tw_fwd, double2* row) {
   double re[16], im[16];
@@ -320,7 +357,7 @@ __device__ __forceinline__ void fbr_forward_digits(const int32_t (&d)[32], int l
     re[m] = fft::i2d(d[m]);
     im[m] = fft::i2d(d[m + 16]);
   }
-  fft::forward(re, im, lane, tw_fwd, row);
+  FftVar<V>::forward(re, im, lane, tw_fwd, row);
 }
 
 // Pointwise sum at frequency k of one lane: rows r = 0..3 hold the digit
@@ -346,13 +383,13 @@ __device__ __forceinline__ void fbr_pointwise(double2* row0, int k, const double
 // Inverse FFT of product row w = (o, half), rounded to the exact integer and
 // added into ACC_o (hi half shifted by 16; torus32 wrap).  TRACK: also the
 // largest distance of a pre-rounding value to its integer (self-test only).
-template <bool TRACK>
+template <int V, bool TRACK>
 __device__ __forceinline__ void fbr_inverse_acc(double2* row, int lane, const double2* tw_inv,
                                                 uint32_t* acc_o, int w,
                                                 unsigned long long* worst) {
   constexpr int M = fft::kM;
   double2 x[8], y[8];
-  fft::inverse(row, lane, tw_inv, row, x, y);
+  FftVar<V>::inverse(row, lane, tw_inv, row, x, y);
   const int sh = (w & 1) ? 0 : 16;
   const int k2 = lane >> 1, hh = lane & 1;
   double dmax = 0.0;
@@ -387,28 +424,48 @@ struct BRFArgs {
   br::Geometry geo;
 };
 
-template <int G, int B = 1>
+// Named barrier over the `count` threads of a lane group (ids 1 + group).
+__device__ __forceinline__ void group_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void group_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// GRP > 1: the CTA's G lanes form GRP independent groups of G / GRP lanes,
+// each with its own pointwise step (BK_i read once per group) and its own
+// named barriers, so that the groups drift apart in phase and one group's
+// FP64-bound transforms overlap another's shared-memory-bound steps; the
+// second group starts one forward transform behind the first.
+template <int G, int B = 1, int V = kFftDefaultVariant, int GRP = 1>
 __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
   using S = ntt::Shape<1024>;
   constexpr int N = fft::kN, M = fft::kM, T = 128 * G;
+  constexpr int LPG = G / GRP, TG = 128 * LPG;  // lanes and threads per group
+  static_assert(G % GRP == 0, "groups of equal size");
   extern __shared__ __align__(16) uint8_t smem[];
   const GateSrc& src = args.src;
   const br::Geometry& geo = args.geo;
   const uint32_t n = geo.n;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = warp >> 2, w = warp & 3, lt = tid & 127;
+  const int grp = g / LPG, gl = g % LPG, gt = tid - grp * TG;  // group, lane in group, thread in group
+  const int gbar = 1 + grp;                                      // the group's named barrier
   const size_t lane_bytes = FLane::bytes(n);
   FLane me(smem + (size_t)g * lane_bytes);
   const uint32_t total = *args.nlanes;
   double2* tw_fwd = reinterpret_cast<double2*>(smem + (size_t)G * lane_bytes);
-  double2* tw_inv = tw_fwd + 512;
-  fft::make_tables(tid, T, tw_fwd, tw_inv);
+  double2* tw_inv = tw_fwd + FftVar<V>::kTab;
+  FftVar<V>::tables(tid, T, tw_fwd, tw_inv);
   __syncthreads();
 
   const uint32_t first = (uint32_t)(((uint64_t)blockIdx.x * total) / gridDim.x);
   const uint32_t last = (uint32_t)(((uint64_t)(blockIdx.x + 1) * total) / gridDim.x);
-  for (uint32_t base = first; base < last; base += G) {
-    const uint32_t L_id = base + g;
+  // phase offset between the groups (only when every group has a lane)
+  bool stagger = GRP > 1 && last - first > (uint32_t)(G - LPG);
+  // group grp serves lanes first + grp * LPG + gl, + G, + 2G, ...
+  for (uint32_t base = first + grp * LPG; base < last; base += G) {
+    const uint32_t L_id = base + gl;
     const bool on = L_id < last;
     uint32_t gate = 0, h = 0;
     if (on) {
@@ -426,7 +483,7 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
         me.abar[k] = (uint16_t)br::modswitch(v, geo.lg2N);
       }
     }
-    __syncthreads();
+    group_sync(gbar, TG);
     if (on) {
       const uint32_t bbar = me.abar[n];
       for (int m = lt; m < N; m += 128) {
@@ -434,42 +491,48 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
         me.acc[N + m] = br::testvec_coeff(m, bbar, N);
       }
     }
-    __syncthreads();
+    group_sync(gbar, TG);
 
     for (uint32_t i = 0; i < n; ++i) {
+      if (stagger && grp == 1) group_sync(15, TG * 2);  // start one forward behind group 0
       if (on) {  // forward FFT of digit row w
         int32_t d[32];
         br::load_digits<S>(geo, w, lane, me.acc, me.abar[i], d);
-        fbr_forward_digits(d, lane, tw_fwd, me.row(w));
+        fbr_forward_digits<V>(d, lane, tw_fwd, me.row(w));
       }
-      // BK_i planes of this thread's first frequency (k = tid) are requested
+      if (stagger) {
+        if (grp == 0) group_arrive(15, TG * 2);
+        stagger = false;
+      }
+      // BK_i planes of this thread's first frequency (k = gt) are requested
       // before the barrier, so their L2 latency overlaps the wait for the
       // slowest warp's forward transform
       const double2* bki = args.bkf + (size_t)i * 16 * M;
       double2 bpre[16];
-      if (tid < M) {
+      if (gt < M) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) bpre[q] = __ldg(bki + (size_t)q * M + tid);
+        for (int q = 0; q < 16; ++q) bpre[q] = __ldg(bki + (size_t)q * M + gt);
       }
-      __syncthreads();
-      {  // pointwise: frequency k, all lanes of the CTA, BK_i planes read once
+      group_sync(gbar, TG);
+      {  // pointwise: frequency k, all lanes of the group, BK_i planes read once
         auto pointwise = [&](int k, const double2 (&b)[16]) {
 #pragma unroll
-          for (int gg = 0; gg < G; ++gg)
-            if (base + gg < last) fbr_pointwise(FLane(smem + (size_t)gg * lane_bytes).row(0), k, b);
+          for (int gg = 0; gg < LPG; ++gg)
+            if (base + gg < last)
+              fbr_pointwise(FLane(smem + (size_t)(grp * LPG + gg) * lane_bytes).row(0), k, b);
         };
-        if (tid < M) pointwise(tid, bpre);
-        for (int k = tid + T; k < M; k += T) {
+        if (gt < M) pointwise(gt, bpre);
+        for (int k = gt + TG; k < M; k += TG) {
           double2 b[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) b[q] = __ldg(bki + (size_t)q * M + k);
           pointwise(k, b);
         }
       }
-      __syncthreads();
+      group_sync(gbar, TG);
       if (on) {  // inverse of output (o, half) = (w >> 1, w & 1), added into ACC_o
-        fbr_inverse_acc<false>(me.row(w), lane, tw_inv, me.acc + (w >> 1) * N, w, nullptr);
-        lane_sync(1 + g);
+        fbr_inverse_acc<V, false>(me.row(w), lane, tw_inv, me.acc + (w >> 1) * N, w, nullptr);
+        lane_sync(1 + GRP + g);
       }
     }
 
@@ -483,19 +546,20 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
         e[m] = v;
       }
     }
-    __syncthreads();
+    group_sync(gbar, TG);
   }
 }
 
 // K1 for the FP64 engine: BK poly (i, w, o) -> two planes (halves), forward
 // FFT, 1/512 folded.  One warp per (poly, half).
+template <int V>
 __global__ void bk_fft_kernel(const uint32_t* bk, double2* out, uint32_t polys) {
   __shared__ double2 row[fft::kRow];
-  __shared__ double2 tw[2 * 512];
+  __shared__ double2 tw[2 * FftVar<V>::kTab];
   const uint32_t item = blockIdx.x, poly = item >> 1, half = item & 1;
   if (poly >= polys) return;
   const int lane = threadIdx.x;
-  fft::make_tables(lane, 32, tw, tw + 512);
+  FftVar<V>::tables(lane, 32, tw, tw + FftVar<V>::kTab);
   __syncwarp();
   const uint32_t* b = bk + (size_t)poly * fft::kN;
   double re[16], im[16];
@@ -506,13 +570,14 @@ __global__ void bk_fft_kernel(const uint32_t* bk, double2* out, uint32_t polys) 
     re[m] = half ? (double)l0 : (double)((v0 - l0) >> 16);
     im[m] = half ? (double)l1 : (double)((v1 - l1) >> 16);
   }
-  fft::forward(re, im, lane, tw, row);
+  FftVar<V>::forward(re, im, lane, tw, row);
   __syncwarp();
-  // storage: [i][plane][512], plane = (w * 2 + o) * 2 + half, poly = i * 8 + w * 2 + o
+  // storage: [i][plane][512], plane = (w * 2 + o) * 2 + half, poly = i * 8 + w * 2 + o;
+  // position p holds frequency k with fpos(k) = p (fpos is an involution)
   const uint32_t i = poly >> 3, wo = poly & 7;
   double2* o = out + ((size_t)i * 16 + wo * 2 + half) * fft::kM;
   for (int k = lane; k < fft::kM; k += 32) {
-    const double2 v = row[k];
+    const double2 v = fft::cmul(row[k], FftVar<V>::bk_correction(fft::fpos(k)));
     o[k] = make_double2(v.x * (1.0 / 512), v.y * (1.0 / 512));
   }
 }
@@ -523,6 +588,7 @@ __global__ void bk_fft_kernel(const uint32_t* bk, double2* out, uint32_t polys) 
 // FFT-domain BK made by bk_fft_kernel, fbr_inverse_acc), one CTA of 4 warps per
 // case (warp w = digit row w, then output row w), and the largest distance of
 // a pre-rounding value to its integer.
+template <int V>
 __global__ void __launch_bounds__(128) fft_selftest_kernel(const int32_t* digits,
                                                            const double2* bkf, uint32_t* out,
                                                            unsigned long long* worst) {
@@ -530,10 +596,10 @@ __global__ void __launch_bounds__(128) fft_selftest_kernel(const int32_t* digits
   extern __shared__ __align__(16) uint8_t smem[];  // kFftSelftestSmem bytes
   double2* rows = reinterpret_cast<double2*>(smem);
   double2* tw = rows + 4 * fft::kRow;
-  uint32_t* acc = reinterpret_cast<uint32_t*>(tw + 2 * 512);
+  uint32_t* acc = reinterpret_cast<uint32_t*>(tw + 2 * 512);  // room for either variant
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const size_t c = blockIdx.x;
-  fft::make_tables(tid, 128, tw, tw + 512);
+  FftVar<V>::tables(tid, 128, tw, tw + FftVar<V>::kTab);
   for (int m = tid; m < 2 * N; m += 128) acc[m] = 0;
   __syncthreads();
   {
@@ -541,7 +607,7 @@ __global__ void __launch_bounds__(128) fft_selftest_kernel(const int32_t* digits
     int32_t dd[32];
 #pragma unroll
     for (int j2 = 0; j2 < 32; ++j2) dd[j2] = d[lane + 32 * j2];
-    fbr_forward_digits(dd, lane, tw, rows + w * fft::kRow);
+    fbr_forward_digits<V>(dd, lane, tw, rows + w * fft::kRow);
   }
   __syncthreads();
   const double2* bki = bkf + c * 16 * M;
@@ -552,7 +618,8 @@ __global__ void __launch_bounds__(128) fft_selftest_kernel(const int32_t* digits
     fbr_pointwise(rows, k, b);
   }
   __syncthreads();
-  fbr_inverse_acc<true>(rows + w * fft::kRow, lane, tw + 512, acc + (w >> 1) * N, w, worst);
+  fbr_inverse_acc<V, true>(rows + w * fft::kRow, lane, tw + FftVar<V>::kTab, acc + (w >> 1) * N, w,
+                           worst);
   __syncthreads();
   for (int m = tid; m < 2 * N; m += 128) out[c * 2 * N + m] = acc[m];
 }
@@ -957,6 +1024,8 @@ struct she_ctx {
   // FP64 FFT engine (br_fft_kernel, N = 1024): G lanes per CTA, 0 = NTT engine
   // (SHE_BR_ENGINE=fft | fft3 | fft4 | ntt)
   int fft_g = 4;
+  int fft_v = kFftDefaultVariant;  // FFT variant (FftVar): 1 = round-1 transform, 2 = v2
+  int fft_grp = 1;                 // independent lane groups per CTA (br_fft_kernel GRP)
   double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
   // staging for the host-buffer API
@@ -1040,17 +1109,25 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
   if (ctx->fft_g && S::N == fft::kN) {  // FFT engine: BK halves in the FFT domain
     ctx->bk_bytes = (size_t)p.n * 16 * fft::kM * sizeof(double2);
     CK(cudaMalloc(&ctx->bkf, ctx->bk_bytes));
-    bk_fft_kernel<<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkf, (uint32_t)polys);
+    if (ctx->fft_v == 1)
+      bk_fft_kernel<1><<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkf, (uint32_t)polys);
+    else
+      bk_fft_kernel<2><<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkf, (uint32_t)polys);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
-    CK(cudaFuncSetAttribute(br_fft_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(3 * FLane::bytes(p.n) + kFftTables)));
-    CK(cudaFuncSetAttribute(br_fft_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(4 * FLane::bytes(p.n) + kFftTables)));
-    CK(cudaFuncSetAttribute(br_fft_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(5 * FLane::bytes(p.n) + kFftTables)));
-    CK(cudaFuncSetAttribute(br_fft_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(2 * FLane::bytes(p.n) + kFftTables)));
+    const size_t lb = FLane::bytes(p.n);
+    CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(4 * lb + fft_tables_bytes<1>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<3, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(3 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(4 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<5, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(5 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<2, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(2 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(4 * lb + fft_tables_bytes<2>())));
   }
   cudaFree(d_bk32);
 #define SHE_BR_SMEM(G, B)                                                            \
@@ -1118,7 +1195,7 @@ she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream
   return SHE_OK;
 }
 
-template <int G, int B = 1>
+template <int G, int B, int V, int GRP = 1>
 she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
   BRFArgs f;
   f.src = a.src;
@@ -1131,7 +1208,7 @@ she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaSt
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms * B)));
   cfg.blockDim = dim3(128 * G);
-  cfg.dynamicSmemBytes = G * FLane::bytes(ctx->p.n) + kFftTables;
+  cfg.dynamicSmemBytes = G * FLane::bytes(ctx->p.n) + fft_tables_bytes<V>();
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   if (ctx->persist) {
@@ -1144,7 +1221,7 @@ she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  CK(cudaLaunchKernelEx(&cfg, br_fft_kernel<G, B>, f));
+  CK(cudaLaunchKernelEx(&cfg, br_fft_kernel<G, B, V, GRP>, f));
   return SHE_OK;
 }
 
@@ -1183,10 +1260,12 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     if (ctx->timing) mark(ctx, stream);
     st = fail(SHE_ERR_STATE, "no blind-rotation kernel for config %dx%d", ctx->br_g, ctx->br_b);
     if (ctx->bkf && S::N == fft::kN) {
-      st = ctx->fft_g == 3   ? launch_br_fft<3>(ctx, a, 2 * cnt, stream)
-           : ctx->fft_g == 5 ? launch_br_fft<5>(ctx, a, 2 * cnt, stream)
-           : ctx->fft_g == 2 ? launch_br_fft<2, 2>(ctx, a, 2 * cnt, stream)
-                             : launch_br_fft<4>(ctx, a, 2 * cnt, stream);
+      st = ctx->fft_v == 1   ? launch_br_fft<4, 1, 1>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_grp == 2 ? launch_br_fft<4, 1, 2, 2>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_g == 3 ? launch_br_fft<3, 1, 2>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_g == 5 ? launch_br_fft<5, 1, 2>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_g == 2 ? launch_br_fft<2, 2, 2>(ctx, a, 2 * cnt, stream)
+                             : launch_br_fft<4, 1, 2>(ctx, a, 2 * cnt, stream);
     } else {
 #define SHE_BR_LAUNCH(G, B) \
     if (ctx->br_g == G && ctx->br_b == B) st = launch_br<S, G, B>(ctx, a, 2 * cnt, stream);
@@ -1263,6 +1342,14 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   if ((o.ntt_lanes || o.ntt_ctas) && use_fft)
     return fail(SHE_ERR_ARG, "ntt_lanes/ntt_ctas given for the FFT engine");
   if (o.ks_kernel < 0 || o.ks_kernel > 1) return fail(SHE_ERR_ARG, "ks_kernel=%d", o.ks_kernel);
+  if (o.fft_variant < 0 || o.fft_variant > 2)
+    return fail(SHE_ERR_ARG, "fft_variant=%d: expected 0, 1 or 2", o.fft_variant);
+  if (o.fft_variant && !use_fft) return fail(SHE_ERR_ARG, "fft_variant given for the NTT engine");
+  if (o.fft_variant == 1 && o.fft_lanes && o.fft_lanes != 4)
+    return fail(SHE_ERR_ARG, "fft_variant 1 is instantiated for 4 lanes per CTA only");
+  if (o.fft_groups < 0 || o.fft_groups > 2) return fail(SHE_ERR_ARG, "fft_groups=%d", o.fft_groups);
+  if (o.fft_groups == 2 && ((o.fft_lanes && o.fft_lanes != 4) || o.fft_variant == 1 || !use_fft))
+    return fail(SHE_ERR_ARG, "fft_groups = 2 is instantiated for 4 lanes per CTA, variant 2");
   CK(cudaSetDevice(device));
   she_ctx* ctx = new (std::nothrow) she_ctx;
   if (!ctx) return fail(SHE_ERR_OOM, "host allocation failed");
@@ -1279,6 +1366,8 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     ctx->br_b = o.ntt_ctas;
   }
   ctx->fft_g = use_fft ? (o.fft_lanes ? o.fft_lanes : 4) : 0;
+  ctx->fft_v = o.fft_variant ? o.fft_variant : kFftDefaultVariant;
+  ctx->fft_grp = o.fft_groups ? o.fft_groups : 1;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
     she_ctx_destroy(ctx);
@@ -1527,10 +1616,13 @@ she_status she_field_selftest(int device, const uint64_t* a, const uint64_t* b, 
   return st;
 }
 
-she_status she_fft_product_selftest(int device, const int32_t* digits, const uint32_t* bk,
-                                    size_t count, uint32_t* out, double* worst_distance) {
+she_status she_fft_product_selftest(int device, int variant, const int32_t* digits,
+                                    const uint32_t* bk, size_t count, uint32_t* out,
+                                    double* worst_distance) {
   if (count == 0) return SHE_OK;
   if (!digits || !bk || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  if (variant < 0 || variant > 2) return fail(SHE_ERR_ARG, "variant=%d", variant);
+  const int V = variant ? variant : kFftDefaultVariant;
   if (count > 65535) return fail(SHE_ERR_ARG, "count > 65535");
   constexpr size_t N = fft::kN;
   CK(cudaSetDevice(device));
@@ -1548,15 +1640,17 @@ she_status she_fft_product_selftest(int device, const int32_t* digits, const uin
   if (e == cudaSuccess) e = cudaMemcpy(dd, digits, count * 4 * N * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(db, bk, count * 8 * N * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {  // the setup transform of the engine (BK -> FFT domain, halves)
-    bk_fft_kernel<<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
+    if (V == 1) bk_fft_kernel<1><<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
+    else bk_fft_kernel<2><<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
     e = cudaGetLastError();
   }
   constexpr size_t smem = (4 * fft::kRow + 2 * 512) * sizeof(double2) + 2 * N * 4;
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(fft_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+    e = cudaFuncSetAttribute(V == 1 ? fft_selftest_kernel<1> : fft_selftest_kernel<2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) {
-    fft_selftest_kernel<<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
+    if (V == 1) fft_selftest_kernel<1><<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
+    else fft_selftest_kernel<2><<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpy(out, dout, count * 2 * N * 4, cudaMemcpyDeviceToHost);

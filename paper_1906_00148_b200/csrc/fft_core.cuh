@@ -317,4 +317,124 @@ __device__ __forceinline__ void make_tables(int t, int nthreads, double2* fwd, d
   }
 }
 
+// ---------------------------------------------------------------------------
+// Variant 2: the same two-pass 512-point DFT with
+//  (a) pass-A twiddles from a 9-entry-per-lane table, t(k2) for k2 < 8 and the
+//      ratio r8 = t(k2 + 8) / t(k2), so 9 shared loads instead of 16 per
+//      transform (8 extra complex products);
+//  (b) a select-free pair exchange: lanes n1 = 3 (mod 4) carry a factor -1
+//      (folded into t), so the odd thread h = 1 of a column computes
+//      Y[k] = E1[k ^ 8] and both threads keep a[brev(j)] and send
+//      a[brev(8 + j)]; both then form keep +- c r with c = w^j (h = 0) or
+//      1 / w'^(8+j) (h = 1): thread 1's outputs come out scaled by
+//      sigma = 1 / w32^(8+j) (x) and -1 / w32^(8+j) (y).  The forward's
+//      scaling is undone in the BK setup (BK spectra multiplied by sigma^-2,
+//      so that D' B'' = sigma D B / sigma = D B); the inverse's is folded into
+//      its untwist constants.  Verified against the exact product on the
+//      device (she_fft_product_selftest) and in tests/test_fft_exactness.py.
+// ---------------------------------------------------------------------------
+constexpr int kTw2 = 9;  // table entries per lane and direction
+
+// v2 tables [9][32] (k2 or 8 = ratio, lane), s(n1) = -1 for n1 = 3 (mod 4):
+//   forward  t(k2) = s zeta^lane w512^(lane k2),  ratio w512^(8 lane)
+//   inverse  t(k2) = s w512^(-lane k2) zeta^(-k2), ratio exp(-i pi 8 (4 lane + 1) / 1024)
+__device__ __forceinline__ void make_tables2(int t, int nthreads, double2* fwd, double2* inv) {
+  for (int e = t; e < kTw2 * 32; e += nthreads) {
+    const int k2 = e >> 5, lane = e & 31;
+    const double sg = (lane & 3) == 3 ? -1.0 : 1.0;
+    double s, c;
+    if (k2 < 8) {
+      sincospi(lane * (1 + 4 * k2) / 1024.0, &s, &c);
+      fwd[e] = make_double2(sg * c, sg * s);
+      sincospi(-k2 * (4 * lane + 1) / 1024.0, &s, &c);
+      inv[e] = make_double2(sg * c, sg * s);
+    } else {
+      sincospi(lane / 32.0, &s, &c);
+      fwd[e] = make_double2(c, s);
+      sincospi(-8 * (4 * lane + 1) / 1024.0, &s, &c);
+      inv[e] = make_double2(c, s);
+    }
+  }
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft512_v2(double2 (&a)[16], int lane, const double2* tw,
+                                          double2* scratch, double2 (&x)[8], double2 (&y)[8]) {
+  dft16<SIGN>(a);
+  const double2 r8 = tw[8 * 32 + lane];
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2) {
+    const double2 p = tw[k2 * 32 + lane];
+    scratch[tslot(lane, k2)] = cmul(a[brev4(k2)], p);
+    scratch[tslot(lane, k2 + 8)] = cmul(a[brev4(k2 + 8)], cmul(p, r8));
+  }
+  __syncwarp();
+  const int k2 = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = scratch[tslot(2 * m + h, k2)];
+  dft16<SIGN>(a);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double2 keep = a[brev4(j)], send = a[brev4(8 + j)];
+    double2 r;
+    r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+    r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+    // c0 = w32^(SIGN j), c1 = w32^(-SIGN (8 + j)): compile-time constants
+    const double2 c0 = c_w128[(SIGN * 4 * j) & 127];
+    const double2 c1 = c_w128[(-SIGN * 4 * (8 + j)) & 127];
+    double2 c;
+    c.x = h ? c1.x : c0.x;
+    c.y = h ? c1.y : c0.y;
+    const double2 t = cmul(r, c);
+    x[j] = cadd(keep, t);
+    y[j] = csub(keep, t);
+  }
+  __syncwarp();  // scratch reads done before the caller reuses the row
+}
+
+// Forward v2: as forward(); the spectrum at k = k2 + 16 k1 is scaled by
+// sigma(k) = w32^(-k1) for k1 & 8, 1 otherwise (see above).
+__device__ __forceinline__ void forward_v2(const double (&re)[16], const double (&im)[16], int lane,
+                                           const double2* tw_fwd, double2* row) {
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = rot<1>(make_double2(re[m], im[m]), 2 * m);  // w64^m
+  double2 x[8], y[8];
+  dft512_v2<1>(a, lane, tw_fwd, row, x, y);
+  const int k2 = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    row[fpos(k2 + 16 * (8 * h + j))] = x[j];
+    row[fpos(k2 + 16 * (16 + 8 * h + j))] = y[j];
+  }
+}
+
+// Inverse v2 of the TRUE spectrum X[k] = row[fpos(k)]: outputs as inverse();
+// the untwist constants absorb thread 1's exchange scaling:
+//   h = 0: x * conj(W128[j]),        y * conj(W128[16 + j])
+//   h = 1: x * conj(W128[40 + 5 j]), y * conj(W128[(5 j - 8) & 127])
+__device__ __forceinline__ void inverse_v2(const double2* row_in, int lane, const double2* tw_inv,
+                                           double2* row, double2 (&x)[8], double2 (&y)[8]) {
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = row_in[fpos(lane + 32 * m)];
+  __syncwarp();
+  dft512_v2<-1>(a, lane, tw_inv, row, x, y);
+  const int h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    x[j] = cmulc(x[j], c_w128[h ? 40 + 5 * j : j]);
+    y[j] = cmulc(y[j], c_w128[h ? (5 * j - 8) & 127 : 16 + j]);
+  }
+}
+
+// sigma(k)^-2 of the v2 forward (BK setup): w16^(k1) for k1 & 8, 1 otherwise.
+__device__ __forceinline__ double2 v2_bk_correction(int k) {
+  const int k1 = k >> 4;
+  if (!(k1 & 8)) return make_double2(1.0, 0.0);
+  double s, c;
+  sincospi(k1 / 8.0, &s, &c);
+  return make_double2(c, s);
+}
+
 }  // namespace fft

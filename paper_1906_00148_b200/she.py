@@ -45,14 +45,16 @@ class she_ctx_options(ctypes.Structure):
     """include/she.h she_ctx_options: engine selection (all engines are exact)."""
     _fields_ = [("br_engine", ctypes.c_int), ("fft_lanes", ctypes.c_int),
                 ("ntt_lanes", ctypes.c_int), ("ntt_ctas", ctypes.c_int),
-                ("ks_kernel", ctypes.c_int), ("reserved", ctypes.c_int * 7)]
+                ("ks_kernel", ctypes.c_int), ("fft_variant", ctypes.c_int),
+                ("fft_groups", ctypes.c_int), ("reserved", ctypes.c_int * 5)]
 
     ENGINES = {"default": 0, "fft": 1, "ntt": 2}
 
     @classmethod
-    def of(cls, engine="default", fft_lanes=0, ntt_shape=(0, 0), ks_kernel="default"):
+    def of(cls, engine="default", fft_lanes=0, ntt_shape=(0, 0), ks_kernel="default",
+           fft_variant=0, fft_groups=0):
         return cls(cls.ENGINES[engine], fft_lanes, ntt_shape[0], ntt_shape[1],
-                   {"default": 0, "general": 1}[ks_kernel])
+                   {"default": 0, "general": 1}[ks_kernel], fft_variant, fft_groups)
 
 
 class she_circuit_stats(ctypes.Structure):
@@ -135,7 +137,7 @@ def lib() -> ctypes.CDLL:
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_field_selftest": ([ctypes.c_int, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
-            "she_fft_product_selftest": ([ctypes.c_int, _vp, _vp, _sz, _vp,
+            "she_fft_product_selftest": ([ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp,
                                           ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
             "she_encrypt_noise": ([_vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
             "she_encrypt_bits_gpu": ([_vp, _vp, _vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp,
@@ -628,7 +630,7 @@ def field_selftest(device: int, a, b, c) -> np.ndarray:
     return out
 
 
-def fft_product_selftest(device: int, digits, bk):
+def fft_product_selftest(device: int, digits, bk, variant: int = 0):
     """FP64-engine CMux product on given inputs (test instrumentation, she.h):
     digits int32 [count][4][1024], bk uint32 [count][4][2][1024] ->
     (out uint32 [count][2][1024], worst distance to an integer)."""
@@ -638,7 +640,7 @@ def fft_product_selftest(device: int, digits, bk):
     assert digits.shape == (count, 4, 1024) and bk.shape == (count, 4, 2, 1024)
     out = np.zeros((count, 2, 1024), dtype=np.uint32)
     worst = ctypes.c_double(0.0)
-    _check(lib().she_fft_product_selftest(device, _np_ptr(digits), _np_ptr(bk), count,
+    _check(lib().she_fft_product_selftest(device, variant, _np_ptr(digits), _np_ptr(bk), count,
                                           _np_ptr(out), ctypes.byref(worst)))
     return out, worst.value
 

@@ -86,14 +86,16 @@ def cases():
     return out
 
 
-def test_fft_product_selftest_matches_schoolbook_on_extreme_inputs(cuda):
+@pytest.mark.parametrize("variant", [2, 1], ids=["v2-default", "v1-round1"])
+def test_fft_product_selftest_matches_schoolbook_on_extreme_inputs(cuda, variant):
     cs = cases()
     digits = np.stack([d for _, d, _ in cs])
     bk = np.stack([b for _, _, b in cs])
-    got, worst = she.fft_product_selftest(0, digits, bk)
+    got, worst = she.fft_product_selftest(0, digits, bk, variant)
     bad = [name for (name, d, b), g in zip(cs, got) if not np.array_equal(g, expected(d, b))]
     assert not bad, f"device FFT product differs from the schoolbook product: {bad}"
-    print(f"\nworst distance to an integer before rounding: {worst:.3e} over {len(cs)} cases")
+    print(f"\nvariant {variant}: worst distance to an integer before rounding: {worst:.3e} "
+          f"over {len(cs)} cases")
     assert worst < 0.5
     # the reading's margin: worst-case bound ~1.1e-3, i.e.
     # more than 100x below 1/2
@@ -101,5 +103,5 @@ def test_fft_product_selftest_matches_schoolbook_on_extreme_inputs(cuda):
 
 
 def test_fft_product_selftest_rejects_bad_arguments(cuda):
-    assert she.lib().she_fft_product_selftest(0, None, None, 1, None, None) == -1  # SHE_ERR_ARG
-    assert she.lib().she_fft_product_selftest(0, None, None, 0, None, None) == 0   # count 0: no-op
+    assert she.lib().she_fft_product_selftest(0, 0, None, None, 1, None, None) == -1  # SHE_ERR_ARG
+    assert she.lib().she_fft_product_selftest(0, 0, None, None, 0, None, None) == 0   # count 0: no-op

@@ -286,10 +286,11 @@ def test_config1_full_parity_vs_oracle_digests(env1, config1_outputs):
 
 
 ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3),
-               "fft2x2": dict(engine="fft", fft_lanes=2)}
+               "fft2x2": dict(engine="fft", fft_lanes=2), "fft-v1": dict(engine="fft", fft_variant=1),
+               "fft-2groups": dict(engine="fft", fft_groups=2)}
 
 
-@pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2"])
+@pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2", "fft-v1", "fft-2groups"])
 def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with 4 lanes per
     CTA; the Goldilocks NTT engine (she_ctx_options.br_engine = 2) and the other
@@ -299,7 +300,8 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
     assert she.br_engine(env0_ctx()) == 0  # N = 256 has no FFT engine
     P = env1.P
     ctx = she.Context(P, env1.ck, device=0, **ENGINE_OPTS[engine])
-    assert she.br_engine(ctx) == {"ntt": 0, "fft3": 3, "fft2x2": 2}[engine]
+    assert she.br_engine(ctx) == {"ntt": 0, "fft3": 3, "fft2x2": 2, "fft-v1": 4,
+                                  "fft-2groups": 4}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
     she.she_gate_batch_ops(ctx, dev(np.asarray(ops, np.uint8)), dev(a), dev(b), dev(c), out)
