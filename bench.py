@@ -449,6 +449,8 @@ def engine_options(args) -> dict:
         opts["fft_variant"] = args.fft_variant
     if args.fft_groups:
         opts["fft_groups"] = args.fft_groups
+    if args.fft_prefetch:
+        opts["fft_prefetch"] = args.fft_prefetch
     return opts
 
 
@@ -773,6 +775,8 @@ def main():
                     help="FFT engine transform (she_ctx_options.fft_variant: 1 round-1, 2 v2)")
     ap.add_argument("--fft-groups", type=int, default=0,
                     help="FFT engine independent lane groups per CTA (she_ctx_options.fft_groups)")
+    ap.add_argument("--fft-prefetch", type=int, default=0,
+                    help="BK planes prefetched before the pointwise barrier (she_ctx_options)")
     ap.add_argument("--count", type=int, default=COUNT,
                     help="gates per step (default: config 1's 4096; other values are A/B only)")
     args = ap.parse_args()

@@ -142,15 +142,20 @@ typedef struct {
                      2 (two CTAs per SM), 3, 4 or 5 */
   int ntt_lanes;  /* NTT engine: lanes per CTA x CTAs per SM, 0 = default 5 x 1; */
   int ntt_ctas;   /*   the instantiated shapes are 5x1, 4x1, 3x1, 2x2, 1x4      */
-  int ks_kernel;  /* 0 = default (ks2_kernel for base 4, t = 8), 1 = the general
-                     ks_kernel (any base-4 decomposition) */
+  int ks_kernel;  /* 0 = default; 1 = the general ks_kernel (any base-4
+                     decomposition); 2 = ks2_kernel (CUDA cores, base 4, t = 8);
+                     3 = the tensor-core key switch (ks_imma.cuh: 0/1 digit
+                     matrix x key byte planes on mma.sync u8, base 4, t = 8) */
   int fft_variant;/* FFT engine transform: 0 = default (2), 1 = the round-1
                      transform (16-entry twiddle tables, select-based pair
                      exchange; 4 lanes per CTA only), 2 = v2 */
   int fft_groups; /* FFT engine: independent lane groups per CTA, 0 = default
                      (1); 2 = two groups of 2 lanes with their own pointwise
                      step and barriers (4 lanes per CTA, variant 2) */
-  int reserved[5];/* must be 0 */
+  int fft_prefetch;/* FFT engine: BK_i planes prefetched into registers before
+                     the pointwise barrier: 0 = default (16), 1 = 16, 2 = 8
+                     (4 or 5 lanes), 3 = none (5 lanes) */
+  int reserved[4];/* must be 0 */
 } she_ctx_options;
 
 /* Create a context on CUDA `device`: uploads BK and KSK and transforms BK for

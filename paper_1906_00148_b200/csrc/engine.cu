@@ -21,6 +21,7 @@
 #include "../../she_inputs/she_rng.h"
 #include "bootstrap_core.cuh"
 #include "fft_core.cuh"
+#include "ks_imma.cuh"
 #include "common.h"
 #include "engine.h"
 #include "keys.h"
@@ -437,7 +438,7 @@ __device__ __forceinline__ void group_arrive(int id, int count) {
 // named barriers, so that the groups drift apart in phase and one group's
 // FP64-bound transforms overlap another's shared-memory-bound steps; the
 // second group starts one forward transform behind the first.
-template <int G, int B = 1, int V = kFftDefaultVariant, int GRP = 1>
+template <int G, int B = 1, int V = kFftDefaultVariant, int GRP = 1, int PRE = 16>
 __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
   using S = ntt::Shape<1024>;
   constexpr int N = fft::kN, M = fft::kM, T = 128 * G;
@@ -507,13 +508,19 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
       // BK_i planes of this thread's first frequency (k = gt) are requested
       // before the barrier, so their L2 latency overlaps the wait for the
       // slowest warp's forward transform
+      // (PRE of the 16 planes: fewer prefetch registers for shapes with more
+      // lanes per CTA; the rest are loaded after the barrier)
       const double2* bki = args.bkf + (size_t)i * 16 * M;
       double2 bpre[16];
       if (gt < M) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) bpre[q] = __ldg(bki + (size_t)q * M + gt);
+        for (int q = 0; q < PRE; ++q) bpre[q] = __ldg(bki + (size_t)q * M + gt);
       }
       group_sync(gbar, TG);
+      if (gt < M) {
+#pragma unroll
+        for (int q = PRE; q < 16; ++q) bpre[q] = __ldg(bki + (size_t)q * M + gt);
+      }
       {  // pointwise: frequency k, all lanes of the group, BK_i planes read once
         auto pointwise = [&](int k, const double2 (&b)[16]) {
 #pragma unroll
@@ -771,6 +778,7 @@ constexpr int kKsG = 16, kKsCH = 64;
 // (gate, i, j) are prepared once per CTA in shared memory (broadcast LDS.64).
 // Device layout of the repacked key: [N][8][3][stride] rows (K1, K2, NK3).
 constexpr int kKs2G = 16, kKs2CH = 16, kKs2T = 256;
+constexpr bool kKsImmaDefault = false;  // default key switch: tensor cores (ks_imma.cuh)
 
 template <int G, int CH>
 __global__ void __launch_bounds__(kKs2T, 2) ks2_kernel(KSArgs args) {
@@ -867,6 +875,75 @@ __global__ void __launch_bounds__(kKs2T, 2) ks2_kernel(KSArgs args) {
       }
       o[kk] = v;
     }
+  }
+}
+
+// K4 on the tensor cores (ks_imma.cuh), step 1: gate g's row of the 0/1
+// matrix A — (b0, b1, b0 b1) of the 8 base-4 digits of every extracted
+// coefficient a'_i rounded to 16 bits (R10), MUX lanes combined — and b'_g.
+// Gates without a key switch (NOT, COPY, padding rows) get a zero row.
+__global__ void ksi_prep_kernel(GateSrc src, const uint32_t* ext, uint32_t ext_stride, uint32_t N,
+                                uint8_t* A, uint32_t K, uint32_t* bprime) {
+  const uint32_t g = blockIdx.x;
+  const int op = g < src.count ? gate_op(src, g) : -1;
+  const bool ks = op >= 0 && op < SHE_NOT;
+  const uint32_t round = 1u << (32 - 2 * 8 - 1);
+  uint32_t* row = reinterpret_cast<uint32_t*>(A + (size_t)g * K);
+  const uint32_t* e0 = ext + (size_t)(2 * g) * ext_stride;
+  const uint32_t* e1 = e0 + ext_stride;
+  for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+    uint32_t w[6] = {0, 0, 0, 0, 0, 0};
+    if (ks) {
+      uint32_t a = e0[i];
+      if (op == SHE_MUX) a += e1[i];
+      const uint32_t y = a + round;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t d = (y >> (30 - 2 * j)) & 3u;
+        const uint32_t b3 = (d & 1u) | ((d >> 1) << 8) | ((d == 3u ? 1u : 0u) << 16);  // 3 bytes
+        const int byte = 3 * j;  // bytes 3j .. 3j + 2 of the 24
+        w[byte >> 2] |= b3 << (8 * (byte & 3));
+        if ((byte & 3) >= 2) w[(byte >> 2) + 1] |= b3 >> (8 * (4 - (byte & 3)));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) row[6 * i + q] = w[q];
+  }
+  if (threadIdx.x == 0) {
+    uint32_t b = 0;
+    if (ks) {
+      b = e0[N];
+      if (op == SHE_MUX) b += e1[N] + kMu;
+    }
+    bprime[g] = b;
+  }
+}
+
+// K4 step 3: out = (0, b') - sum_p C_p << 8p over the columns (word, plane);
+// NOT / COPY gates copy (negated) input a, as the other key-switch kernels.
+__global__ void ksi_combine_kernel(GateSrc src, const int32_t* C, uint32_t ncols,
+                                   const uint32_t* bprime, uint32_t n) {
+  const uint32_t g = blockIdx.x;
+  const int op = gate_op(src, g);
+  if (op < 0) return;
+  uint32_t* o = gate_out(src, g);
+  const uint32_t stride = src.stride;
+  for (uint32_t w = threadIdx.x; w < stride; w += blockDim.x) {
+    uint32_t v;
+    if (op == SHE_NOT || op == SHE_COPY) {
+      bool neg;
+      const uint32_t* a = gate_in(src, g, 0, neg);
+      if (op == SHE_NOT) neg = !neg;
+      v = w <= n ? (neg ? 0u - a[w] : a[w]) : 0u;
+    } else if (w <= n) {
+      const int4 c = *reinterpret_cast<const int4*>(C + (size_t)g * ncols + 4 * w);
+      const uint32_t s = (uint32_t)c.x + ((uint32_t)c.y << 8) + ((uint32_t)c.z << 16) +
+                         ((uint32_t)c.w << 24);
+      v = (w == n ? bprime[g] : 0u) - s;
+    } else {
+      v = 0u;
+    }
+    o[w] = v;
   }
 }
 
@@ -1026,8 +1103,16 @@ struct she_ctx {
   int fft_g = 4;
   int fft_v = kFftDefaultVariant;  // FFT variant (FftVar): 1 = round-1 transform, 2 = v2
   int fft_grp = 1;                 // independent lane groups per CTA (br_fft_kernel GRP)
+  int fft_pre = 16;                // BK planes prefetched before the pre-pointwise barrier
   double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
+  // key switch on the tensor cores (ks_imma.cuh; base 4, t = 8)
+  bool ksi = false;
+  uint8_t* ksi_bt = nullptr;   // [stride * 4 columns (word, plane)][K = 24 N] key byte planes
+  uint8_t* ksi_a = nullptr;    // [ksi_cap rows][K] 0/1 digit matrix
+  int32_t* ksi_c = nullptr;    // [ksi_cap][stride * 4] products
+  uint32_t* ksi_bp = nullptr;  // [ksi_cap] b'
+  size_t ksi_cap = 0;
   // staging for the host-buffer API
   uint8_t* h_ops = nullptr;
   uint32_t* h_io = nullptr;
@@ -1128,6 +1213,12 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
                             (int)(2 * lb + fft_tables_bytes<2>())));
     CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(4 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<5, 1, 2, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(5 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<5, 1, 2, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(5 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 2, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(4 * lb + fft_tables_bytes<2>())));
   }
   cudaFree(d_bk32);
 #define SHE_BR_SMEM(G, B)                                                            \
@@ -1195,7 +1286,7 @@ she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream
   return SHE_OK;
 }
 
-template <int G, int B, int V, int GRP = 1>
+template <int G, int B, int V, int GRP = 1, int PRE = 16>
 she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
   BRFArgs f;
   f.src = a.src;
@@ -1221,7 +1312,63 @@ she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  CK(cudaLaunchKernelEx(&cfg, br_fft_kernel<G, B, V, GRP>, f));
+  CK(cudaLaunchKernelEx(&cfg, br_fft_kernel<G, B, V, GRP, PRE>, f));
+  return SHE_OK;
+}
+
+// The gate window [g0, g0 + cnt) of a source as a source of its own.
+GateSrc shift_src(GateSrc s, size_t g0, size_t cnt) {
+  if (s.ops) s.ops += g0;
+  if (s.in_idx) {
+    s.in_idx += 3 * g0;
+    s.out_idx += g0;
+  } else {
+    for (int j = 0; j < 3; ++j)
+      if (s.in[j]) s.in[j] += g0 * s.stride;
+    s.out += g0 * s.stride;
+  }
+  s.count = (uint32_t)cnt;
+  return s;
+}
+
+// Gates per tensor-core key-switch pass (bounds the A and C scratch).
+constexpr size_t kKsiBatch = 8192;
+
+// K4 on the tensor cores for the `cnt` gates of s (their extracted samples at
+// ctx->ext rows 2g, 2g + 1): prep -> IMMA GEMM -> combine, in passes of
+// kKsiBatch gates.
+she_status run_ks_imma(she_ctx* ctx, const GateSrc& s, size_t cnt, cudaStream_t stream) {
+  const uint32_t N = ctx->p.N;
+  const size_t K = (size_t)N * 8 * 3, ncols = (size_t)ctx->stride * 4;
+  const size_t want = std::min(kKsiBatch, (cnt + ksi::BM - 1) / ksi::BM * ksi::BM);
+  if (ctx->ksi_cap < want) {
+    CK(cudaStreamSynchronize(stream));
+    cudaFree(ctx->ksi_a);
+    cudaFree(ctx->ksi_c);
+    cudaFree(ctx->ksi_bp);
+    ctx->ksi_a = nullptr;
+    ctx->ksi_c = nullptr;
+    ctx->ksi_bp = nullptr;
+    ctx->ksi_cap = 0;
+    CK(cudaMalloc(&ctx->ksi_a, want * K));
+    CK(cudaMalloc(&ctx->ksi_c, want * ncols * 4));
+    CK(cudaMalloc(&ctx->ksi_bp, want * 4));
+    ctx->ksi_cap = want;
+  }
+  for (size_t b0 = 0; b0 < cnt; b0 += kKsiBatch) {
+    const size_t bc = std::min(kKsiBatch, cnt - b0);
+    const size_t rows = (bc + ksi::BM - 1) / ksi::BM * ksi::BM;
+    GateSrc sb = shift_src(s, b0, bc);
+    // extracted samples of this pass start at row 2 * b0
+    ksi_prep_kernel<<<(unsigned)rows, 256, 0, stream>>>(sb, ctx->ext + 2 * b0 * ctx->ext_stride,
+                                                        ctx->ext_stride, N, ctx->ksi_a, (uint32_t)K,
+                                                        ctx->ksi_bp);
+    ksi::ksi_gemm<<<dim3((unsigned)(ncols / ksi::BN), (unsigned)(rows / ksi::BM)), ksi::kThreads,
+                    ksi::kSmem, stream>>>(ctx->ksi_a, ctx->ksi_bt, ctx->ksi_c, (int)K, (int)ncols);
+    ksi_combine_kernel<<<(unsigned)bc, 128, 0, stream>>>(sb, ctx->ksi_c, (uint32_t)ncols,
+                                                         ctx->ksi_bp, ctx->p.n);
+    CK(cudaGetLastError());
+  }
   return SHE_OK;
 }
 
@@ -1263,6 +1410,9 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
       st = ctx->fft_v == 1   ? launch_br_fft<4, 1, 1>(ctx, a, 2 * cnt, stream)
            : ctx->fft_grp == 2 ? launch_br_fft<4, 1, 2, 2>(ctx, a, 2 * cnt, stream)
            : ctx->fft_g == 3 ? launch_br_fft<3, 1, 2>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_g == 5 && ctx->fft_pre == 0 ? launch_br_fft<5, 1, 2, 1, 0>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_g == 5 && ctx->fft_pre == 8 ? launch_br_fft<5, 1, 2, 1, 8>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_g == 4 && ctx->fft_pre == 8 ? launch_br_fft<4, 1, 2, 1, 8>(ctx, a, 2 * cnt, stream)
            : ctx->fft_g == 5 ? launch_br_fft<5, 1, 2>(ctx, a, 2 * cnt, stream)
            : ctx->fft_g == 2 ? launch_br_fft<2, 2, 2>(ctx, a, 2 * cnt, stream)
                              : launch_br_fft<4, 1, 2>(ctx, a, 2 * cnt, stream);
@@ -1283,10 +1433,14 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     k.N = ctx->p.N;
     k.n = ctx->p.n;
     k.t = ctx->p.ks_t;
-    if (ctx->ks2)
+    if (ctx->ksi) {
+      st = run_ks_imma(ctx, s, cnt, stream);
+      if (st != SHE_OK) return st;
+    } else if (ctx->ks2) {
       ks2_kernel<kKs2G, kKs2CH><<<(unsigned)((cnt + kKs2G - 1) / kKs2G), kKs2T, 0, stream>>>(k);
-    else
+    } else {
       ks_kernel<kKsG, kKsCH><<<(unsigned)((cnt + kKsG - 1) / kKsG), ctx->stride, 0, stream>>>(k);
+    }
     CK(cudaGetLastError());
     if (ctx->timing) mark(ctx, stream);
     ctx->br_launches++;
@@ -1341,13 +1495,21 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     return fail(SHE_ERR_ARG, "NTT shape %dx%d is not instantiated", o.ntt_lanes, o.ntt_ctas);
   if ((o.ntt_lanes || o.ntt_ctas) && use_fft)
     return fail(SHE_ERR_ARG, "ntt_lanes/ntt_ctas given for the FFT engine");
-  if (o.ks_kernel < 0 || o.ks_kernel > 1) return fail(SHE_ERR_ARG, "ks_kernel=%d", o.ks_kernel);
+  if (o.ks_kernel < 0 || o.ks_kernel > 3) return fail(SHE_ERR_ARG, "ks_kernel=%d", o.ks_kernel);
+  if (o.ks_kernel >= 2 && !(p->ks_t == 8 && p->ks_base_bits == 2))
+    return fail(SHE_ERR_ARG, "ks_kernel %d needs base 4, t = 8", o.ks_kernel);
   if (o.fft_variant < 0 || o.fft_variant > 2)
     return fail(SHE_ERR_ARG, "fft_variant=%d: expected 0, 1 or 2", o.fft_variant);
   if (o.fft_variant && !use_fft) return fail(SHE_ERR_ARG, "fft_variant given for the NTT engine");
   if (o.fft_variant == 1 && o.fft_lanes && o.fft_lanes != 4)
     return fail(SHE_ERR_ARG, "fft_variant 1 is instantiated for 4 lanes per CTA only");
   if (o.fft_groups < 0 || o.fft_groups > 2) return fail(SHE_ERR_ARG, "fft_groups=%d", o.fft_groups);
+  if (o.fft_prefetch < 0 || o.fft_prefetch > 3)
+    return fail(SHE_ERR_ARG, "fft_prefetch=%d", o.fft_prefetch);
+  if (o.fft_prefetch >= 2 && (o.fft_groups == 2 || o.fft_variant == 1 || !use_fft ||
+                              (o.fft_lanes != 4 && o.fft_lanes != 5 && o.fft_lanes != 0) ||
+                              (o.fft_prefetch == 3 && o.fft_lanes != 5)))
+    return fail(SHE_ERR_ARG, "fft_prefetch %d is not instantiated for this shape", o.fft_prefetch);
   if (o.fft_groups == 2 && ((o.fft_lanes && o.fft_lanes != 4) || o.fft_variant == 1 || !use_fft))
     return fail(SHE_ERR_ARG, "fft_groups = 2 is instantiated for 4 lanes per CTA, variant 2");
   CK(cudaSetDevice(device));
@@ -1368,6 +1530,7 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   ctx->fft_g = use_fft ? (o.fft_lanes ? o.fft_lanes : 4) : 0;
   ctx->fft_v = o.fft_variant ? o.fft_variant : kFftDefaultVariant;
   ctx->fft_grp = o.fft_groups ? o.fft_groups : 1;
+  ctx->fft_pre = o.fft_prefetch == 0 ? 16 : o.fft_prefetch == 3 ? 0 : o.fft_prefetch == 2 ? 8 : 16;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
     she_ctx_destroy(ctx);
@@ -1385,7 +1548,34 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
                  &ck->ksk[(((size_t)i * t + j) * base + v) * (n + 1)], (n + 1) * 4);
     // ks_kernel = 1 forces ks_kernel (the general-parameter path) so that the
     // tests can pin it on the configs' parameters as well
-    ctx->ks2 = o.ks_kernel == 0 && (t == 8 && base == 4 && ctx->stride <= 2 * (uint32_t)kKs2T);
+    const bool base4t8 = t == 8 && base == 4 && ctx->stride <= 2 * (uint32_t)kKs2T;
+    ctx->ksi = base4t8 && (o.ks_kernel == 3 || (o.ks_kernel == 0 && kKsImmaDefault));
+    ctx->ks2 = base4t8 && !ctx->ksi && (o.ks_kernel == 0 || o.ks_kernel == 2);
+    if (ctx->ksi) {  // the key's byte planes, columns (word, plane), K = (i, j, v) contiguous
+      const size_t K = (size_t)N * t * 3, cols = (size_t)ctx->stride * 4;
+      std::vector<uint8_t> bt(cols * K, 0);
+      for (uint32_t i = 0; i < N; ++i)
+        for (uint32_t j = 0; j < t; ++j) {
+          const uint32_t* k1 = &ck->ksk[(((size_t)i * t + j) * base + 1) * (n + 1)];
+          const uint32_t* k2 = k1 + (n + 1);
+          const uint32_t* k3 = k2 + (n + 1);
+          for (uint32_t w = 0; w <= n; ++w) {
+            const uint32_t r[3] = {k1[w], k2[w], k3[w] - k1[w] - k2[w]};
+            for (int v = 0; v < 3; ++v)
+              for (int p = 0; p < 4; ++p)
+                bt[((size_t)w * 4 + p) * K + ((size_t)i * t + j) * 3 + v] = (uint8_t)(r[v] >> (8 * p));
+          }
+        }
+      cudaError_t e = cudaMalloc(&ctx->ksi_bt, bt.size());
+      if (e == cudaSuccess) e = cudaMemcpy(ctx->ksi_bt, bt.data(), bt.size(), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ksi::ksi_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)ksi::kSmem);
+      if (e != cudaSuccess) {
+        she_ctx_destroy(ctx);
+        return cuda_fail(e, "tensor-core key-switch setup");
+      }
+    }
     if (ctx->ks2)  // third row -> K1 + K2 - K3 (mod 2^32), see ks2_kernel
       for (size_t r = 0; r < (size_t)N * t; ++r) {
         uint32_t* row = &h[r * 3 * ctx->stride];
@@ -1427,6 +1617,10 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaFree(ctx->bkf);
 
   cudaFree(ctx->ksk);
+  cudaFree(ctx->ksi_bt);
+  cudaFree(ctx->ksi_a);
+  cudaFree(ctx->ksi_c);
+  cudaFree(ctx->ksi_bp);
   cudaFree(ctx->tw);
   cudaFree(ctx->itw);
   cudaFree(ctx->ext);

@@ -46,15 +46,17 @@ class she_ctx_options(ctypes.Structure):
     _fields_ = [("br_engine", ctypes.c_int), ("fft_lanes", ctypes.c_int),
                 ("ntt_lanes", ctypes.c_int), ("ntt_ctas", ctypes.c_int),
                 ("ks_kernel", ctypes.c_int), ("fft_variant", ctypes.c_int),
-                ("fft_groups", ctypes.c_int), ("reserved", ctypes.c_int * 5)]
+                ("fft_groups", ctypes.c_int), ("fft_prefetch", ctypes.c_int),
+                ("reserved", ctypes.c_int * 4)]
 
     ENGINES = {"default": 0, "fft": 1, "ntt": 2}
 
     @classmethod
     def of(cls, engine="default", fft_lanes=0, ntt_shape=(0, 0), ks_kernel="default",
-           fft_variant=0, fft_groups=0):
+           fft_variant=0, fft_groups=0, fft_prefetch=0):
         return cls(cls.ENGINES[engine], fft_lanes, ntt_shape[0], ntt_shape[1],
-                   {"default": 0, "general": 1}[ks_kernel], fft_variant, fft_groups)
+                   {"default": 0, "general": 1, "cuda": 2, "imma": 3}[ks_kernel], fft_variant,
+                   fft_groups, fft_prefetch)
 
 
 class she_circuit_stats(ctypes.Structure):

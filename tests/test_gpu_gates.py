@@ -287,10 +287,13 @@ def test_config1_full_parity_vs_oracle_digests(env1, config1_outputs):
 
 ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3),
                "fft2x2": dict(engine="fft", fft_lanes=2), "fft-v1": dict(engine="fft", fft_variant=1),
-               "fft-2groups": dict(engine="fft", fft_groups=2)}
+               "fft-2groups": dict(engine="fft", fft_groups=2),
+               "fft5-noprefetch": dict(engine="fft", fft_lanes=5, fft_prefetch=3),
+               "ks-imma": dict(ks_kernel="imma"), "ks-cuda": dict(ks_kernel="cuda")}
 
 
-@pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2", "fft-v1", "fft-2groups"])
+@pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2", "fft-v1", "fft-2groups",
+                                    "fft5-noprefetch", "ks-imma", "ks-cuda"])
 def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with 4 lanes per
     CTA; the Goldilocks NTT engine (she_ctx_options.br_engine = 2) and the other
@@ -301,7 +304,8 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
     P = env1.P
     ctx = she.Context(P, env1.ck, device=0, **ENGINE_OPTS[engine])
     assert she.br_engine(ctx) == {"ntt": 0, "fft3": 3, "fft2x2": 2, "fft-v1": 4,
-                                  "fft-2groups": 4}[engine]
+                                  "fft-2groups": 4, "fft5-noprefetch": 5, "ks-imma": 4,
+                                  "ks-cuda": 4}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
     she.she_gate_batch_ops(ctx, dev(np.asarray(ops, np.uint8)), dev(a), dev(b), dev(c), out)
@@ -397,13 +401,16 @@ def test_gpu_client_matches_host_client(cuda, cfg):
 
 
 
-def test_legacy_key_switch_kernel_c0(cuda):
-    """ks_kernel (any base / t; used when the key-switching parameters are not
-    base 4, t = 8) on the config-0 gates: bit-exact with the oracle too."""
+@pytest.mark.parametrize("ks", ["general", "cuda", "imma"])
+def test_key_switch_kernels_c0(cuda, ks):
+    """Every key-switch kernel on the config-0 gates (n = 128: an LWE slot of
+    160 words, 5 column tiles of the tensor-core GEMM): bit-exact with the
+    oracle.  "general" is ks_kernel (any base / t), "cuda" ks2_kernel, "imma"
+    the tensor-core product (ks_imma.cuh)."""
     cfg, count = 0, 16
     P = si.CONFIG_PARAMS[cfg]
     sk, ck = she.she_keygen(P, si.key_seed(cfg))
-    ctx = she.Context(P, ck, device=0, ks_kernel="general")
+    ctx = she.Context(P, ck, device=0, ks_kernel=ks)
     ops = si.gate_ops(cfg, count)
     bits = si.gate_input_bits(cfg, count)
     cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0).reshape(count, 3, -1)
@@ -414,3 +421,35 @@ def test_legacy_key_switch_kernel_c0(cuda):
     K = oracle.keygen(P, si.key_seed(cfg))
     assert np.array_equal(host(out), oracle.gates(K, ops, a, b, c))
     ctx.close()
+
+
+def test_tensor_core_key_switch_multi_pass_c0(cuda):
+    """8,300 config-0 gates: the tensor-core key switch runs in passes of 8,192
+    gates (kKsiBatch) with a ragged last pass; every output equals the CUDA-core
+    ks2 path's (itself pinned to the oracle above), and a seed-sampled subset
+    equals the oracle directly."""
+    cfg, count = 0, 8300
+    P = si.CONFIG_PARAMS[cfg]
+    sk, ck = she.she_keygen(P, si.key_seed(cfg))
+    ops = si.gate_ops(cfg, count)
+    bits = si.gate_input_bits(cfg, count)
+    cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0).reshape(count, 3, -1)
+    a, b, c = (np.ascontiguousarray(cts[:, j]) for j in range(3))
+    outs = {}
+    for ks in ("imma", "cuda"):
+        ctx = she.Context(P, ck, device=0, ks_kernel=ks)
+        out = torch.zeros((count, P.stride), dtype=torch.int32, device="cuda")
+        she.she_gate_batch_ops(ctx, torch.from_numpy(ops.astype(np.uint8)).cuda(), dev(a), dev(b),
+                               dev(c), out)
+        torch.cuda.synchronize()
+        outs[ks] = host(out)
+        ctx.close()
+    assert np.array_equal(outs["imma"], outs["cuda"])
+    rng = np.random.default_rng(si.sample_seed(0) + 3)
+    pick = np.sort(rng.choice(count, 24, replace=False))
+    pick[-1] = count - 1  # the last gate of the ragged pass
+    K = oracle.keygen(P, si.key_seed(cfg))
+    ref = oracle.gates(K, ops[pick], a[pick], b[pick], c[pick])
+    assert np.array_equal(outs["imma"][pick], ref)
+    want = np.array([si.truth(o, *bb) for o, bb in zip(ops, bits)])
+    assert np.array_equal(she.she_decrypt_bits(sk, outs["imma"]), want)
