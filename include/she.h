@@ -148,7 +148,9 @@ typedef struct {
                      matrix x key byte planes on mma.sync u8, base 4, t = 8) */
   int fft_variant;/* FFT engine transform: 0 = default (2), 1 = the round-1
                      transform (16-entry twiddle tables, select-based pair
-                     exchange; 4 lanes per CTA only), 2 = v2 */
+                     exchange; 4 lanes per CTA only), 2 = v2,
+                     3 = v2 with DIT/FMA 16-point DFTs (4 lanes, or 5 lanes
+                     with fft_prefetch = 3) */
   int fft_groups; /* FFT engine: independent lane groups per CTA, 0 = default
                      (1); 2 = two groups of 2 lanes with their own pointwise
                      step and barriers (4 lanes per CTA, variant 2) */

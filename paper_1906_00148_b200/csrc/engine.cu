@@ -340,6 +340,20 @@ struct FftVar<2> {
   }
   __device__ static double2 bk_correction(int k) { return fft::v2_bk_correction(k); }
 };
+template <>
+struct FftVar<3> {  // v2's tables and scaling, DIT/FMA DFT16s (fft_core.cuh)
+  static constexpr int kTab = fft::kTw2 * 32;
+  __device__ static void tables(int t, int n, double2* f, double2* i) { fft::make_tables2(t, n, f, i); }
+  __device__ static void forward(const double (&re)[16], const double (&im)[16], int lane,
+                                 const double2* tw, double2* row) {
+    fft::forward_v3(re, im, lane, tw, row);
+  }
+  __device__ static void inverse(const double2* in, int lane, const double2* tw, double2* row,
+                                 double2 (&x)[8], double2 (&y)[8]) {
+    fft::inverse_v3(in, lane, tw, row, x, y);
+  }
+  __device__ static double2 bk_correction(int k) { return fft::v2_bk_correction(k); }
+};
 constexpr int kFftDefaultVariant = 2;
 template <int V>
 constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double2); }
@@ -1196,6 +1210,8 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
     CK(cudaMalloc(&ctx->bkf, ctx->bk_bytes));
     if (ctx->fft_v == 1)
       bk_fft_kernel<1><<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkf, (uint32_t)polys);
+    else if (ctx->fft_v == 3)
+      bk_fft_kernel<3><<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkf, (uint32_t)polys);
     else
       bk_fft_kernel<2><<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkf, (uint32_t)polys);
     CK(cudaGetLastError());
@@ -1219,6 +1235,10 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
                             (int)(5 * lb + fft_tables_bytes<2>())));
     CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 2, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(4 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(4 * lb + fft_tables_bytes<3>())));
+    CK(cudaFuncSetAttribute(br_fft_kernel<5, 1, 3, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(5 * lb + fft_tables_bytes<3>())));
   }
   cudaFree(d_bk32);
 #define SHE_BR_SMEM(G, B)                                                            \
@@ -1408,6 +1428,8 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     st = fail(SHE_ERR_STATE, "no blind-rotation kernel for config %dx%d", ctx->br_g, ctx->br_b);
     if (ctx->bkf && S::N == fft::kN) {
       st = ctx->fft_v == 1   ? launch_br_fft<4, 1, 1>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_v == 3 && ctx->fft_g == 5 ? launch_br_fft<5, 1, 3, 1, 0>(ctx, a, 2 * cnt, stream)
+           : ctx->fft_v == 3 ? launch_br_fft<4, 1, 3>(ctx, a, 2 * cnt, stream)
            : ctx->fft_grp == 2 ? launch_br_fft<4, 1, 2, 2>(ctx, a, 2 * cnt, stream)
            : ctx->fft_g == 3 ? launch_br_fft<3, 1, 2>(ctx, a, 2 * cnt, stream)
            : ctx->fft_g == 5 && ctx->fft_pre == 0 ? launch_br_fft<5, 1, 2, 1, 0>(ctx, a, 2 * cnt, stream)
@@ -1498,15 +1520,19 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   if (o.ks_kernel < 0 || o.ks_kernel > 3) return fail(SHE_ERR_ARG, "ks_kernel=%d", o.ks_kernel);
   if (o.ks_kernel >= 2 && !(p->ks_t == 8 && p->ks_base_bits == 2))
     return fail(SHE_ERR_ARG, "ks_kernel %d needs base 4, t = 8", o.ks_kernel);
-  if (o.fft_variant < 0 || o.fft_variant > 2)
-    return fail(SHE_ERR_ARG, "fft_variant=%d: expected 0, 1 or 2", o.fft_variant);
+  if (o.fft_variant < 0 || o.fft_variant > 3)
+    return fail(SHE_ERR_ARG, "fft_variant=%d: expected 0 .. 3", o.fft_variant);
+  if (o.fft_variant == 3 && !((o.fft_lanes == 0 || o.fft_lanes == 4) ||
+                              (o.fft_lanes == 5 && o.fft_prefetch == 3)))
+    return fail(SHE_ERR_ARG, "fft_variant 3 is instantiated for 4 lanes, or 5 without prefetch");
   if (o.fft_variant && !use_fft) return fail(SHE_ERR_ARG, "fft_variant given for the NTT engine");
   if (o.fft_variant == 1 && o.fft_lanes && o.fft_lanes != 4)
     return fail(SHE_ERR_ARG, "fft_variant 1 is instantiated for 4 lanes per CTA only");
   if (o.fft_groups < 0 || o.fft_groups > 2) return fail(SHE_ERR_ARG, "fft_groups=%d", o.fft_groups);
   if (o.fft_prefetch < 0 || o.fft_prefetch > 3)
     return fail(SHE_ERR_ARG, "fft_prefetch=%d", o.fft_prefetch);
-  if (o.fft_prefetch >= 2 && (o.fft_groups == 2 || o.fft_variant == 1 || !use_fft ||
+  if (o.fft_prefetch >= 2 && (o.fft_groups == 2 || o.fft_variant == 1 ||
+                              (o.fft_variant == 3 && o.fft_prefetch != 3) || !use_fft ||
                               (o.fft_lanes != 4 && o.fft_lanes != 5 && o.fft_lanes != 0) ||
                               (o.fft_prefetch == 3 && o.fft_lanes != 5)))
     return fail(SHE_ERR_ARG, "fft_prefetch %d is not instantiated for this shape", o.fft_prefetch);
@@ -1815,7 +1841,7 @@ she_status she_fft_product_selftest(int device, int variant, const int32_t* digi
                                     double* worst_distance) {
   if (count == 0) return SHE_OK;
   if (!digits || !bk || !out) return fail(SHE_ERR_ARG, "NULL argument");
-  if (variant < 0 || variant > 2) return fail(SHE_ERR_ARG, "variant=%d", variant);
+  if (variant < 0 || variant > 3) return fail(SHE_ERR_ARG, "variant=%d", variant);
   const int V = variant ? variant : kFftDefaultVariant;
   if (count > 65535) return fail(SHE_ERR_ARG, "count > 65535");
   constexpr size_t N = fft::kN;
@@ -1835,16 +1861,17 @@ she_status she_fft_product_selftest(int device, int variant, const int32_t* digi
   if (e == cudaSuccess) e = cudaMemcpy(db, bk, count * 8 * N * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {  // the setup transform of the engine (BK -> FFT domain, halves)
     if (V == 1) bk_fft_kernel<1><<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
+    else if (V == 3) bk_fft_kernel<3><<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
     else bk_fft_kernel<2><<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
     e = cudaGetLastError();
   }
   constexpr size_t smem = (4 * fft::kRow + 2 * 512) * sizeof(double2) + 2 * N * 4;
+  auto selftest = V == 1 ? fft_selftest_kernel<1> : V == 3 ? fft_selftest_kernel<3>
+                                                            : fft_selftest_kernel<2>;
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(V == 1 ? fft_selftest_kernel<1> : fft_selftest_kernel<2>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) {
-    if (V == 1) fft_selftest_kernel<1><<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
-    else fft_selftest_kernel<2><<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
+    selftest<<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpy(out, dout, count * 2 * N * 4, cudaMemcpyDeviceToHost);

@@ -217,6 +217,52 @@ __device__ __forceinline__ void dft16(double2 (&a)[16]) {
   }
 }
 
+// The same 16-point DFT by radix-2 decimation in time with FMA butterflies
+// (variant 3): the input is read through the compile-time relabelling
+// b[i] = a[brev4(i)], so the output lands in the same registers as dft16's,
+// a[brev4(k)] = X[k].  A butterfly (u, v) -> (u + w v, u - w v) with a general
+// twiddle is 4 DFMA for x = u + w v and 2 DFMA for y = 2 u - x: 6 FP64
+// instructions instead of DIF's 8; w = +-1, +-i cost 4 DADD.  148 FP64
+// instructions per DFT16 instead of 168.
+template <int SIGN>
+__device__ __forceinline__ void dft16_dit(double2 (&a)[16]) {
+#pragma unroll
+  for (int s = 1; s <= 8; s <<= 1) {
+#pragma unroll
+    for (int g0 = 0; g0 < 16; g0 += 2 * s) {
+#pragma unroll
+      for (int j = 0; j < s; ++j) {
+        double2& U = a[brev4(g0 + j)];
+        double2& Vr = a[brev4(g0 + j + s)];
+        const double2 u = U, v = Vr;
+        const int e = (SIGN * j * (64 / s)) & 127;  // w = W128^e = w_(2s)^(SIGN j)
+        double2 x, y;
+        if (e == 0) {
+          x = cadd(u, v);
+          y = csub(u, v);
+        } else if (e == 64) {
+          x = csub(u, v);
+          y = cadd(u, v);
+        } else if (e == 32) {  // w = i: w v = (-v.y, v.x)
+          x = make_double2(u.x - v.y, u.y + v.x);
+          y = make_double2(u.x + v.y, u.y - v.x);
+        } else if (e == 96) {  // w = -i: w v = (v.y, -v.x)
+          x = make_double2(u.x + v.y, u.y - v.x);
+          y = make_double2(u.x - v.y, u.y + v.x);
+        } else {
+          const double2 w = c_w128[e];
+          x.x = fma(w.x, v.x, fma(-w.y, v.y, u.x));
+          x.y = fma(w.x, v.y, fma(w.y, v.x, u.y));
+          y.x = fma(2.0, u.x, -x.x);
+          y.y = fma(2.0, u.y, -x.y);
+        }
+        U = x;
+        Vr = y;
+      }
+    }
+  }
+}
+
 // Pass A + transpose + pass B of one 512-point DFT (direction SIGN) on warp-
 // private scratch (kRow complex).  In: a[n2] = point lane + 32 n2.  Per-thread
 // twiddle after pass A: tw[k2 * 32 + lane] (a shared table, see make_tables).
@@ -420,6 +466,80 @@ __device__ __forceinline__ void inverse_v2(const double2* row_in, int lane, cons
   for (int m = 0; m < 16; ++m) a[m] = row_in[fpos(lane + 32 * m)];
   __syncwarp();
   dft512_v2<-1>(a, lane, tw_inv, row, x, y);
+  const int h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    x[j] = cmulc(x[j], c_w128[h ? 40 + 5 * j : j]);
+    y[j] = cmulc(y[j], c_w128[h ? (5 * j - 8) & 127 : 16 + j]);
+  }
+}
+
+// ---- variant 3: variant 2 with DIT/FMA DFT16s and the FMA pair exchange ----
+template <int SIGN>
+__device__ __forceinline__ void dft512_v3(double2 (&a)[16], int lane, const double2* tw,
+                                          double2* scratch, double2 (&x)[8], double2 (&y)[8]) {
+  dft16_dit<SIGN>(a);
+  const double2 r8 = tw[8 * 32 + lane];
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2) {
+    const double2 p = tw[k2 * 32 + lane];
+    scratch[tslot(lane, k2)] = cmul(a[brev4(k2)], p);
+    scratch[tslot(lane, k2 + 8)] = cmul(a[brev4(k2 + 8)], cmul(p, r8));
+  }
+  __syncwarp();
+  const int k2 = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = scratch[tslot(2 * m + h, k2)];
+  dft16_dit<SIGN>(a);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double2 keep = a[brev4(j)], send = a[brev4(8 + j)];
+    double2 r;
+    r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+    r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+    // c0 = w32^(SIGN j), c1 = w32^(-SIGN (8 + j)): compile-time constants
+    const double2 c0 = c_w128[(SIGN * 4 * j) & 127];
+    const double2 c1 = c_w128[(-SIGN * 4 * (8 + j)) & 127];
+    double2 c;
+    c.x = h ? c1.x : c0.x;
+    c.y = h ? c1.y : c0.y;
+    // x = keep + c r (4 DFMA), y = 2 keep - x (2 DFMA)
+    x[j].x = fma(c.x, r.x, fma(-c.y, r.y, keep.x));
+    x[j].y = fma(c.x, r.y, fma(c.y, r.x, keep.y));
+    y[j].x = fma(2.0, keep.x, -x[j].x);
+    y[j].y = fma(2.0, keep.y, -x[j].y);
+  }
+  __syncwarp();  // scratch reads done before the caller reuses the row
+}
+
+// Forward v3: as forward_v2 with dft512_v3 (same scaling); the spectrum at k = k2 + 16 k1 is scaled by
+// sigma(k) = w32^(-k1) for k1 & 8, 1 otherwise (see above).
+__device__ __forceinline__ void forward_v3(const double (&re)[16], const double (&im)[16], int lane,
+                                           const double2* tw_fwd, double2* row) {
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = rot<1>(make_double2(re[m], im[m]), 2 * m);  // w64^m
+  double2 x[8], y[8];
+  dft512_v3<1>(a, lane, tw_fwd, row, x, y);
+  const int k2 = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    row[fpos(k2 + 16 * (8 * h + j))] = x[j];
+    row[fpos(k2 + 16 * (16 + 8 * h + j))] = y[j];
+  }
+}
+
+// Inverse v3 (as inverse_v2, dft512_v3) of the TRUE spectrum X[k] = row[fpos(k)]: outputs as inverse();
+// the untwist constants absorb thread 1's exchange scaling:
+//   h = 0: x * conj(W128[j]),        y * conj(W128[16 + j])
+//   h = 1: x * conj(W128[40 + 5 j]), y * conj(W128[(5 j - 8) & 127])
+__device__ __forceinline__ void inverse_v3(const double2* row_in, int lane, const double2* tw_inv,
+                                           double2* row, double2 (&x)[8], double2 (&y)[8]) {
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = row_in[fpos(lane + 32 * m)];
+  __syncwarp();
+  dft512_v3<-1>(a, lane, tw_inv, row, x, y);
   const int h = lane & 1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
