@@ -225,6 +225,10 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
     t_enc = time.perf_counter()  # client side (host): the paper's EDL column
     cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0)
     t_enc = time.perf_counter() - t_enc
+    t_ser = time.perf_counter()  # the message the client sends (MSize)
+    wire = she.serialize(P, cts)
+    cts = she.deserialize(P, wire)
+    t_ser = time.perf_counter() - t_ser
     x = torch.from_numpy(cts.view(np.int32)).cuda().reshape(28, 28, 1, 8, stride)
 
     from paper_1906_00148_b200.parallel import gather_shards, max_over_ranks, padded_words
@@ -307,7 +311,7 @@ def net_latency(ctx, sk, P, world: int, rank: int, tcn: bool = False):
             "logits": [int(v) for v in logits],
             "client": {"encrypt_s": round(t_enc, 4), "decrypt_s": round(t_dec, 5),
                        "edl_s": round(t_enc + t_dec, 4),
-                       "msize_bytes": int(bits.size * (P.n + 1) * 4),
+                       "msize_bytes": len(wire), "serialize_roundtrip_s": round(t_ser, 4),
                        "note": "host client (she_encrypt_bits / she_decrypt_bits): 784 pixels x 8 "
                                "bit-wise LWE ciphertexts of n+1 = 501 words (PAPER.md:256 MSize)",
                        "gpu": gpu_client},

@@ -109,6 +109,21 @@ she_status she_encrypt_bits(const she_secret_key* sk, const uint8_t* bits, size_
 she_status she_decrypt_bits(const she_secret_key* sk, const uint32_t* in, size_t count,
                             uint8_t* bits);
 
+/* Ciphertext batches on the wire (NEXT-4; the paper's MSize, PAPER.md:232,
+ * :256): a 16-byte header {u32 magic "SHEC", u32 n, u64 count} followed by
+ * count x (n + 1) little-endian uint32 words (a[0..n-1], b), slot padding not
+ * sent: she_serialized_bytes(p, count) = 16 + 4 count (n + 1).
+ * she_serialize_ciphertexts: in = count slots (host, stride words each); buf =
+ * NULL queries *len; else *len is the capacity in, the size written out.
+ * she_deserialize_ciphertexts: *count = the batch's count; out (host, cap
+ * slots, padding zeroed) may be NULL to query.  A wrong magic or length is
+ * SHE_ERR_SHAPE, another n SHE_ERR_PARAMS. */
+size_t she_serialized_bytes(const she_params* p, size_t count);
+she_status she_serialize_ciphertexts(const she_params* p, const uint32_t* in, size_t count,
+                                     void* buf, size_t* len);
+she_status she_deserialize_ciphertexts(const she_params* p, const void* buf, size_t len,
+                                       uint32_t* out, size_t cap, size_t* count);
+
 /* ---- client side on the GPU --------------------- */
 /* Host: the rounded-Gaussian noise words that fresh ciphertexts first_index ..
  * first_index + count - 1 draw (stream 8 of she_rng.h), i.e. exactly what

@@ -216,4 +216,58 @@ she_status she_decrypt_bits(const she_secret_key* sk, const uint32_t* in, size_t
   return SHE_OK;
 }
 
+// Wire format of a ciphertext batch (NEXT-4; the paper's MSize column,
+// PAPER.md:232, :256): 16-byte header {magic "SHEC", n, count (u64)} then
+// count x (n + 1) little-endian uint32 words (a[0..n-1], b) — the slot padding
+// is not sent.
+static const uint32_t kSerMagic = 0x43454853u;  // "SHEC"
+
+size_t she_serialized_bytes(const she_params* p, size_t count) {
+  return p ? 16 + count * (size_t)(p->n + 1) * 4 : 0;
+}
+
+she_status she_serialize_ciphertexts(const she_params* p, const uint32_t* in, size_t count,
+                                     void* buf, size_t* len) {
+  if (!p || !len) return fail(SHE_ERR_ARG, "NULL argument");
+  const size_t need = she_serialized_bytes(p, count);
+  if (!buf) {
+    *len = need;
+    return SHE_OK;
+  }
+  if (*len < need) return fail(SHE_ERR_ARG, "buffer of %zu bytes, need %zu", *len, need);
+  if (count && !in) return fail(SHE_ERR_ARG, "NULL input");
+  uint8_t* o = (uint8_t*)buf;
+  const uint32_t hdr[2] = {kSerMagic, p->n};
+  const uint64_t cnt = count;
+  memcpy(o, hdr, 8);
+  memcpy(o + 8, &cnt, 8);
+  const size_t stride = lwe_stride(*p), words = p->n + 1;
+  for (size_t c = 0; c < count; ++c) memcpy(o + 16 + c * words * 4, in + c * stride, words * 4);
+  *len = need;
+  return SHE_OK;
+}
+
+she_status she_deserialize_ciphertexts(const she_params* p, const void* buf, size_t len,
+                                       uint32_t* out, size_t cap, size_t* count) {
+  if (!p || !buf || !count) return fail(SHE_ERR_ARG, "NULL argument");
+  if (len < 16) return fail(SHE_ERR_SHAPE, "truncated header");
+  const uint8_t* b = (const uint8_t*)buf;
+  uint32_t hdr[2];
+  uint64_t cnt;
+  memcpy(hdr, b, 8);
+  memcpy(&cnt, b + 8, 8);
+  if (hdr[0] != kSerMagic) return fail(SHE_ERR_SHAPE, "not a ciphertext batch");
+  if (hdr[1] != p->n) return fail(SHE_ERR_PARAMS, "batch made for n = %u, params n = %u", hdr[1], p->n);
+  if (len != she_serialized_bytes(p, cnt)) return fail(SHE_ERR_SHAPE, "length does not match count");
+  *count = cnt;
+  if (!out) return SHE_OK;
+  if (cap < cnt) return fail(SHE_ERR_ARG, "capacity %zu < %llu", cap, (unsigned long long)cnt);
+  const size_t stride = lwe_stride(*p), words = p->n + 1;
+  for (size_t c = 0; c < cnt; ++c) {
+    memcpy(out + c * stride, b + 16 + c * words * 4, words * 4);
+    memset(out + c * stride + words, 0, (stride - words) * 4);
+  }
+  return SHE_OK;
+}
+
 }  // extern "C"

@@ -139,6 +139,10 @@ def lib() -> ctypes.CDLL:
             "she_maxpool2x2": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp, _vp], ctypes.c_int),
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_field_selftest": ([ctypes.c_int, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_serialized_bytes": ([P, _sz], _sz),
+            "she_serialize_ciphertexts": ([P, _vp, _sz, _vp, ctypes.POINTER(_sz)], ctypes.c_int),
+            "she_deserialize_ciphertexts": ([P, _vp, _sz, _vp, _sz, ctypes.POINTER(_sz)],
+                                            ctypes.c_int),
             "she_fft_product_selftest": ([ctypes.c_int, ctypes.c_int, _vp, _vp, _sz, _vp,
                                           ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
             "she_encrypt_noise": ([_vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
@@ -265,6 +269,30 @@ def she_decrypt_bits(sk: SecretKey, cts) -> np.ndarray:
     if len(bits):
         _check(lib().she_decrypt_bits(sk.handle, _np_ptr(cts2), cts2.shape[0], _np_ptr(bits)))
     return bits.reshape(cts.shape[:-1])
+
+
+def serialize(params, cts) -> bytes:
+    """Wire format of a ciphertext batch (she.h she_serialize_ciphertexts)."""
+    cts = np.ascontiguousarray(cts, dtype=np.uint32).reshape(-1, stride(params))
+    P = she_params.of(params)
+    n = _sz(0)
+    _check(lib().she_serialize_ciphertexts(ctypes.byref(P), None, cts.shape[0], None, ctypes.byref(n)))
+    buf = np.zeros(n.value, dtype=np.uint8)
+    _check(lib().she_serialize_ciphertexts(ctypes.byref(P), _np_ptr(cts), cts.shape[0], _np_ptr(buf),
+                                           ctypes.byref(n)))
+    return buf.tobytes()
+
+
+def deserialize(params, data: bytes) -> np.ndarray:
+    P = she_params.of(params)
+    buf = np.frombuffer(data, dtype=np.uint8).copy()
+    cnt = _sz(0)
+    _check(lib().she_deserialize_ciphertexts(ctypes.byref(P), _np_ptr(buf), buf.size, None, 0,
+                                             ctypes.byref(cnt)))
+    out = np.zeros((max(cnt.value, 1), stride(params)), dtype=np.uint32)
+    _check(lib().she_deserialize_ciphertexts(ctypes.byref(P), _np_ptr(buf), buf.size, _np_ptr(out),
+                                             cnt.value, ctypes.byref(cnt)))
+    return out[:cnt.value]
 
 
 # ---- server side -------------------------------------------------------------

@@ -216,3 +216,28 @@ def test_ctx_options_reserved_and_params_checked():
     st = she.lib().she_ctx_create_ex(ctypes.byref(she.she_params.of(big)), ck.handle, 0, 0, 1,
                                      None, ctypes.byref(h))
     assert st == -2  # n > 511: SHE_ERR_PARAMS (include/she.h she_params)
+
+
+@pytest.mark.parametrize("params", [si.C0, si.C1], ids=["C0", "C1"])
+def test_ciphertext_serialization_roundtrip_and_size(params):
+    """NEXT-4: the wire format carries n + 1 words per ciphertext (the paper's
+    MSize arithmetic: bits x ciphertext bytes), round-trips
+    bit for bit and is read by an independent parser (numpy) the same way."""
+    sk, _ = she.she_keygen(params, 77)
+    bits = np.random.default_rng(3).integers(0, 2, 100).astype(np.uint8)
+    cts = she.she_encrypt_bits(sk, bits, 5, 0)
+    data = she.serialize(params, cts)
+    assert len(data) == 16 + 100 * (params.n + 1) * 4
+    hdr = np.frombuffer(data[:8], dtype="<u4")
+    assert hdr[0] == 0x43454853 and hdr[1] == params.n
+    assert int(np.frombuffer(data[8:16], dtype="<u8")[0]) == 100
+    body = np.frombuffer(data[16:], dtype="<u4").reshape(100, params.n + 1)
+    assert np.array_equal(body, cts[:, : params.n + 1])
+    back = she.deserialize(params, data)
+    assert np.array_equal(back, cts)
+    assert np.array_equal(she.she_decrypt_bits(sk, back), bits)
+    with pytest.raises(she.SheError):
+        she.deserialize(params, data[:-4])
+    # the MNIST image of config 3: 784 pixels x 8 bit-wise ciphertexts
+    assert she.lib().she_serialized_bytes(ctypes.byref(she.she_params.of(si.C1)), 6272) == \
+        16 + 6272 * 501 * 4
