@@ -273,6 +273,50 @@ she_status she_gate_level(she_ctx* ctx, uint32_t* wires, const uint8_t* ops,
                           const uint32_t* in, const uint32_t* out_idx, size_t count,
                           void* stream);
 
+/* ---- leveled mode (reading R-LV) -------
+ * PAPER.md:188 evaluates its networks "in the LHE mode" with "all 3 levels of
+ * TFHE": here the client's bits are TRGSW selectors (the BK_i layout,
+ * uint32[2l][2][N]), the data are TRLWE (uint32[2][N], a bit = +-1/8 on the
+ * constant coefficient), and a gate is a CMux with no bootstrapping, so the
+ * noise grows by one external product per CMux on a data path (the depth
+ * budget).  Only client-supplied bits can select, which is why
+ * the leveled units below take client words.  The FFT engine (N = 1024) only. */
+typedef enum { SHE_LVL_ADD = 0, SHE_LVL_MAX = 1, SHE_LVL_RELU = 2 } she_lvl_op;
+/* Host, client: selectors q = first_index + idx as TRGSW_S(bits[idx]) (masks
+ * stream 9, noise stream 10 of she_rng.h with alpha_bk); out: count x
+ * [2l][2][N] uint32. */
+she_status she_lvl_encrypt_selectors(const she_secret_key* sk, const uint8_t* bits, size_t count,
+                                     uint64_t seed, uint64_t first_index, uint32_t* out);
+/* Host, client: bits of count TRLWE data ciphertexts ([2][N] each). */
+she_status she_lvl_decrypt(const she_secret_key* sk, const uint32_t* in, size_t count,
+                           uint8_t* bits);
+/* Bytes of one selector in the FFT domain (device layout of she_lvl_*). */
+size_t she_lvl_selector_bytes(void);
+/* Upload + transform count selectors (HOST [count][2l][2][N]) into `out`
+ * (DEVICE, count * she_lvl_selector_bytes(), caller-owned). */
+she_status she_lvl_selectors_to_device(she_ctx* ctx, const uint32_t* sel, size_t count,
+                                       void* out, void* stream);
+/* count CMuxes out[i] = d0[i] + sel[sel_idx[i]] [x] (d1[i] - d0[i]) (= sel ? d1 :
+ * d0); all DEVICE: sel from she_lvl_selectors_to_device, sel_idx uint32[count],
+ * d1, d0, out uint32[count][2][N] (out must not overlap d1, d0). */
+she_status she_lvl_cmux_batch(she_ctx* ctx, const void* sel, const uint32_t* sel_idx,
+                              const uint32_t* d1, const uint32_t* d0, uint32_t* out, size_t count,
+                              void* stream);
+/* Leveled units on client words (F2 circuits of the paper, PAPER.md:92, :110,
+ * and its adder) as CMux programs levelised on the host: x_sel / y_sel (HOST
+ * uint32[count][width]) give each bit's selector index, LSB first.
+ *   SHE_LVL_ADD   out = x + y mod 2^width (ripple carry: MAJ and XOR3 as CMux
+ *                 trees, 6 CMux per bit)
+ *   SHE_LVL_MAX   out = max(x, y) (signed when is_signed; the comparator's
+ *                 x < y flag is TRLWE data driving 3 CMux per output bit)
+ *   SHE_LVL_RELU  out = relu(x) of a signed word, width - 1 bits (y unused)
+ * out: DEVICE uint32[count][width or width - 1][2][N] TRLWE bits.
+ * *cmux_count / *depth (may be NULL): CMuxes run and CMux levels (the
+ * multiplicative depth of the unit).  Synchronous. */
+she_status she_lvl_unit(she_ctx* ctx, int op, const void* sel, const uint32_t* x_sel,
+                        const uint32_t* y_sel, size_t count, int width, int is_signed,
+                        uint32_t* out, uint64_t* cmux_count, uint32_t* depth, void* stream);
+
 /* ---- layer calls (§3; scheduled by the library) ------------------ */
 /* Each call builds the layer's gate circuit on the host from the PLAINTEXT
  * weights (shifts = rewiring, negations = literal flags, constants folded),

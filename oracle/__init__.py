@@ -58,6 +58,7 @@ def _cpu_has_avx512() -> bool:
 
 
 COMPILER_FLAGS = " ".join(CFLAGS)
+MU = 1 << 29  # +-1/8 on the 2^32 torus scale (R4)
 _lib = None
 
 
@@ -110,6 +111,11 @@ def _setup(L):
                            ctypes.c_size_t, _u32p]
     L.orc_gates.argtypes = [_pp, _u32p, _u32p, _u8p, _u32p, _u32p, _u32p, ctypes.c_size_t,
                             ctypes.c_size_t, _u32p, ctypes.c_int]
+    L.orc_lvl_encrypt_sel.argtypes = [_pp, _u8p, _u8p, ctypes.c_size_t, ctypes.c_uint64,
+                                      ctypes.c_uint64, _u32p]
+    L.orc_lvl_cmux.argtypes = [_pp, _u32p, _u32p, _u32p, _u32p]
+    L.orc_lvl_cmux_batch.argtypes = [_pp, _u32p, _u32p, _u32p, _u32p, ctypes.c_size_t, _u32p]
+    L.orc_lvl_decrypt.argtypes = [_pp, _u8p, _u32p, ctypes.c_size_t, _u8p]
 
 
 def _ptr(a: np.ndarray, t):
@@ -256,4 +262,59 @@ def gates(keys: Keys, ops, a, b, c, nthreads: int = 0) -> np.ndarray:
         lib().orc_gates(ctypes.byref(_p(P)), _ptr(keys.bk, _u32p), _ptr(keys.ksk, _u32p),
                         _ptr(ops, _u8p), _ptr(a, _u32p), _ptr(b, _u32p), _ptr(c, _u32p),
                         count, stride, _ptr(out, _u32p), nthreads)
+    return out
+
+
+# ---- leveled mode (NEXT-2; reading R-LV) ------------------------------
+
+def lvl_encrypt_sel(params, S, bits, seed: int, first: int = 0) -> np.ndarray:
+    """Selectors TRGSW_S(bit): uint32 [count][2l][2][N] (streams 9, 10)."""
+    bits = np.ascontiguousarray(bits, dtype=np.uint8).ravel()
+    S = np.ascontiguousarray(S, dtype=np.uint8)
+    out = np.zeros((len(bits), 2 * params.l, 2, params.N), dtype=np.uint32)
+    if len(bits):
+        lib().orc_lvl_encrypt_sel(ctypes.byref(_p(params)), _ptr(S, _u8p), _ptr(bits, _u8p),
+                                  len(bits), seed, first, _ptr(out, _u32p))
+    return out
+
+
+def lvl_cmux(params, sel, d1, d0) -> np.ndarray:
+    """CMux(sel, d1, d0) = d0 + sel [x] (d1 - d0) on TRLWE data [2][N]."""
+    sel = np.ascontiguousarray(sel, dtype=np.uint32)
+    d1 = np.ascontiguousarray(d1, dtype=np.uint32)
+    d0 = np.ascontiguousarray(d0, dtype=np.uint32)
+    out = np.zeros((2, params.N), dtype=np.uint32)
+    lib().orc_lvl_cmux(ctypes.byref(_p(params)), _ptr(sel, _u32p), _ptr(d1, _u32p),
+                       _ptr(d0, _u32p), _ptr(out, _u32p))
+    return out
+
+
+def lvl_cmux_batch(params, sels, sel_idx, d1, d0) -> np.ndarray:
+    sels = np.ascontiguousarray(sels, dtype=np.uint32)
+    sel_idx = np.ascontiguousarray(sel_idx, dtype=np.uint32)
+    d1 = np.ascontiguousarray(d1, dtype=np.uint32)
+    d0 = np.ascontiguousarray(d0, dtype=np.uint32)
+    out = np.zeros_like(d1)
+    if len(sel_idx):
+        lib().orc_lvl_cmux_batch(ctypes.byref(_p(params)), _ptr(sels, _u32p), _ptr(sel_idx, _u32p),
+                                 _ptr(d1, _u32p), _ptr(d0, _u32p), len(sel_idx), _ptr(out, _u32p))
+    return out
+
+
+def lvl_decrypt(params, S, cts) -> np.ndarray:
+    cts = np.ascontiguousarray(cts, dtype=np.uint32)
+    S = np.ascontiguousarray(S, dtype=np.uint8)
+    c2 = cts.reshape(-1, 2 * params.N)
+    bits = np.zeros(c2.shape[0], dtype=np.uint8)
+    if len(bits):
+        lib().orc_lvl_decrypt(ctypes.byref(_p(params)), _ptr(S, _u8p), _ptr(c2, _u32p), len(bits),
+                              _ptr(bits, _u8p))
+    return bits.reshape(cts.shape[:-2])
+
+
+def lvl_trivial(params, bits) -> np.ndarray:
+    """Noiseless TRLWE data (A = 0, B = +-1/8 on the constant coefficient)."""
+    bits = np.asarray(bits, dtype=np.uint8).ravel()
+    out = np.zeros((len(bits), 2, params.N), dtype=np.uint32)
+    out[:, 1, 0] = np.where(bits == 1, MU, (1 << 32) - MU).astype(np.uint32)
     return out

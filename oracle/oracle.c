@@ -346,3 +346,84 @@ void orc_gates(const orc_params* P, const uint32_t* bk, const uint32_t* ksk, con
     orc_gate(P, bk, ksk, ops[g], a + g * stride, b + g * stride, c + g * stride, stride,
              out + g * stride);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Leveled mode (reading R-LV)              */
+/* PAPER.md:188 "We used all 3 levels of TFHE in the LHE mode": selector bits */
+/* as TRGSW (the top level), data as TRLWE (level 1), gates as CMux without   */
+/* bootstrapping.                                                             */
+/* ------------------------------------------------------------------------ */
+
+/* Selector q = TRGSW_S(bit) in the BK row layout (R2): row r = c*l + j is a
+ * TRLWE encryption of 0 under S (A from stream 9, B = A*S + e, e from stream
+ * 10 with alpha_bk) plus bit * 2^{32-(j+1)bg} on component c's constant
+ * coefficient.  out: count x [2l][2][N]; selector idx draws number first+idx. */
+void orc_lvl_encrypt_sel(const orc_params* P, const uint8_t* S, const uint8_t* bits, size_t count,
+                         uint64_t seed, uint64_t first, uint32_t* out) {
+  const uint32_t N = P->N, l = P->l;
+  int32_t* Sd = (int32_t*)malloc(sizeof(int32_t) * N);
+  for (uint32_t j = 0; j < N; j++) Sd[j] = S[j];
+#pragma omp parallel for schedule(dynamic)
+  for (long q = 0; q < (long)count; q++) {
+    const uint64_t qq = first + (uint64_t)q;
+    for (uint32_t r = 0; r < 2 * l; r++) {
+      uint32_t* A = out + (((size_t)q * 2 * l + r) * 2 + 0) * N;
+      uint32_t* B = A + N;
+      for (uint32_t m = 0; m < N; m++)
+        A[m] = she_rng_u32(seed, SHE_STREAM_LVL_MASK, she_idx_bk(N, l, (uint32_t)qq, r, m));
+      orc_negacyclic_mul(N, Sd, A, B); /* B = S * A */
+      for (uint32_t m = 0; m < N; m++)
+        B[m] += she_rng_gauss32(seed, SHE_STREAM_LVL_NOISE, she_idx_bk(N, l, (uint32_t)qq, r, m),
+                                P->alpha_bk);
+      const uint32_t c = r / l, j = r % l;
+      if (bits[q]) (c == 0 ? A : B)[0] += 1u << (32 - (j + 1) * P->bg_bits);
+    }
+  }
+  free(Sd);
+}
+
+/* CMux(sel, d1, d0) = d0 + sel [x] (d1 - d0) on TRLWE data (A then B, 2N
+ * words each): the external product of the CMux step of orc_blind_rotate
+ * (rows r = (c, j): digit_j(D_c) * sel[r], signed gadget decomposition R8,
+ * schoolbook negacyclic products) with D = d1 - d0 in place of X^a ACC - ACC. */
+void orc_lvl_cmux(const orc_params* P, const uint32_t* sel, const uint32_t* d1, const uint32_t* d0,
+                  uint32_t* out) {
+  const uint32_t N = P->N, l = P->l;
+  int32_t* dig = (int32_t*)malloc(sizeof(int32_t) * 2 * l * N);
+  int32_t* tmp = (int32_t*)malloc(sizeof(int32_t) * l);
+  uint32_t* acc = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+  for (uint32_t comp = 0; comp < 2; comp++)
+    for (uint32_t m = 0; m < N; m++) {
+      orc_decompose(P, d1[comp * N + m] - d0[comp * N + m], tmp);
+      for (uint32_t j = 0; j < l; j++) dig[(comp * l + j) * N + m] = tmp[j];
+    }
+  memcpy(acc, d0, sizeof(uint32_t) * 2 * N);
+  for (uint32_t r = 0; r < 2 * l; r++)
+    for (uint32_t o = 0; o < 2; o++)
+      negacyclic_mac(N, dig + (size_t)r * N, sel + ((size_t)r * 2 + o) * N, acc + o * N);
+  memcpy(out, acc, sizeof(uint32_t) * 2 * N);
+  free(dig); free(tmp); free(acc);
+}
+
+/* A batch of CMuxes (threaded): item i = CMux(sels[sel_idx[i]], d1[i], d0[i]). */
+void orc_lvl_cmux_batch(const orc_params* P, const uint32_t* sels, const uint32_t* sel_idx,
+                        const uint32_t* d1, const uint32_t* d0, size_t count, uint32_t* out) {
+  const size_t T = (size_t)2 * P->N, R = (size_t)2 * P->l * 2 * P->N;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long i = 0; i < (long)count; i++)
+    orc_lvl_cmux(P, sels + sel_idx[i] * R, d1 + i * T, d0 + i * T, out + i * T);
+}
+
+/* Bit of TRLWE data (R5 on the constant coefficient): phase_0 = B_0 - (A S)_0. */
+void orc_lvl_decrypt(const orc_params* P, const uint8_t* S, const uint32_t* in, size_t count,
+                     uint8_t* bits) {
+  const uint32_t N = P->N;
+  for (size_t c = 0; c < count; c++) {
+    const uint32_t* A = in + c * 2 * N;
+    uint32_t ph = A[N];  /* B_0 */
+    /* (A S)_0 = A_0 S_0 - sum_{m >= 1} A_m S_{N-m} (negacyclic) */
+    ph -= A[0] * (uint32_t)S[0];
+    for (uint32_t m = 1; m < N; m++) ph += A[m] * (uint32_t)S[N - m];
+    bits[c] = (int32_t)ph >= 0;
+  }
+}

@@ -216,6 +216,56 @@ she_status she_decrypt_bits(const she_secret_key* sk, const uint32_t* in, size_t
   return SHE_OK;
 }
 
+// ---- leveled mode, client side (NEXT-2; reading R-LV) ----------
+// Selector number first + idx = TRGSW_S(bit) in the BK row layout: row r =
+// c*l + j is TRLWE_S(0) (A from stream 9, B = A*S + e with e from stream 10,
+// alpha_bk) plus bit * g_j on component c's constant coefficient (R1, R2).
+// out: count x [2l][2][N] (host).
+she_status she_lvl_encrypt_selectors(const she_secret_key* sk, const uint8_t* bits, size_t count,
+                                     uint64_t seed, uint64_t first_index, uint32_t* out) {
+  if (count == 0) return SHE_OK;
+  if (!sk || !bits || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  const she_params& p = sk->p;
+  const uint32_t N = p.N, l = p.l;
+  std::vector<uint32_t> ones;
+  for (uint32_t j = 0; j < N; ++j)
+    if (sk->S[j]) ones.push_back(j);
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t qr = 0; qr < (int64_t)count * 2 * l; ++qr) {
+    const size_t idx = (size_t)(qr / (2 * l));
+    const uint32_t q = (uint32_t)(first_index + idx), r = (uint32_t)(qr % (2 * l));
+    uint32_t* A = out + ((size_t)qr * 2 + 0) * N;
+    uint32_t* B = out + ((size_t)qr * 2 + 1) * N;
+    for (uint32_t m = 0; m < N; ++m) {
+      A[m] = she_rng_u32(seed, SHE_STREAM_LVL_MASK, she_idx_bk(N, l, q, r, m));
+      B[m] = she_rng_gauss32(seed, SHE_STREAM_LVL_NOISE, she_idx_bk(N, l, q, r, m), p.alpha_bk);
+    }
+    for (uint32_t j : ones) add_rotated(N, j, A, B);  // B = A*S + e
+    if (bits[idx]) {
+      const uint32_t c = r / l, j = r % l;
+      (c == 0 ? A : B)[0] += 1u << (32 - (j + 1) * p.bg_bits);
+    }
+  }
+  return SHE_OK;
+}
+
+// Bit of leveled data (TRLWE [2][N], host): R5 on the constant coefficient of
+// the phase B - A*S, i.e. B_0 - A_0 S_0 + sum_{m>=1} A_m S_{N-m}.
+she_status she_lvl_decrypt(const she_secret_key* sk, const uint32_t* in, size_t count,
+                           uint8_t* bits) {
+  if (count == 0) return SHE_OK;
+  if (!sk || !in || !bits) return fail(SHE_ERR_ARG, "NULL argument");
+  const uint32_t N = sk->p.N;
+  for (size_t c = 0; c < count; ++c) {
+    const uint32_t* A = in + c * 2 * N;
+    uint32_t ph = A[N] - (sk->S[0] ? A[0] : 0u);
+    for (uint32_t m = 1; m < N; ++m)
+      if (sk->S[N - m]) ph += A[m];
+    bits[c] = (int32_t)ph >= 0 ? 1 : 0;
+  }
+  return SHE_OK;
+}
+
 // Wire format of a ciphertext batch (NEXT-4; the paper's MSize column,
 // PAPER.md:232, :256): 16-byte header {magic "SHEC", n, count (u64)} then
 // count x (n + 1) little-endian uint32 words (a[0..n-1], b) — the slot padding

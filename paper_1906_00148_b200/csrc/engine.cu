@@ -645,6 +645,105 @@ __global__ void __launch_bounds__(128) fft_selftest_kernel(const int32_t* digits
   for (int m = tid; m < 2 * N; m += 128) out[c * 2 * N + m] = acc[m];
 }
 
+// ---------------------------------------------------------------------------
+// Leveled mode (reading R-LV): a CMux
+//   out = d0 + sel [x] (d1 - d0)
+// with sel a client TRGSW in the FFT domain ([16][512], the BK_i layout made by
+// bk_fft_kernel) and d1, d0, out TRLWE data ([2][N]) — the external product
+// of the CMux step of the blind rotation without the rotation, on the same
+// device functions (exact).  One CTA of 4 warps per CMux:
+// warp w decomposes component c = w / l at digit level j = w % l (R8).
+// Array mode: sel_idx[i], d1 + i, d0 + i, out + i.  Program mode: prog[4 i ..]
+// = (selector, in1 literal, in0 literal, out slot) on a wire table of TRLWE
+// slots, a literal's bit 31 negating the slot (NOT of +-1/8 data).
+struct LvlSrc {
+  const double2* sel;
+  const uint32_t* sel_idx;
+  const uint32_t* d1;
+  const uint32_t* d0;
+  uint32_t* out;
+  uint32_t* wires;
+  const uint32_t* prog;
+  uint32_t count;
+};
+
+template <int V>
+__global__ void __launch_bounds__(128) lvl_cmux_kernel(LvlSrc s, br::Geometry geo) {
+  constexpr int N = fft::kN, M = fft::kM;
+  extern __shared__ __align__(16) uint8_t smem[];
+  double2* rows = reinterpret_cast<double2*>(smem);
+  double2* tw = rows + 4 * fft::kRow;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(tw + 2 * 512);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t item = blockIdx.x;
+  uint32_t sidx, l1, l0;
+  const uint32_t *p1, *p0;
+  uint32_t* po;
+  if (s.prog) {
+    const uint32_t* pr = s.prog + 4 * (size_t)item;
+    sidx = pr[0];
+    l1 = pr[1];
+    l0 = pr[2];
+    p1 = s.wires + (size_t)(l1 & 0x7FFFFFFFu) * 2 * N;
+    p0 = s.wires + (size_t)(l0 & 0x7FFFFFFFu) * 2 * N;
+    po = s.wires + (size_t)pr[3] * 2 * N;
+  } else {
+    sidx = s.sel_idx[item];
+    l1 = l0 = 0;
+    p1 = s.d1 + (size_t)item * 2 * N;
+    p0 = s.d0 + (size_t)item * 2 * N;
+    po = s.out + (size_t)item * 2 * N;
+  }
+  const uint32_t n1 = (l1 >> 31) ? 0u - 1u : 1u, n0 = (l0 >> 31) ? 0u - 1u : 1u;  // +-1
+  FftVar<V>::tables(tid, 128, tw, tw + FftVar<V>::kTab);
+  for (int m = tid; m < 2 * N; m += 128) acc[m] = n0 * p0[m];
+  {  // digits of D_c = d1 - d0, level j (R8)
+    const int c = w / (int)geo.l, j = w % (int)geo.l;
+    const uint32_t shift = 32 - (j + 1) * geo.bg_bits;
+    const uint32_t mask = (1u << geo.bg_bits) - 1, half = 1u << (geo.bg_bits - 1);
+    int32_t d[32];
+#pragma unroll
+    for (int j2 = 0; j2 < 32; ++j2) {
+      const int m = c * N + lane + 32 * j2;
+      const uint32_t y = n1 * p1[m] - n0 * p0[m] + geo.dec_offset;
+      d[j2] = (int32_t)((y >> shift) & mask) - (int32_t)half;
+    }
+    fbr_forward_digits<V>(d, lane, tw, rows + w * fft::kRow);
+  }
+  __syncthreads();
+  const double2* sel = s.sel + (size_t)sidx * 16 * M;
+  for (int k = tid; k < M; k += 128) {
+    double2 b[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) b[q] = __ldg(sel + (size_t)q * M + k);
+    fbr_pointwise(rows, k, b);
+  }
+  __syncthreads();
+  fbr_inverse_acc<V, false>(rows + w * fft::kRow, lane, tw + FftVar<V>::kTab, acc + (w >> 1) * N, w,
+                            nullptr);
+  __syncthreads();
+  for (int m = tid; m < 2 * N; m += 128) po[m] = acc[m];
+}
+
+// Trivial TRLWE data of the leveled wire table: slot 0 = TRUE (0, +1/8),
+// slot 1 = FALSE (0, -1/8) on the constant coefficient.
+__global__ void lvl_const_kernel(uint32_t* wires, uint32_t N) {
+  for (uint32_t m = threadIdx.x; m < 4 * N; m += blockDim.x) {
+    const uint32_t slot = m / (2 * N), k = m % (2 * N);
+    wires[m] = k == N ? (slot == 0 ? kMu : 0u - kMu) : 0u;
+  }
+}
+
+// out[i] = wires[lits[i] & 0x7fffffff] (negated when bit 31 is set), TRLWE slots.
+__global__ void lvl_gather_kernel(uint32_t* out, const uint32_t* wires, const uint32_t* lits,
+                                  uint32_t N) {
+  const uint32_t lit = lits[blockIdx.x];
+  const uint32_t* src = wires + (size_t)(lit & 0x7FFFFFFFu) * 2 * N;
+  const uint32_t sg = (lit >> 31) ? 0u - 1u : 1u;
+  for (uint32_t m = threadIdx.x; m < 2 * N; m += blockDim.x)
+    out[(size_t)blockIdx.x * 2 * N + m] = sg * src[m];
+}
+
 // Compact lane list of a gate batch: gate g contributes lane (g, 0) if it is
 // bootstrapped and (g, 1) too if it is a MUX.  One CTA, block-wide scan.
 __global__ void lane_list_kernel(GateSrc src, uint32_t* lanes, uint32_t* nlanes) {
@@ -1127,6 +1226,11 @@ struct she_ctx {
   int32_t* ksi_c = nullptr;    // [ksi_cap][stride * 4] products
   uint32_t* ksi_bp = nullptr;  // [ksi_cap] b'
   size_t ksi_cap = 0;
+  // leveled mode scratch (she_lvl_*): TRLWE wire table + program staging
+  uint32_t* lvl_wires = nullptr;
+  size_t lvl_slots = 0;
+  uint32_t* lvl_prog = nullptr;
+  size_t lvl_prog_cap = 0;
   // staging for the host-buffer API
   uint8_t* h_ops = nullptr;
   uint32_t* h_io = nullptr;
@@ -1647,6 +1751,8 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaFree(ctx->ksi_a);
   cudaFree(ctx->ksi_c);
   cudaFree(ctx->ksi_bp);
+  cudaFree(ctx->lvl_wires);
+  cudaFree(ctx->lvl_prog);
   cudaFree(ctx->tw);
   cudaFree(ctx->itw);
   cudaFree(ctx->ext);
@@ -2039,6 +2145,172 @@ she_status she_gate_level(she_ctx* ctx, uint32_t* wires, const uint8_t* ops, con
   s.stride = ctx->stride;
   s.count = (uint32_t)count;
   return dispatch(ctx, s, (cudaStream_t)stream);
+}
+
+// ---- leveled mode (NEXT-2; reading R-LV) --------------------------
+
+size_t she_lvl_selector_bytes(void) { return (size_t)16 * fft::kM * sizeof(double2); }
+
+she_status she_lvl_selectors_to_device(she_ctx* ctx, const uint32_t* sel, size_t count,
+                                       void* out, void* stream) {
+  if (count == 0) return SHE_OK;
+  if (!ctx || !sel || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  if (!ctx->bkf) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t words = count * 2 * ctx->p.l * 2 * ctx->p.N;
+  uint32_t* d = nullptr;
+  CK(cudaMallocAsync(&d, words * 4, st));
+  CK(cudaMemcpyAsync(d, sel, words * 4, cudaMemcpyHostToDevice, st));
+  const uint32_t polys = (uint32_t)(count * 8);
+  if (ctx->fft_v == 1) bk_fft_kernel<1><<<2 * polys, 32, 0, st>>>(d, (double2*)out, polys);
+  else if (ctx->fft_v == 3) bk_fft_kernel<3><<<2 * polys, 32, 0, st>>>(d, (double2*)out, polys);
+  else bk_fft_kernel<2><<<2 * polys, 32, 0, st>>>(d, (double2*)out, polys);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(d, st));
+  return SHE_OK;
+}
+
+static constexpr size_t kLvlSmem = (4 * fft::kRow + 2 * 512) * sizeof(double2) + 2 * fft::kN * 4;
+
+static she_status lvl_launch(she_ctx* ctx, const LvlSrc& s, cudaStream_t st) {
+  auto k = ctx->fft_v == 1 ? lvl_cmux_kernel<1> : ctx->fft_v == 3 ? lvl_cmux_kernel<3>
+                                                                  : lvl_cmux_kernel<2>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLvlSmem));
+  k<<<s.count, 128, kLvlSmem, st>>>(s, ctx->geo);
+  CK(cudaGetLastError());
+  return SHE_OK;
+}
+
+she_status she_lvl_cmux_batch(she_ctx* ctx, const void* sel, const uint32_t* sel_idx,
+                              const uint32_t* d1, const uint32_t* d0, uint32_t* out, size_t count,
+                              void* stream) {
+  if (count == 0) return SHE_OK;
+  if (!ctx || !sel || !sel_idx || !d1 || !d0 || !out) return fail(SHE_ERR_ARG, "NULL argument");
+  if (!ctx->bkf) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
+  if (count > 0x7FFFFFFFull) return fail(SHE_ERR_ARG, "count too large");
+  const size_t bytes = count * 2 * ctx->p.N * 4;
+  if (overlaps(out, bytes, d1, bytes) || overlaps(out, bytes, d0, bytes))
+    return fail(SHE_ERR_ARG, "out overlaps an input");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  LvlSrc s = {};
+  s.sel = (const double2*)sel;
+  s.sel_idx = sel_idx;
+  s.d1 = d1;
+  s.d0 = d0;
+  s.out = out;
+  s.count = (uint32_t)count;
+  return lvl_launch(ctx, s, (cudaStream_t)stream);
+}
+
+she_status she_lvl_unit(she_ctx* ctx, int op, const void* sel, const uint32_t* x_sel,
+                        const uint32_t* y_sel, size_t count, int width, int is_signed,
+                        uint32_t* out, uint64_t* cmux_count, uint32_t* depth, void* stream) {
+  if (op < SHE_LVL_ADD || op > SHE_LVL_RELU) return fail(SHE_ERR_ARG, "bad leveled op %d", op);
+  if (width < 2 || width > 32) return fail(SHE_ERR_ARG, "width %d", width);
+  if (count == 0) return SHE_OK;
+  if (!ctx || !sel || !x_sel || !out || (op != SHE_LVL_RELU && !y_sel))
+    return fail(SHE_ERR_ARG, "NULL argument");
+  if (!ctx->bkf) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
+  // ---- the CMux program (host): slots 0 = TRUE, 1 = FALSE; lit bit 31 = NOT
+  constexpr uint32_t T = 0, F = 1, NEG = 0x80000000u;
+  struct Item { uint32_t sel, in1, in0, out; };
+  std::vector<std::vector<Item>> levels;
+  std::vector<uint32_t> lvl_of(2, 0);  // level at which a slot is ready
+  uint32_t next = 2;
+  auto cmux = [&](uint32_t s, uint32_t in1, uint32_t in0) {
+    const uint32_t L = std::max(lvl_of[in1 & ~NEG], lvl_of[in0 & ~NEG]);
+    if (levels.size() <= L) levels.resize(L + 1);
+    const uint32_t o = next++;
+    levels[L].push_back({s, in1, in0, o});
+    lvl_of.push_back(L + 1);
+    return o;
+  };
+  const int wout = op == SHE_LVL_RELU ? width - 1 : width;
+  std::vector<uint32_t> results;  // count x wout literals
+  results.reserve(count * wout);
+  for (size_t q = 0; q < count; ++q) {
+    const uint32_t* xs = x_sel + q * width;
+    const uint32_t* ys = y_sel ? y_sel + q * width : nullptr;
+    if (op == SHE_LVL_ADD) {  // ripple carry: MAJ and XOR3 by CMux trees, 6 per bit
+      uint32_t c = F;
+      for (int j = 0; j < width; ++j) {
+        const uint32_t u1 = cmux(ys[j], c, c | NEG), u0 = cmux(ys[j], c | NEG, c);
+        results.push_back(cmux(xs[j], u1, u0));  // x ^ y ^ c
+        if (j + 1 < width) {
+          const uint32_t t1 = cmux(ys[j], T, c), t0 = cmux(ys[j], c, F);
+          c = cmux(xs[j], t1, t0);  // MAJ(x, y, c)
+        }
+      }
+    } else if (op == SHE_LVL_MAX) {  // lt = [x < y] LSB -> MSB, then z_i = lt ? y_i : x_i
+      uint32_t lt = F;
+      for (int j = 0; j < width; ++j) {
+        const bool msb = is_signed && j == width - 1;  // signed MSB: x = 1 (negative) is smaller
+        const uint32_t a1 = cmux(ys[j], lt, msb ? T : F), a0 = cmux(ys[j], msb ? F : T, lt);
+        lt = cmux(xs[j], a1, a0);
+      }
+      for (int i = 0; i < width; ++i) {
+        const uint32_t b1 = cmux(ys[i], T, lt | NEG), b0 = cmux(ys[i], lt, F);
+        results.push_back(cmux(xs[i], b1, b0));
+      }
+    } else {  // ReLU: R_i = x_i AND NOT sign
+      const uint32_t ns = cmux(xs[width - 1], F, T);
+      for (int i = 0; i < wout; ++i) results.push_back(cmux(xs[i], ns, F));
+    }
+  }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t N = ctx->p.N, slots = next;
+  if (ctx->lvl_slots < slots) {
+    CK(cudaStreamSynchronize(st));
+    cudaFree(ctx->lvl_wires);
+    ctx->lvl_wires = nullptr;
+    ctx->lvl_slots = 0;
+    CK(cudaMalloc(&ctx->lvl_wires, slots * 2 * N * 4));
+    ctx->lvl_slots = slots;
+  }
+  size_t items = 0;
+  for (auto& L : levels) items += L.size();
+  const size_t prog_words = 4 * items + results.size();
+  if (ctx->lvl_prog_cap < prog_words) {
+    CK(cudaStreamSynchronize(st));
+    cudaFree(ctx->lvl_prog);
+    ctx->lvl_prog = nullptr;
+    ctx->lvl_prog_cap = 0;
+    CK(cudaMalloc(&ctx->lvl_prog, prog_words * 4));
+    ctx->lvl_prog_cap = prog_words;
+  }
+  std::vector<uint32_t> h;
+  h.reserve(prog_words);
+  std::vector<size_t> first;
+  for (auto& L : levels) {
+    first.push_back(h.size() / 4);
+    for (const Item& it : L) h.insert(h.end(), {it.sel, it.in1, it.in0, it.out});
+  }
+  const size_t res_off = h.size();
+  h.insert(h.end(), results.begin(), results.end());
+  CK(cudaMemcpyAsync(ctx->lvl_prog, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
+  lvl_const_kernel<<<1, 256, 0, st>>>(ctx->lvl_wires, (uint32_t)N);
+  CK(cudaGetLastError());
+  for (size_t L = 0; L < levels.size(); ++L) {
+    LvlSrc s = {};
+    s.sel = (const double2*)sel;
+    s.wires = ctx->lvl_wires;
+    s.prog = ctx->lvl_prog + 4 * first[L];
+    s.count = (uint32_t)levels[L].size();
+    she_status r = lvl_launch(ctx, s, st);
+    if (r != SHE_OK) return r;
+  }
+  lvl_gather_kernel<<<(unsigned)results.size(), 256, 0, st>>>(out, ctx->lvl_wires,
+                                                              ctx->lvl_prog + res_off, (uint32_t)N);
+  CK(cudaGetLastError());
+  if (cmux_count) *cmux_count = items;
+  if (depth) *depth = (uint32_t)levels.size();
+  CK(cudaStreamSynchronize(st));  // the host program buffer h is freed on return
+  return SHE_OK;
 }
 
 }  // extern "C"

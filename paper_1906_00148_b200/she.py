@@ -140,6 +140,15 @@ def lib() -> ctypes.CDLL:
             "she_ctx_layer_stats": ([_vp, ctypes.POINTER(she_circuit_stats)], ctypes.c_int),
             "she_field_selftest": ([ctypes.c_int, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
             "she_serialized_bytes": ([P, _sz], _sz),
+            "she_lvl_encrypt_selectors": ([_vp, _vp, _sz, ctypes.c_uint64, ctypes.c_uint64, _vp],
+                                          ctypes.c_int),
+            "she_lvl_decrypt": ([_vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_lvl_selector_bytes": ([], _sz),
+            "she_lvl_selectors_to_device": ([_vp, _vp, _sz, _vp, _vp], ctypes.c_int),
+            "she_lvl_cmux_batch": ([_vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
+            "she_lvl_unit": ([_vp, ctypes.c_int, _vp, _vp, _vp, _sz, ctypes.c_int, ctypes.c_int, _vp,
+                              ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), _vp],
+                             ctypes.c_int),
             "she_serialize_ciphertexts": ([P, _vp, _sz, _vp, ctypes.POINTER(_sz)], ctypes.c_int),
             "she_deserialize_ciphertexts": ([P, _vp, _sz, _vp, _sz, ctypes.POINTER(_sz)],
                                             ctypes.c_int),
@@ -706,3 +715,71 @@ def she_decrypt_bits_gpu(sk: SecretKey, cts, out=None, stream=None):
     _check(lib().she_decrypt_bits_gpu(sk.handle, _dev_ptr(cts), count, _dev_ptr(out),
                                       cts.device.index or 0, _stream_ptr(stream)))
     return out
+
+
+# ---- leveled mode (she.h she_lvl_*; NEXT-2, reading R-LV) ----------
+
+SHE_LVL_ADD, SHE_LVL_MAX, SHE_LVL_RELU = 0, 1, 2
+
+
+def lvl_encrypt_selectors(sk: SecretKey, bits, seed: int, first_index: int = 0) -> np.ndarray:
+    """Client: bits -> TRGSW selectors, uint32 [count][2l][2][N] (host)."""
+    P = sk.params
+    bits = np.ascontiguousarray(bits, dtype=np.uint8).ravel()
+    out = np.zeros((len(bits), 2 * P.l, 2, P.N), dtype=np.uint32)
+    if len(bits):
+        _check(lib().she_lvl_encrypt_selectors(sk.handle, _np_ptr(bits), len(bits), seed,
+                                               first_index, _np_ptr(out)))
+    return out
+
+
+def lvl_decrypt(sk: SecretKey, cts) -> np.ndarray:
+    """Client: TRLWE data [..][2][N] (host) -> bits."""
+    P = sk.params
+    cts = np.ascontiguousarray(cts, dtype=np.uint32)
+    flat = cts.reshape(-1, 2 * P.N)
+    bits = np.zeros(flat.shape[0], dtype=np.uint8)
+    if len(bits):
+        _check(lib().she_lvl_decrypt(sk.handle, _np_ptr(flat), len(bits), _np_ptr(bits)))
+    return bits.reshape(cts.shape[:-2])
+
+
+def lvl_selectors_to_device(ctx: Context, sel: np.ndarray, stream=None):
+    """Upload + FFT-transform selectors; returns the device buffer (torch uint8)."""
+    import torch
+    sel = np.ascontiguousarray(sel, dtype=np.uint32)
+    count = sel.shape[0]
+    out = torch.empty(max(count, 1) * int(lib().she_lvl_selector_bytes()), dtype=torch.uint8,
+                      device=f"cuda:{ctx.device}")
+    _check(lib().she_lvl_selectors_to_device(ctx.handle, _np_ptr(sel), count, _dev_ptr(out),
+                                             _stream_ptr(stream)))
+    return out
+
+
+def lvl_cmux_batch(ctx: Context, sel_dev, sel_idx, d1, d0, out=None, stream=None):
+    """out[i] = sel[sel_idx[i]] ? d1[i] : d0[i] (device int32 [count][2][N])."""
+    import torch
+    if out is None:
+        out = torch.empty_like(d1)
+    _check(lib().she_lvl_cmux_batch(ctx.handle, _dev_ptr(sel_dev), _dev_ptr(sel_idx), _dev_ptr(d1),
+                                    _dev_ptr(d0), _dev_ptr(out), sel_idx.numel(),
+                                    _stream_ptr(stream)))
+    return out
+
+
+def lvl_unit(ctx: Context, op: int, sel_dev, x_sel, y_sel, width: int, signed: bool, stream=None):
+    """Leveled ADD / MAX / RELU on client words; returns (out device int32
+    [count][w_out][2][N], cmux_count, depth)."""
+    import torch
+    x_sel = np.ascontiguousarray(x_sel, dtype=np.uint32)
+    count = x_sel.shape[0]
+    y_sel = None if y_sel is None else np.ascontiguousarray(y_sel, dtype=np.uint32)
+    wout = width - 1 if op == SHE_LVL_RELU else width
+    N = ctx.params.N
+    out = torch.zeros((count, wout, 2, N), dtype=torch.int32, device=f"cuda:{ctx.device}")
+    n_cmux, depth = ctypes.c_uint64(0), ctypes.c_uint32(0)
+    _check(lib().she_lvl_unit(ctx.handle, op, _dev_ptr(sel_dev), _np_ptr(x_sel),
+                              None if y_sel is None else _np_ptr(y_sel), count, width, int(signed),
+                              _dev_ptr(out), ctypes.byref(n_cmux), ctypes.byref(depth),
+                              _stream_ptr(stream)))
+    return out, int(n_cmux.value), int(depth.value)

@@ -46,7 +46,9 @@ enum {
   SHE_STREAM_KSK_MASK = 5,  /* a of KSK entries     (u32)                      */
   SHE_STREAM_KSK_NOISE = 6, /* e of KSK entries     (gaussian, a_lwe)          */
   SHE_STREAM_ENC_MASK = 7,  /* a of fresh ciphertexts                          */
-  SHE_STREAM_ENC_NOISE = 8  /* e of fresh ciphertexts                          */
+  SHE_STREAM_ENC_NOISE = 8, /* e of fresh ciphertexts                          */
+  SHE_STREAM_LVL_MASK = 9,  /* A coeffs of leveled selectors (TRGSW rows, u32)  */
+  SHE_STREAM_LVL_NOISE = 10 /* e coeffs of leveled selectors (gaussian, a_bk)   */
 };
 
 SHE_RNG_FN uint64_t she_mix64(uint64_t z) {
@@ -96,6 +98,9 @@ SHE_RNG_FN uint64_t she_idx_ksk_entry(uint32_t t, uint32_t base, uint32_t i, uin
 SHE_RNG_FN uint64_t she_idx_ksk_mask(uint32_t n, uint64_t entry, uint32_t k) {
   return entry * n + k;
 }
+/* Leveled selector number q (a TRGSW, DESIGN.md R-LV): row r, coefficient m
+ * numbered as BK row r of TRGSW q: she_idx_bk(N, l, q, r, m). */
+
 /* Fresh ciphertext number q (global ordinal), mask word k < n.  Noise index = q. */
 SHE_RNG_FN uint64_t she_idx_enc_mask(uint32_t n, uint64_t q, uint32_t k) {
   return q * n + k;
