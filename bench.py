@@ -409,6 +409,50 @@ def dshe_latency(ctx, sk, P, world: int, rank: int, H=28, ch=4, k=4):
             "logits": [int(v) for v in logits]}
 
 
+def leveled_units(ctx, sk, P, words=720, width=16):
+    """NEXT-2 leveled mode (reading R-LV): ADD, MAX and ReLU units on
+    `words` client word pairs of `width` bits (the 720 accumulators of config
+    2's conv layer), each a CMux program on TRGSW selectors with no
+    bootstrapping; device time per unit (CUDA events), CMuxes, depth, and the
+    decrypted outputs against the plaintext."""
+    import torch
+    from paper_1906_00148_b200 import she
+    rng = np.random.default_rng(si.input_seed(2) + 77)
+    lo, hi = -(1 << (width - 1)), 1 << (width - 1)
+    x, y = rng.integers(lo, hi, words), rng.integers(lo, hi, words)
+    bits = lambda v: ((v[:, None] >> np.arange(width)) & 1).astype(np.uint8)
+    t0 = time.perf_counter()
+    sel = she.lvl_encrypt_selectors(sk, np.concatenate([bits(x).ravel(), bits(y).ravel()]),
+                                    si.input_seed(2) + 78, 0)
+    t_enc = time.perf_counter() - t0
+    sel_dev = she.lvl_selectors_to_device(ctx, sel)
+    xs = np.arange(words * width, dtype=np.uint32).reshape(words, width)
+    ys = xs + words * width
+    res = {"workload": f"{words} client word pairs of {width} bits (config 2's conv outputs), "
+                       "TRGSW selectors (N=1024, Bg=2^10, l=2, alpha_bk), TRLWE data",
+           "client_selector_encrypt_s": round(t_enc, 3),
+           "selector_bytes_each": int(sel[0].nbytes)}
+    for name, op, ref in (("add", she.SHE_LVL_ADD, lambda: (x + y) & ((1 << width) - 1)),
+                          ("max", she.SHE_LVL_MAX, lambda: np.maximum(x, y)),
+                          ("relu", she.SHE_LVL_RELU, lambda: np.maximum(x, 0))):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out, n_cmux, depth = she.lvl_unit(ctx, op, sel_dev, xs, None if op == she.SHE_LVL_RELU
+                                          else ys, width, True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        got = she.lvl_decrypt(sk, out.cpu().numpy().view(np.uint32)).astype(np.int64)
+        v = (got << np.arange(got.shape[-1])).sum(axis=-1)
+        if name == "max":
+            v = np.where(got[:, -1] == 1, v - (1 << width), v)
+        res[name] = {"ms": round(ms, 2), "cmux": n_cmux, "depth": depth,
+                     "cmux_per_s": round(n_cmux / (ms * 1e-3), 1),
+                     "decrypted_mismatches": int(np.sum(v != ref()))}
+    return res
+
+
 def batch_sweep(ctx, sk, P, sizes=(148, 740, 1480, 4096, 8192, 16384, 32768)):
     """Gates/s against the batch size (config-1 gates; one lane per CTA below
     148 lanes, G = 5 lock-step lanes per CTA above): where the persistent
@@ -661,6 +705,8 @@ def run_she(args):
         line["weak_scaled"] = weak
     if not args.no_net:
         line["net_latency"] = net_latency(ctx, sk, P, world, rank)
+        if engine:
+            line["leveled_units"] = leveled_units(ctx, sk, P)
     if args.tcn:
         line["tcn_net_latency"] = net_latency(ctx, sk, P, world, rank, tcn=True)
     if args.dshe:
