@@ -363,6 +363,42 @@ constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double
 // exactly the arithmetic the blind rotation runs.
 //
 // Forward FFT of one digit row (32 digits per thread: coefficient lane + 32 m).
+// Digit fields of row w (R8) without the -Bg/2 shift: u = (y >> shift) & mask,
+// digit = u - Bg/2, y = (X^a P)[m] - P[m] + offset for m = lane + 32 j2 (the
+// rotation of br::load_digits); the shift is applied in the conversion to
+// double (fbr_forward_fields).
+__device__ __forceinline__ void fbr_load_fields(const br::Geometry& g, int w, int lane,
+                                                const uint32_t* acc, uint32_t a,
+                                                uint32_t (&u)[32]) {
+  constexpr int N = fft::kN;
+  const int c = w / (int)g.l, j = w % (int)g.l;
+  const uint32_t* P = acc + c * N;
+  const uint32_t shift = 32 - (j + 1) * g.bg_bits, mask = (1u << g.bg_bits) - 1;
+#pragma unroll
+  for (int j2 = 0; j2 < 32; ++j2) {
+    const uint32_t m = lane + 32 * j2;
+    const uint32_t idx = (m - a) & (2 * N - 1);  // (X^a P)[m] = +-P[m - a]
+    uint32_t v = P[idx & (N - 1)];
+    if (idx >= (uint32_t)N) v = 0u - v;
+    u[j2] = ((v - P[m] + g.dec_offset) >> shift) & mask;
+  }
+}
+
+// Forward FFT of one digit row given as fields u = d + Bg/2 in [0, Bg): the
+// exact conversion 2^52 + u - (2^52 + Bg/2) = d is one DADD.
+template <int V>
+__device__ __forceinline__ void fbr_forward_fields(const uint32_t (&u)[32], double half, int lane,
+                                                   const double2* tw_fwd, double2* row) {
+  const double off = 4503599627370496.0 + half;  // 2^52 + Bg/2
+  double re[16], im[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    re[m] = __hiloint2double(0x43300000, (int)u[m]) - off;
+    im[m] = __hiloint2double(0x43300000, (int)u[m + 16]) - off;
+  }
+  FftVar<V>::forward(re, im, lane, tw_fwd, row);
+}
+
 template <int V>
 __device__ __forceinline__ void fbr_forward_digits(const int32_t (&d)[32], int lane,
                                                    const double2* tw_fwd, double2* row) {
@@ -511,9 +547,9 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
     for (uint32_t i = 0; i < n; ++i) {
       if (stagger && grp == 1) group_sync(15, TG * 2);  // start one forward behind group 0
       if (on) {  // forward FFT of digit row w
-        int32_t d[32];
-        br::load_digits<S>(geo, w, lane, me.acc, me.abar[i], d);
-        fbr_forward_digits<V>(d, lane, tw_fwd, me.row(w));
+        uint32_t u[32];
+        fbr_load_fields(geo, w, lane, me.acc, me.abar[i], u);
+        fbr_forward_fields<V>(u, (double)(1u << (geo.bg_bits - 1)), lane, tw_fwd, me.row(w));
       }
       if (stagger) {
         if (grp == 0) group_arrive(15, TG * 2);
@@ -624,11 +660,13 @@ __global__ void __launch_bounds__(128) fft_selftest_kernel(const int32_t* digits
   for (int m = tid; m < 2 * N; m += 128) acc[m] = 0;
   __syncthreads();
   {
+    // the caller's digits as fields u = d + 2^11 (|d| <= 2^11), through the
+    // blind rotation's conversion (fbr_forward_fields)
     const int32_t* d = digits + (c * 4 + w) * N;
-    int32_t dd[32];
+    uint32_t uu[32];
 #pragma unroll
-    for (int j2 = 0; j2 < 32; ++j2) dd[j2] = d[lane + 32 * j2];
-    fbr_forward_digits<V>(dd, lane, tw, rows + w * fft::kRow);
+    for (int j2 = 0; j2 < 32; ++j2) uu[j2] = (uint32_t)(d[lane + 32 * j2] + 2048);
+    fbr_forward_fields<V>(uu, 2048.0, lane, tw, rows + w * fft::kRow);
   }
   __syncthreads();
   const double2* bki = bkf + c * 16 * M;
