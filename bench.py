@@ -48,6 +48,11 @@ COUNT = 4096
 # (passes A and B, folding twist, int<->double conversions) + pointwise
 # 512 x 4 x 16 = 176,128; ncu's DADD + DMUL + DFMA count: 176,129
 FP64_OPS_PER_CMUX = 8 * 17_920 + 512 * 4 * 16
+# The work unit above is fixed (the round-1 transform's count, DESIGN.md
+# §4.2b), so the fraction measures useful work per second whichever transform
+# runs.  FP64 instructions the default transform (v2, §4.2c) actually executes
+# per CMux and lane, from ncu (profiles/r2/: DADD + DMUL + DFMA / lanes / n):
+FP64_EXECUTED_PER_CMUX = {1: 176_129, 2: 183_875}
 MODMUL_PER_LANE = {1024: 19_456_000, 256: 1_048_576}  # n[(k+1)l+(k+1)](N/2)log2N + n(k+1)l(k+1)N
 WORKLOAD = ("config1: 4096 independent bootstrapped gates, ops uniform over "
             "NAND/AND/OR/XOR/XNOR/MUX, uniform input bits; TFHE N=1024 k=1 n=500 "
@@ -629,6 +634,9 @@ def run_she(args):
                           "FFT + sample extract)",
                 "algorithmic_per_launch": f"{lanes_rank} BR lanes x {P.n} CMux x {FP64_OPS_PER_CMUX} "
                                           "FP64 instr (DESIGN.md §4.2b)",
+                "fp64_executed_per_cmux_default_transform": FP64_EXECUTED_PER_CMUX[2],
+                "frac_of_executed": round(lanes_rank * P.n * FP64_EXECUTED_PER_CMUX[2]
+                                          / (br_ms_per_launch * 1e-3) / fp64_peak, 4),
                 **common,
                 "wave_rounds": {"lanes": lanes_rank, "slots_per_round": slots, "rounds": rounds,
                                 "last_round_fill": round(lanes_rank / slots - (rounds - 1), 3)},
