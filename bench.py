@@ -837,7 +837,7 @@ def main():
                     help="FFT engine independent lane groups per CTA (she_ctx_options.fft_groups)")
     ap.add_argument("--fft-prefetch", type=int, default=0,
                     help="BK planes prefetched before the pointwise barrier (she_ctx_options)")
-    ap.add_argument("--ks-kernel", default="default", choices=["default", "general", "cuda", "imma"],
+    ap.add_argument("--ks-kernel", default="default", choices=["default", "general", "cuda", "imma", "tcgen05"],
                     help="key-switch kernel (she_ctx_options.ks_kernel)")
     ap.add_argument("--count", type=int, default=COUNT,
                     help="gates per step (default: config 1's 4096; other values are A/B only)")

@@ -160,7 +160,8 @@ typedef struct {
   int ks_kernel;  /* 0 = default; 1 = the general ks_kernel (any base-4
                      decomposition); 2 = ks2_kernel (CUDA cores, base 4, t = 8);
                      3 = the tensor-core key switch (ks_imma.cuh: 0/1 digit
-                     matrix x key byte planes on mma.sync u8, base 4, t = 8) */
+                     matrix x key byte planes on mma.sync u8, base 4, t = 8),
+                     4 = the same product on tcgen05 (kind::i8, TMEM) */
   int fft_variant;/* FFT engine transform: 0 = default (2), 1 = the round-1
                      transform (16-entry twiddle tables, select-based pair
                      exchange; 4 lanes per CTA only), 2 = v2,

@@ -930,6 +930,7 @@ constexpr int kKsG = 16, kKsCH = 64;
 // Device layout of the repacked key: [N][8][3][stride] rows (K1, K2, NK3).
 constexpr int kKs2G = 16, kKs2CH = 16, kKs2T = 256;
 constexpr bool kKsImmaDefault = true;  // default key switch: tensor cores (ks_imma.cuh)
+constexpr bool kKsTcgen05Default = false;  // ... on tcgen05 (true) or mma.sync (false)
 
 template <int G, int CH>
 __global__ void __launch_bounds__(kKs2T, 2) ks2_kernel(KSArgs args) {
@@ -1257,8 +1258,10 @@ struct she_ctx {
   int fft_pre = 16;                // BK planes prefetched before the pre-pointwise barrier
   double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
-  // key switch on the tensor cores (ks_imma.cuh; base 4, t = 8)
+  // key switch on the tensor cores (ks_imma.cuh; base 4, t = 8): mma.sync
+  // (IMMA) or, ksi_tc, tcgen05 kind::i8 with the accumulator in TMEM
   bool ksi = false;
+  bool ksi_tc = false;
   uint8_t* ksi_bt = nullptr;   // [stride * 4 columns (word, plane)][K = 24 N] key byte planes
   uint8_t* ksi_a = nullptr;    // [ksi_cap rows][K] 0/1 digit matrix
   int32_t* ksi_c = nullptr;    // [ksi_cap][stride * 4] products
@@ -1525,8 +1528,13 @@ she_status run_ks_imma(she_ctx* ctx, const GateSrc& s, size_t cnt, cudaStream_t 
     ksi_prep_kernel<<<(unsigned)rows, 256, 0, stream>>>(sb, ctx->ext + 2 * b0 * ctx->ext_stride,
                                                         ctx->ext_stride, N, ctx->ksi_a, (uint32_t)K,
                                                         ctx->ksi_bp);
-    ksi::ksi_gemm<<<dim3((unsigned)(ncols / ksi::BN), (unsigned)(rows / ksi::BM)), ksi::kThreads,
-                    ksi::kSmem, stream>>>(ctx->ksi_a, ctx->ksi_bt, ctx->ksi_c, (int)K, (int)ncols);
+    const dim3 grid((unsigned)(ncols / ksi::BN), (unsigned)(rows / ksi::BM));
+    if (ctx->ksi_tc)
+      ksi::ksi_gemm_tc<<<grid, ksi::kThreads, ksi::kSmemTc, stream>>>(ctx->ksi_a, ctx->ksi_bt,
+                                                                     ctx->ksi_c, (int)K, (int)ncols);
+    else
+      ksi::ksi_gemm<<<grid, ksi::kThreads, ksi::kSmem, stream>>>(ctx->ksi_a, ctx->ksi_bt, ctx->ksi_c,
+                                                                 (int)K, (int)ncols);
     ksi_combine_kernel<<<(unsigned)bc, 128, 0, stream>>>(sb, ctx->ksi_c, (uint32_t)ncols,
                                                          ctx->ksi_bp, ctx->p.n);
     CK(cudaGetLastError());
@@ -1659,7 +1667,7 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     return fail(SHE_ERR_ARG, "NTT shape %dx%d is not instantiated", o.ntt_lanes, o.ntt_ctas);
   if ((o.ntt_lanes || o.ntt_ctas) && use_fft)
     return fail(SHE_ERR_ARG, "ntt_lanes/ntt_ctas given for the FFT engine");
-  if (o.ks_kernel < 0 || o.ks_kernel > 3) return fail(SHE_ERR_ARG, "ks_kernel=%d", o.ks_kernel);
+  if (o.ks_kernel < 0 || o.ks_kernel > 4) return fail(SHE_ERR_ARG, "ks_kernel=%d", o.ks_kernel);
   if (o.ks_kernel >= 2 && !(p->ks_t == 8 && p->ks_base_bits == 2))
     return fail(SHE_ERR_ARG, "ks_kernel %d needs base 4, t = 8", o.ks_kernel);
   if (o.fft_variant < 0 || o.fft_variant > 3)
@@ -1717,7 +1725,8 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     // ks_kernel = 1 forces ks_kernel (the general-parameter path) so that the
     // tests can pin it on the configs' parameters as well
     const bool base4t8 = t == 8 && base == 4 && ctx->stride <= 2 * (uint32_t)kKs2T;
-    ctx->ksi = base4t8 && (o.ks_kernel == 3 || (o.ks_kernel == 0 && kKsImmaDefault));
+    ctx->ksi = base4t8 && (o.ks_kernel == 3 || o.ks_kernel == 4 || (o.ks_kernel == 0 && kKsImmaDefault));
+    ctx->ksi_tc = ctx->ksi && (o.ks_kernel == 4 || (o.ks_kernel == 0 && kKsTcgen05Default));
     ctx->ks2 = base4t8 && !ctx->ksi && (o.ks_kernel == 0 || o.ks_kernel == 2);
     if (ctx->ksi) {  // the key's byte planes, columns (word, plane), K = (i, j, v) contiguous
       const size_t K = (size_t)N * t * 3, cols = (size_t)ctx->stride * 4;
@@ -1739,6 +1748,9 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(ksi::ksi_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)ksi::kSmem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ksi::ksi_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)ksi::kSmemTc);
       if (e != cudaSuccess) {
         she_ctx_destroy(ctx);
         return cuda_fail(e, "tensor-core key-switch setup");

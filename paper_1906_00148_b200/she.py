@@ -55,7 +55,7 @@ class she_ctx_options(ctypes.Structure):
     def of(cls, engine="default", fft_lanes=0, ntt_shape=(0, 0), ks_kernel="default",
            fft_variant=0, fft_groups=0, fft_prefetch=0):
         return cls(cls.ENGINES[engine], fft_lanes, ntt_shape[0], ntt_shape[1],
-                   {"default": 0, "general": 1, "cuda": 2, "imma": 3}[ks_kernel], fft_variant,
+                   {"default": 0, "general": 1, "cuda": 2, "imma": 3, "tcgen05": 4}[ks_kernel], fft_variant,
                    fft_groups, fft_prefetch)
 
 

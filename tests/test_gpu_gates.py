@@ -290,12 +290,14 @@ ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3
                "fft-2groups": dict(engine="fft", fft_groups=2),
                "fft5-noprefetch": dict(engine="fft", fft_lanes=5, fft_prefetch=3),
                "ks-imma": dict(ks_kernel="imma"), "ks-cuda": dict(ks_kernel="cuda"),
+               "ks-tcgen05": dict(ks_kernel="tcgen05"),
                "fft-v3": dict(engine="fft", fft_variant=3),
                "fft5-v3": dict(engine="fft", fft_lanes=5, fft_prefetch=3, fft_variant=3)}
 
 
 @pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2", "fft-v1", "fft-2groups",
-                                    "fft5-noprefetch", "ks-imma", "ks-cuda", "fft-v3", "fft5-v3"])
+                                    "fft5-noprefetch", "ks-imma", "ks-cuda", "fft-v3", "fft5-v3",
+                                    "ks-tcgen05"])
 def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with 4 lanes per
     CTA; the Goldilocks NTT engine (she_ctx_options.br_engine = 2) and the other
@@ -307,7 +309,7 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
     ctx = she.Context(P, env1.ck, device=0, **ENGINE_OPTS[engine])
     assert she.br_engine(ctx) == {"ntt": 0, "fft3": 3, "fft2x2": 2, "fft-v1": 4,
                                   "fft-2groups": 4, "fft5-noprefetch": 5, "ks-imma": 4,
-                                  "ks-cuda": 4, "fft-v3": 4, "fft5-v3": 5}[engine]
+                                  "ks-cuda": 4, "fft-v3": 4, "fft5-v3": 5, "ks-tcgen05": 4}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
     she.she_gate_batch_ops(ctx, dev(np.asarray(ops, np.uint8)), dev(a), dev(b), dev(c), out)
@@ -403,7 +405,7 @@ def test_gpu_client_matches_host_client(cuda, cfg):
 
 
 
-@pytest.mark.parametrize("ks", ["general", "cuda", "imma"])
+@pytest.mark.parametrize("ks", ["general", "cuda", "imma", "tcgen05"])
 def test_key_switch_kernels_c0(cuda, ks):
     """Every key-switch kernel on the config-0 gates (n = 128: an LWE slot of
     160 words, 5 column tiles of the tensor-core GEMM): bit-exact with the
@@ -438,7 +440,7 @@ def test_tensor_core_key_switch_multi_pass_c0(cuda):
     cts = she.she_encrypt_bits(sk, bits.ravel(), si.input_seed(cfg), 0).reshape(count, 3, -1)
     a, b, c = (np.ascontiguousarray(cts[:, j]) for j in range(3))
     outs = {}
-    for ks in ("imma", "cuda"):
+    for ks in ("imma", "cuda", "tcgen05"):
         ctx = she.Context(P, ck, device=0, ks_kernel=ks)
         out = torch.zeros((count, P.stride), dtype=torch.int32, device="cuda")
         she.she_gate_batch_ops(ctx, torch.from_numpy(ops.astype(np.uint8)).cuda(), dev(a), dev(b),
@@ -447,6 +449,7 @@ def test_tensor_core_key_switch_multi_pass_c0(cuda):
         outs[ks] = host(out)
         ctx.close()
     assert np.array_equal(outs["imma"], outs["cuda"])
+    assert np.array_equal(outs["tcgen05"], outs["cuda"])
     rng = np.random.default_rng(si.sample_seed(0) + 3)
     pick = np.sort(rng.choice(count, 24, replace=False))
     pick[-1] = count - 1  # the last gate of the ragged pass
