@@ -930,7 +930,7 @@ constexpr int kKsG = 16, kKsCH = 64;
 // Device layout of the repacked key: [N][8][3][stride] rows (K1, K2, NK3).
 constexpr int kKs2G = 16, kKs2CH = 16, kKs2T = 256;
 constexpr bool kKsImmaDefault = true;  // default key switch: tensor cores (ks_imma.cuh)
-constexpr bool kKsTcgen05Default = false;  // ... on tcgen05 (true) or mma.sync (false)
+constexpr bool kKsTcgen05Default = true;   // ... on tcgen05 (true) or mma.sync (false)
 
 template <int G, int CH>
 __global__ void __launch_bounds__(kKs2T, 2) ks2_kernel(KSArgs args) {
