@@ -654,6 +654,26 @@ def run_she(args):
                 **common,
                 "peak_source": peak_src, "ncu_profile": read_ncu_summary()}
 
+    # the key switch's own roofline: the tcgen05 kind::i8 product (DESIGN.md
+    # §4.3) of a (gates padded to 128) x 24N one-hot matrix and the key's
+    # (stride x 4 planes) columns, against the int8 dense tensor peak = the
+    # measured bf16 peak x 2 (the nominal int8 / bf16 ratio, 4.5 / 2.25 PF)
+    ks_ms = t["ks_ms"] / max(1, t["ks_launches"])
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = float(json.load(f)["bf16_tflops"])
+        src = "MEASURED_PEAKS.json bf16_tflops (burst) x 2"
+    except (OSError, ValueError, KeyError):
+        bf16, src = 1590.0, "B200_PROFILING.md fallback 1.59 PF bf16 x 2"
+    gemm_ops = 2.0 * (-(-(hi - lo) // 128) * 128) * (stride * 4) * (24 * P.N)
+    roof["key_switch"] = {"bound": "tensor", "kernel": "ksi_gemm_tc (tcgen05.mma kind::i8, TMEM)",
+                          "ms_per_launch": round(ks_ms, 4),
+                          "achieved": round(gemm_ops / (ks_ms * 1e-3) / 1e12, 1),
+                          "peak": round(2 * bf16, 1), "unit": "T int8-op/s",
+                          "frac": round(gemm_ops / (ks_ms * 1e-3) / 1e12 / (2 * bf16), 4),
+                          "peak_source": src,
+                          "note": "ks_ms spans the prep, GEMM and combine launches"}
+
     # ---- end to end through the public host-buffer API (H2D + D2H inside) ----
     pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()
     h_ops = pin((COUNT,), torch.uint8)
