@@ -504,6 +504,8 @@ def engine_options(args) -> dict:
         opts["fft_groups"] = args.fft_groups
     if args.fft_prefetch:
         opts["fft_prefetch"] = args.fft_prefetch
+    if args.fft_streams:
+        opts["fft_streams"] = args.fft_streams
     if args.ks_kernel != "default":
         opts["ks_kernel"] = args.ks_kernel
     return opts
@@ -857,6 +859,8 @@ def main():
                     help="FFT engine independent lane groups per CTA (she_ctx_options.fft_groups)")
     ap.add_argument("--fft-prefetch", type=int, default=0,
                     help="BK planes prefetched before the pointwise barrier (she_ctx_options)")
+    ap.add_argument("--fft-streams", type=int, default=0,
+                    help="FFT engine lanes per warp (she_ctx_options.fft_streams: 1 or 2)")
     ap.add_argument("--ks-kernel", default="default", choices=["default", "general", "cuda", "imma", "tcgen05"],
                     help="key-switch kernel (she_ctx_options.ks_kernel)")
     ap.add_argument("--count", type=int, default=COUNT,

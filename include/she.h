@@ -173,7 +173,11 @@ typedef struct {
   int fft_prefetch;/* FFT engine: BK_i planes prefetched into registers before
                      the pointwise barrier: 0 = default (16), 1 = 16, 2 = 8
                      (4 or 5 lanes), 3 = none (5 lanes) */
-  int reserved[4];/* must be 0 */
+  int fft_streams;/* FFT engine: 0 = default; 1 = one lane per warp
+                     (br_fft_kernel); 2 = two lanes per warp with one lane a
+                     step behind the other (br_fft2s_kernel, 4 lanes per CTA
+                     on 8 warps, variant 2) */
+  int reserved[3];/* must be 0 */
 } she_ctx_options;
 
 /* Create a context on CUDA `device`: uploads BK and KSK and transforms BK for

@@ -355,6 +355,7 @@ struct FftVar<3> {  // v2's tables and scaling, DIT/FMA DFT16s (fft_core.cuh)
   __device__ static double2 bk_correction(int k) { return fft::v2_bk_correction(k); }
 };
 constexpr int kFftDefaultVariant = 2;
+constexpr int kFftDefaultStreams = 1;  // br_fft_kernel (1) or the two-stream br_fft2s_kernel (2)
 template <int V>
 constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double2); }
 
@@ -434,13 +435,10 @@ __device__ __forceinline__ void fbr_pointwise(double2* row0, int k, const double
 // Inverse FFT of product row w = (o, half), rounded to the exact integer and
 // added into ACC_o (hi half shifted by 16; torus32 wrap).  TRACK: also the
 // largest distance of a pre-rounding value to its integer (self-test only).
-template <int V, bool TRACK>
-__device__ __forceinline__ void fbr_inverse_acc(double2* row, int lane, const double2* tw_inv,
-                                                uint32_t* acc_o, int w,
-                                                unsigned long long* worst) {
+template <bool TRACK>
+__device__ __forceinline__ void fbr_round_acc(const double2 (&x)[8], const double2 (&y)[8], int lane,
+                                              uint32_t* acc_o, int w, unsigned long long* worst) {
   constexpr int M = fft::kM;
-  double2 x[8], y[8];
-  FftVar<V>::inverse(row, lane, tw_inv, row, x, y);
   const int sh = (w & 1) ? 0 : 16;
   const int k2 = lane >> 1, hh = lane & 1;
   double dmax = 0.0;
@@ -463,6 +461,92 @@ __device__ __forceinline__ void fbr_inverse_acc(double2* row, int lane, const do
     atomicAdd(acc_o + n_y + M, fft::d2u_round(yv.y) << sh);
   }
   if (TRACK) atomicMax(worst, (unsigned long long)__double_as_longlong(dmax));
+}
+
+template <int V, bool TRACK>
+__device__ __forceinline__ void fbr_inverse_acc(double2* row, int lane, const double2* tw_inv,
+                                                uint32_t* acc_o, int w,
+                                                unsigned long long* worst) {
+  double2 x[8], y[8];
+  FftVar<V>::inverse(row, lane, tw_inv, row, x, y);
+  fbr_round_acc<TRACK>(x, y, lane, acc_o, w, worst);
+}
+
+// ---- two-stream warps (she_ctx_options.fft_streams = 2) ----
+// A warp runs row w of TWO lanes, A and B, with B one step behind A, so that
+// every step pairs one lane's FP64 work (a 16-point DFT) with the other's
+// shared-memory work (digit loads, twiddle-and-transpose stores, transposed
+// loads, output stores, atomics) and the in-order warp always has independent
+// instructions of both kinds to issue.  Transform v2 (the same arithmetic, so
+// the same ciphertexts as br_fft_kernel).
+__device__ __forceinline__ void fbr2_fields_in(const br::Geometry& g, int w, int lane,
+                                               const uint32_t* acc, uint32_t abar,
+                                               double2 (&a)[16]) {
+  uint32_t u[32];
+  fbr_load_fields(g, w, lane, acc, abar, u);
+  const double off = 4503599627370496.0 + (double)(1u << (g.bg_bits - 1));
+  double re[16], im[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    re[m] = __hiloint2double(0x43300000, (int)u[m]) - off;
+    im[m] = __hiloint2double(0x43300000, (int)u[m + 16]) - off;
+  }
+  fft::v2_fwd_in(re, im, a);
+}
+
+__device__ __forceinline__ void fbr2_forward_pair(const br::Geometry& g, int w, int lane,
+                                                  const uint32_t* accA, uint32_t abarA,
+                                                  double2* rowA, const uint32_t* accB,
+                                                  uint32_t abarB, double2* rowB,
+                                                  const double2* tw) {
+  double2 a[16], b[16];
+  fbr2_fields_in(g, w, lane, accA, abarA, a);  // A: digits
+  fft::dft16<1>(a);                            // A: DFT16 || B: digits
+  fbr2_fields_in(g, w, lane, accB, abarB, b);
+  fft::v2_pa_store(a, lane, tw, rowA);         // A: twiddle + transpose store || B: DFT16
+  fft::dft16<1>(b);
+  __syncwarp();
+  fft::v2_pb_load(a, lane, rowA);              // A: transposed load || B: store
+  fft::v2_pa_store(b, lane, tw, rowB);
+  __syncwarp();
+  fft::dft16<1>(a);                            // A: DFT16 || B: transposed load
+  fft::v2_pb_load(b, lane, rowB);
+  double2 xa[8], ya[8];
+  fft::v2_exchange<1>(a, lane, xa, ya);        // A: pair exchange || B: DFT16
+  fft::dft16<1>(b);
+  __syncwarp();                                // transposed loads done before the rows are overwritten
+  fft::v2_fwd_out(xa, ya, lane, rowA);         // A: spectrum store || B: pair exchange
+  double2 xb[8], yb[8];
+  fft::v2_exchange<1>(b, lane, xb, yb);
+  fft::v2_fwd_out(xb, yb, lane, rowB);
+}
+
+__device__ __forceinline__ void fbr2_inverse_pair(int w, int lane, double2* rowA, uint32_t* accA,
+                                                  double2* rowB, uint32_t* accB,
+                                                  const double2* tw) {
+  double2 a[16], b[16];
+  fft::v2_inv_in(rowA, lane, a);               // A: spectrum load
+  __syncwarp();
+  fft::dft16<-1>(a);                           // A: DFT16 || B: spectrum load
+  fft::v2_inv_in(rowB, lane, b);
+  __syncwarp();
+  fft::v2_pa_store(a, lane, tw, rowA);         // A: twiddle + transpose store || B: DFT16
+  fft::dft16<-1>(b);
+  __syncwarp();
+  fft::v2_pb_load(a, lane, rowA);              // A: transposed load || B: store
+  fft::v2_pa_store(b, lane, tw, rowB);
+  __syncwarp();
+  fft::dft16<-1>(a);                           // A: DFT16 || B: transposed load
+  fft::v2_pb_load(b, lane, rowB);
+  double2 xa[8], ya[8], xb[8], yb[8];
+  fft::v2_exchange<-1>(a, lane, xa, ya);       // A: exchange + untwist || B: DFT16
+  fft::v2_inv_untwist(lane, xa, ya);
+  fft::dft16<-1>(b);
+  fbr_round_acc<false>(xa, ya, lane, accA, w, nullptr);  // A: round + atomics || B: exchange
+  fft::v2_exchange<-1>(b, lane, xb, yb);
+  fft::v2_inv_untwist(lane, xb, yb);
+  fbr_round_acc<false>(xb, yb, lane, accB, w, nullptr);
+  __syncwarp();
 }
 
 struct BRFArgs {
@@ -604,6 +688,117 @@ __global__ void __launch_bounds__(128 * G, B) br_fft_kernel(BRFArgs args) {
       }
     }
     group_sync(gbar, TG);
+  }
+}
+
+// K3, two-stream FP64 engine: 4 lanes per CTA on 8 warps (256 threads, up to
+// 255 registers); warp w runs row (or output) r = w & 3 of lanes 2p and 2p + 1,
+// p = w >> 2, through fbr2_forward_pair / fbr2_inverse_pair; the pointwise
+// step is CTA-wide as in br_fft_kernel (thread k: frequencies k and k + 256 of
+// the 4 lanes, both BK_i columns requested before the barrier).
+__global__ void __launch_bounds__(256, 1) br_fft2s_kernel(BRFArgs args) {
+  using S = ntt::Shape<1024>;
+  constexpr int G = 4, N = fft::kN, M = fft::kM, T = 256, V = 2;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const GateSrc& src = args.src;
+  const br::Geometry& geo = args.geo;
+  const uint32_t n = geo.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = warp & 3, p = warp >> 2, lt = tid & 127;
+  const size_t lane_bytes = FLane::bytes(n);
+  FLane la(smem + (size_t)(2 * p) * lane_bytes), lb(smem + (size_t)(2 * p + 1) * lane_bytes);
+  const uint32_t total = *args.nlanes;
+  double2* tw_fwd = reinterpret_cast<double2*>(smem + (size_t)G * lane_bytes);
+  double2* tw_inv = tw_fwd + FftVar<V>::kTab;
+  FftVar<V>::tables(tid, T, tw_fwd, tw_inv);
+  __syncthreads();
+
+  const uint32_t first = (uint32_t)(((uint64_t)blockIdx.x * total) / gridDim.x);
+  const uint32_t last = (uint32_t)(((uint64_t)(blockIdx.x + 1) * total) / gridDim.x);
+  for (uint32_t base = first; base < last; base += G) {
+    const bool on[2] = {base + 2 * p < last, base + 2 * p + 1 < last};
+    uint32_t gate[2] = {0, 0}, hh[2] = {0, 0};
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (!on[s]) continue;
+      FLane& me = s ? lb : la;
+      const uint32_t e = args.lanes[base + 2 * p + s];
+      gate[s] = e & 0x7FFFFFFFu;
+      hh[s] = e >> 31;
+      const LaneForm f = lane_form(gate_op(src, gate[s]), (int)hh[s]);
+      bool n0, n1;
+      const uint32_t* x0 = gate_in(src, gate[s], 0, n0);
+      const uint32_t* x1 = gate_in(src, gate[s], f.j1, n1);
+      const uint32_t k0 = (uint32_t)(n0 ? -f.k0 : f.k0), k1 = (uint32_t)(n1 ? -f.k1 : f.k1);
+      for (uint32_t k = lt; k <= n; k += 128) {
+        uint32_t v = k0 * x0[k] + k1 * x1[k];
+        if (k == n) v += f.kappa;
+        me.abar[k] = (uint16_t)br::modswitch(v, geo.lg2N);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (!on[s]) continue;
+      FLane& me = s ? lb : la;
+      const uint32_t bbar = me.abar[n];
+      for (int m = lt; m < N; m += 128) {
+        me.acc[m] = 0;
+        me.acc[N + m] = br::testvec_coeff(m, bbar, N);
+      }
+    }
+    __syncthreads();
+
+    for (uint32_t i = 0; i < n; ++i) {
+      if (on[0] && on[1]) {
+        fbr2_forward_pair(geo, r, lane, la.acc, la.abar[i], la.row(r), lb.acc, lb.abar[i],
+                          lb.row(r), tw_fwd);
+      } else if (on[0] || on[1]) {
+        FLane& me = on[0] ? la : lb;
+        uint32_t u[32];
+        fbr_load_fields(geo, r, lane, me.acc, me.abar[i], u);
+        fbr_forward_fields<V>(u, (double)(1u << (geo.bg_bits - 1)), lane, tw_fwd, me.row(r));
+      }
+      const double2* bki = args.bkf + (size_t)i * 16 * M;
+      double2 b0[16], b1[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        b0[q] = __ldg(bki + (size_t)q * M + tid);
+        b1[q] = __ldg(bki + (size_t)q * M + tid + T);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+        if (base + gg < last) {
+          double2* row0 = FLane(smem + (size_t)gg * lane_bytes).row(0);
+          fbr_pointwise(row0, tid, b0);
+          fbr_pointwise(row0, tid + T, b1);
+        }
+      __syncthreads();
+      if (on[0] && on[1]) {
+        fbr2_inverse_pair(r, lane, la.row(r), la.acc + (r >> 1) * N, lb.row(r), lb.acc + (r >> 1) * N,
+                          tw_inv);
+      } else if (on[0] || on[1]) {
+        FLane& me = on[0] ? la : lb;
+        fbr_inverse_acc<V, false>(me.row(r), lane, tw_inv, me.acc + (r >> 1) * N, r, nullptr);
+      }
+      if (on[0] || on[1]) lane_sync(1 + p);  // the pair's 4 warps: ACC complete
+    }
+
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (!on[s]) continue;
+      FLane& me = s ? lb : la;
+      uint32_t* e = args.ext + (size_t)(2 * gate[s] + hh[s]) * args.ext_stride;
+      for (int m = lt; m <= N; m += 128) {
+        uint32_t v;
+        if (m == 0) v = me.acc[0];
+        else if (m < N) v = 0u - me.acc[N - m];
+        else v = me.acc[N];
+        e[m] = v;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1256,6 +1451,7 @@ struct she_ctx {
   int fft_v = kFftDefaultVariant;  // FFT variant (FftVar): 1 = round-1 transform, 2 = v2
   int fft_grp = 1;                 // independent lane groups per CTA (br_fft_kernel GRP)
   int fft_pre = 16;                // BK planes prefetched before the pre-pointwise barrier
+  int fft_streams = 1;             // 2: br_fft2s_kernel (two lanes per warp, skewed)
   double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
   // key switch on the tensor cores (ks_imma.cuh; base 4, t = 8): mma.sync
@@ -1380,6 +1576,8 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
                             (int)(5 * lb + fft_tables_bytes<2>())));
     CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 2, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(4 * lb + fft_tables_bytes<2>())));
+    CK(cudaFuncSetAttribute(br_fft2s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(4 * lb + fft_tables_bytes<2>())));
     CK(cudaFuncSetAttribute(br_fft_kernel<4, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(4 * lb + fft_tables_bytes<3>())));
     CK(cudaFuncSetAttribute(br_fft_kernel<5, 1, 3, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1448,6 +1646,35 @@ she_status launch_br(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream
     cfg.numAttrs = 1;
   }
   CK(cudaLaunchKernelEx(&cfg, br_kernel<S, G, B>, a));
+  return SHE_OK;
+}
+
+she_status launch_br_fft2s(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
+  BRFArgs f;
+  f.src = a.src;
+  f.lanes = a.lanes;
+  f.nlanes = a.nlanes;
+  f.bkf = ctx->bkf;
+  f.ext = a.ext;
+  f.ext_stride = a.ext_stride;
+  f.geo = a.geo;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms)));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 4 * FLane::bytes(ctx->p.n) + fft_tables_bytes<2>();
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (ctx->persist) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = ctx->bkf;
+    attr[0].val.accessPolicyWindow.num_bytes = ctx->window_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = ctx->window_hit;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  CK(cudaLaunchKernelEx(&cfg, br_fft2s_kernel, f));
   return SHE_OK;
 }
 
@@ -1577,7 +1804,8 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     if (ctx->timing) mark(ctx, stream);
     st = fail(SHE_ERR_STATE, "no blind-rotation kernel for config %dx%d", ctx->br_g, ctx->br_b);
     if (ctx->bkf && S::N == fft::kN) {
-      st = ctx->fft_v == 1   ? launch_br_fft<4, 1, 1>(ctx, a, 2 * cnt, stream)
+      st = ctx->fft_streams == 2 ? launch_br_fft2s(ctx, a, 2 * cnt, stream)
+           : ctx->fft_v == 1   ? launch_br_fft<4, 1, 1>(ctx, a, 2 * cnt, stream)
            : ctx->fft_v == 3 && ctx->fft_g == 5 ? launch_br_fft<5, 1, 3, 1, 0>(ctx, a, 2 * cnt, stream)
            : ctx->fft_v == 3 ? launch_br_fft<4, 1, 3>(ctx, a, 2 * cnt, stream)
            : ctx->fft_grp == 2 ? launch_br_fft<4, 1, 2, 2>(ctx, a, 2 * cnt, stream)
@@ -1679,6 +1907,10 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   if (o.fft_variant == 1 && o.fft_lanes && o.fft_lanes != 4)
     return fail(SHE_ERR_ARG, "fft_variant 1 is instantiated for 4 lanes per CTA only");
   if (o.fft_groups < 0 || o.fft_groups > 2) return fail(SHE_ERR_ARG, "fft_groups=%d", o.fft_groups);
+  if (o.fft_streams < 0 || o.fft_streams > 2) return fail(SHE_ERR_ARG, "fft_streams=%d", o.fft_streams);
+  if (o.fft_streams == 2 && (!use_fft || (o.fft_lanes && o.fft_lanes != 4) || o.fft_groups == 2 ||
+                             (o.fft_variant && o.fft_variant != 2) || o.fft_prefetch >= 2))
+    return fail(SHE_ERR_ARG, "fft_streams = 2 is instantiated for 4 lanes, variant 2");
   if (o.fft_prefetch < 0 || o.fft_prefetch > 3)
     return fail(SHE_ERR_ARG, "fft_prefetch=%d", o.fft_prefetch);
   if (o.fft_prefetch >= 2 && (o.fft_groups == 2 || o.fft_variant == 1 ||
@@ -1706,6 +1938,7 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   ctx->fft_g = use_fft ? (o.fft_lanes ? o.fft_lanes : 4) : 0;
   ctx->fft_v = o.fft_variant ? o.fft_variant : kFftDefaultVariant;
   ctx->fft_grp = o.fft_groups ? o.fft_groups : 1;
+  ctx->fft_streams = o.fft_streams ? o.fft_streams : kFftDefaultStreams;
   ctx->fft_pre = o.fft_prefetch == 0 ? 16 : o.fft_prefetch == 3 ? 0 : o.fft_prefetch == 2 ? 8 : 16;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {

@@ -474,6 +474,71 @@ __device__ __forceinline__ void inverse_v2(const double2* row_in, int lane, cons
   }
 }
 
+// ---- the steps of the v2 transform, for the two-stream kernel --------------
+// (dft512_v2 split at its shared-memory / FP64 boundaries so that a warp can
+// run one lane's FP64 step and another lane's shared-memory step together)
+__device__ __forceinline__ void v2_pa_store(const double2 (&a)[16], int lane, const double2* tw,
+                                            double2* scratch) {
+  const double2 r8 = tw[8 * 32 + lane];
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2) {
+    const double2 p = tw[k2 * 32 + lane];
+    scratch[tslot(lane, k2)] = cmul(a[brev4(k2)], p);
+    scratch[tslot(lane, k2 + 8)] = cmul(a[brev4(k2 + 8)], cmul(p, r8));
+  }
+}
+__device__ __forceinline__ void v2_pb_load(double2 (&a)[16], int lane, const double2* scratch) {
+  const int k2 = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = scratch[tslot(2 * m + h, k2)];
+}
+template <int SIGN>
+__device__ __forceinline__ void v2_exchange(const double2 (&a)[16], int lane, double2 (&x)[8],
+                                            double2 (&y)[8]) {
+  const int h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double2 keep = a[brev4(j)], send = a[brev4(8 + j)];
+    double2 r;
+    r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+    r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+    const double2 c0 = c_w128[(SIGN * 4 * j) & 127];
+    const double2 c1 = c_w128[(-SIGN * 4 * (8 + j)) & 127];
+    double2 c;
+    c.x = h ? c1.x : c0.x;
+    c.y = h ? c1.y : c0.y;
+    const double2 t = cmul(r, c);
+    x[j] = cadd(keep, t);
+    y[j] = csub(keep, t);
+  }
+}
+__device__ __forceinline__ void v2_fwd_in(const double (&re)[16], const double (&im)[16],
+                                          double2 (&a)[16]) {
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = rot<1>(make_double2(re[m], im[m]), 2 * m);  // w64^m
+}
+__device__ __forceinline__ void v2_fwd_out(const double2 (&x)[8], const double2 (&y)[8], int lane,
+                                           double2* row) {
+  const int k2 = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    row[fpos(k2 + 16 * (8 * h + j))] = x[j];
+    row[fpos(k2 + 16 * (16 + 8 * h + j))] = y[j];
+  }
+}
+__device__ __forceinline__ void v2_inv_in(const double2* row_in, int lane, double2 (&a)[16]) {
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = row_in[fpos(lane + 32 * m)];
+}
+__device__ __forceinline__ void v2_inv_untwist(int lane, double2 (&x)[8], double2 (&y)[8]) {
+  const int h = lane & 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    x[j] = cmulc(x[j], c_w128[h ? 40 + 5 * j : j]);
+    y[j] = cmulc(y[j], c_w128[h ? (5 * j - 8) & 127 : 16 + j]);
+  }
+}
+
 // ---- variant 3: variant 2 with DIT/FMA DFT16s and the FMA pair exchange ----
 template <int SIGN>
 __device__ __forceinline__ void dft512_v3(double2 (&a)[16], int lane, const double2* tw,
