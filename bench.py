@@ -506,6 +506,10 @@ def engine_options(args) -> dict:
         opts["fft_prefetch"] = args.fft_prefetch
     if args.fft_streams:
         opts["fft_streams"] = args.fft_streams
+    if args.fft_store != "default":
+        opts["fft_store"] = args.fft_store
+    if args.fft_stagger_ns:
+        opts["fft_stagger_ns"] = args.fft_stagger_ns
     if args.ks_kernel != "default":
         opts["ks_kernel"] = args.ks_kernel
     return opts
@@ -861,6 +865,10 @@ def main():
                     help="BK planes prefetched before the pointwise barrier (she_ctx_options)")
     ap.add_argument("--fft-streams", type=int, default=0,
                     help="FFT engine lanes per warp (she_ctx_options.fft_streams: 1 or 2)")
+    ap.add_argument("--fft-store", default="default", choices=["default", "smem", "tmem"],
+                    help="FFT engine spectra store (she_ctx_options.fft_store): shared or tensor memory")
+    ap.add_argument("--fft-stagger-ns", type=int, default=0,
+                    help="TMEM engine: start delay per quarter pipeline (ns)")
     ap.add_argument("--ks-kernel", default="default", choices=["default", "general", "cuda", "imma", "tcgen05"],
                     help="key-switch kernel (she_ctx_options.ks_kernel)")
     ap.add_argument("--count", type=int, default=COUNT,

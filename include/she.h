@@ -177,7 +177,16 @@ typedef struct {
                      (br_fft_kernel); 2 = two lanes per warp with one lane a
                      step behind the other (br_fft2s_kernel, 4 lanes per CTA
                      on 8 warps, variant 2) */
-  int reserved[3];/* must be 0 */
+  int fft_store;  /* FFT engine: where the digit spectra and products live
+                     between the transforms: 0 = default (1); 1 = shared
+                     memory (br_fft_kernel, CTA-wide pointwise step); 2 =
+                     tensor memory (br_fft_tm_kernel: four independent
+                     two-lane pipelines per SM, one per sub-partition, spectra
+                     in TMEM, the inverse on the forward's register layout;
+                     DESIGN.md §4.2e; no other shape option applies) */
+  int fft_stagger_ns;/* TMEM engine: start delay of quarter q = q x this (ns),
+                     0..100000 (phase offset between the pipelines) */
+  int reserved[1];/* must be 0 */
 } she_ctx_options;
 
 /* Create a context on CUDA `device`: uploads BK and KSK and transforms BK for
@@ -242,7 +251,9 @@ she_status she_field_selftest(int device, const uint64_t* a, const uint64_t* b, 
  * pointwise sum, inverse FFT, rounding, hi/lo recombination),
  * so that the exactness reading is pinned on the kernel that runs, not on a
  * model of it.  variant: the transform (she_ctx_options.fft_variant; 0 =
- * the default).  N = 1024 only.  HOST buffers:
+ * the default); 4 = the TMEM engine (fft_store = 2: bk_tm_kernel's setup, the
+ * digit spectra and products in tensor memory, the register-layout inverse
+ * inverse_tr; br_tmem.cuh).  N = 1024 only.  HOST buffers:
  *   digits int32[count][4][1024]      digit rows r = c*l + j, |d| <= 2^11
  *   bk     uint32[count][4][2][1024]  torus32 BK rows (r, output o)
  *   out    uint32[count][2][1024]     out[c][o] = sum_r digits[c][r] * bk[c][r][o]

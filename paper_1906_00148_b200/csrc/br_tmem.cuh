@@ -1,0 +1,457 @@
+// br_tmem.cuh — the TMEM blind-rotation engine (she_ctx_options.fft_engine =
+// tmem).  Included by engine.cu inside its anonymous
+// namespace (uses GateSrc, lane_form, fbr_load_fields, FLane's layout rules).
+//
+// The CMux product of the FP64 engine (exact split-BK negacyclic FFT, DESIGN.md
+// §4.2b; PAPER.md:31 / :188, TFHE bootstrapping) with the digit spectra and the
+// products kept in tensor memory instead of shared memory:
+//
+//  * Each SM sub-partition (quarter Q = warps Q, Q+4, Q+8, Q+12, which are the
+//    warps that can address TMEM lanes 32Q .. 32Q+31) is an independent
+//    pipeline of two blind-rotation lanes (slots), with its own named barrier:
+//    no CTA-wide barrier inside the CMux loop, so the four quarters drift
+//    apart in phase and one quarter's shared-memory steps overlap another's
+//    FP64 steps.
+//  * Thread t of a quarter owns TMEM row 32Q + t.  A forward transform leaves
+//    thread t holding 16 frequencies of its digit row (x[8], y[8], the
+//    register layout of dft512_v2); they go to the row with one tcgen05.st
+//    (columns slot * 256 + row * 64 + 4 fi).  The pointwise step reads the
+//    four digit spectra of frequency slot fi from the same row, multiplies by
+//    BK_i (laid out [i][fi][plane][t], so 32 threads read 512 contiguous
+//    bytes) and writes the four products in place; the inverse reads its
+//    product row back with tcgen05.ld and runs inverse_tr (fft_core.cuh),
+//    which takes exactly that register layout and returns natural order.
+//    The three shared-memory passes over the spectra of the smem engine
+//    (forward output, pointwise, inverse input: 1,024 wavefronts per lane and
+//    CMux) leave the L1 data path; TMEM moves ~700 B/clk/SM on its own path
+//    (tools/microbench/tmem_bench.cu).
+//  * BK_i is read once per quarter (two lanes) instead of once per CTA (four
+//    lanes): 512 instead of 256 wavefronts per lane and CMux, loaded through
+//    a register ring PD units ahead of use.
+//
+// smem per quarter: ACC [2 slots][2][N] (16 KB), a-bar [2][512] (2 KB), four
+// 8 KB transpose rows (one per warp): 50 KB; + the v2 twiddle tables.
+// TMEM: 512 columns x 128 lanes (all of it; one CTA per SM).
+#pragma once
+
+constexpr int kTmSlots = 2;
+constexpr size_t kTmAccBytes = (size_t)kTmSlots * 2 * fft::kN * 4;
+constexpr size_t kTmAbarBytes = (size_t)kTmSlots * 512 * 2;
+constexpr size_t kTmScratchBytes = (size_t)4 * fft::kRow * 16;
+constexpr size_t kTmQuarterBytes = kTmAccBytes + kTmAbarBytes + kTmScratchBytes;
+constexpr size_t kTmSmemBytes = 4 * kTmQuarterBytes + 2 * fft::kTw2 * 32 * sizeof(double2);
+constexpr int kTmPrefetch = 3;  // BK units (4 planes each) in flight ahead of use
+
+// ---- tensor-memory access (tcgen05, 32x32b shape: thread t <-> TMEM lane) ---
+__device__ __forceinline__ void tm_st4(uint32_t addr, const double2 (&v)[4]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "r"(__double2loint(v[0].x)), "r"(__double2hiint(v[0].x)), "r"(__double2loint(v[0].y)),
+      "r"(__double2hiint(v[0].y)), "r"(__double2loint(v[1].x)), "r"(__double2hiint(v[1].x)),
+      "r"(__double2loint(v[1].y)), "r"(__double2hiint(v[1].y)), "r"(__double2loint(v[2].x)),
+      "r"(__double2hiint(v[2].x)), "r"(__double2loint(v[2].y)), "r"(__double2hiint(v[2].y)),
+      "r"(__double2loint(v[3].x)), "r"(__double2hiint(v[3].x)), "r"(__double2loint(v[3].y)),
+      "r"(__double2hiint(v[3].y))
+      : "memory");
+}
+__device__ __forceinline__ void tm_ld4(uint32_t addr, double2 (&v)[4]) {
+  int r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15])
+      : "r"(addr)
+      : "memory");
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    v[q] = make_double2(__hiloint2double(r[4 * q + 1], r[4 * q]), __hiloint2double(r[4 * q + 3], r[4 * q + 2]));
+}
+__device__ __forceinline__ void tm_st1(uint32_t addr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr),
+               "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)),
+               "r"(__double2hiint(v.y))
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld1(uint32_t addr, double2& v) {
+  int r0, r1, r2, r3;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr)
+               : "memory");
+  v = make_double2(__hiloint2double(r1, r0), __hiloint2double(r3, r2));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// Barrier over the 128 threads of quarter Q (id 1 + Q) with the tcgen05
+// ordering fences around it (TMEM writes before, reads after).
+__device__ __forceinline__ void tm_quarter_sync(int q) {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Spectrum of one digit row to TMEM: x[j] at column 8 j, y[j] at 8 j + 4
+// (frequency slot fi = 2 j and 2 j + 1), in the order the pair exchange
+// produces them.
+__device__ __forceinline__ void tm_store_spectrum(uint32_t addr, const double2 (&x)[8], const double2 (&y)[8]) {
+  tm_st4(addr, {x[0], y[0], x[1], y[1]});
+  tm_st4(addr + 16, {x[2], y[2], x[3], y[3]});
+  tm_st4(addr + 32, {x[4], y[4], x[5], y[5]});
+  tm_st4(addr + 48, {x[6], y[6], x[7], y[7]});
+}
+__device__ __forceinline__ void tm_load_spectrum(uint32_t addr, double2 (&x)[8], double2 (&y)[8]) {
+  double2 v[4][4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) tm_ld4(addr + 16 * p, v[p]);
+  tm_wait_ld();
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    x[2 * p] = v[p][0];
+    y[2 * p] = v[p][1];
+    x[2 * p + 1] = v[p][2];
+    y[2 * p + 1] = v[p][3];
+  }
+}
+
+// Forward transform of one digit row given as fields u = d + Bg/2 (the
+// conversion of fbr_forward_fields) into the TMEM row at addr.
+__device__ __forceinline__ void tm_forward_fields(const uint32_t (&u)[32], double half, int lane,
+                                                  const double2* tw, double2* scratch, uint32_t addr) {
+  const double off = 4503599627370496.0 + half;  // 2^52 + Bg/2
+  double re[16], im[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    re[m] = __hiloint2double(0x43300000, (int)u[m]) - off;
+    im[m] = __hiloint2double(0x43300000, (int)u[m + 16]) - off;
+  }
+  double2 a[16], x[8], y[8];
+  fft::v2_fwd_in(re, im, a);
+  fft::dft512_v2<1>(a, lane, tw, scratch, x, y);
+  tm_store_spectrum(addr, x, y);
+}
+
+// Inverse of the product row at addr, rounded to the exact integer and added
+// into ACC_o at n = lane + 32 m (re) and n + 512 (im), shifted by sh (16 for
+// the hi half).  TRACK: the largest distance to an integer (self-test).
+template <bool TRACK>
+__device__ __forceinline__ void tm_inverse_acc(uint32_t addr, int lane, const double2* tw, double2* scratch,
+                                               uint32_t* acc_o, int sh, unsigned long long* worst) {
+  double2 x[8], y[8], a[16];
+  tm_load_spectrum(addr, x, y);
+  fft::inverse_tr(x, y, lane, tw, scratch, a);
+  double dmax = 0.0;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    if (TRACK) {
+      dmax = fmax(dmax, fabs(a[m].x - rint(a[m].x)));
+      dmax = fmax(dmax, fabs(a[m].y - rint(a[m].y)));
+    }
+    atomicAdd(acc_o + lane + 32 * m, fft::d2u_round(a[m].x) << sh);
+    atomicAdd(acc_o + lane + 32 * m + fft::kM, fft::d2u_round(a[m].y) << sh);
+  }
+  if (TRACK) atomicMax(worst, (unsigned long long)__double_as_longlong(dmax));
+}
+
+// A 16-byte read-only global load the compiler keeps in program order (an
+// __ldg is an invariant load that may be hoisted arbitrarily far, which turns
+// the BK ring below into 256 live registers).
+__device__ __forceinline__ double2 ldg_ordered(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// BK unit u = f * 4 + q of warp s: the four planes (r, q), r < 4, of frequency
+// slot fi = 4 s + f (bkt: [fi][plane][32] for this i, thread t added).
+template <int U>
+__device__ __forceinline__ void tm_bk_unit(const double2* bk_s, double2 (&b)[4]) {
+  constexpr int f = U >> 2, q = U & 3;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) b[r] = ldg_ordered(bk_s + ((size_t)f * 16 + r * 4 + q) * 32);
+}
+
+// Pointwise step of one quarter, warp s: frequency slots fi = 4 s .. 4 s + 3
+// of this thread's TMEM row, both slots; the 16 BK units stream through a ring
+// of PD + 1 register buffers (the first PD were requested by tm_bk_prefetch).
+template <int PD>
+struct TmRing {
+  double2 b[PD + 1][4];
+};
+template <int PD>
+__device__ __forceinline__ void tm_bk_prefetch(const double2* bk_s, TmRing<PD>& ring) {
+  if (PD > 0) tm_bk_unit<0>(bk_s, ring.b[0]);
+  if (PD > 1) tm_bk_unit<1>(bk_s, ring.b[1 % (PD + 1)]);
+  if (PD > 2) tm_bk_unit<2>(bk_s, ring.b[2 % (PD + 1)]);
+  if (PD > 3) tm_bk_unit<3>(bk_s, ring.b[3 % (PD + 1)]);
+}
+template <int PD, int U>
+__device__ __forceinline__ void tm_pw_unit(const double2* bk_s, TmRing<PD>& ring, const double2 (&D)[2][4],
+                                           uint32_t row_base, int fi) {
+  if (U + PD < 16) tm_bk_unit<(U + PD < 16 ? U + PD : 0)>(bk_s, ring.b[(U + PD) % (PD + 1)]);
+  constexpr int q = U & 3;
+  const double2(&b)[4] = ring.b[U % (PD + 1)];
+#pragma unroll
+  for (int sl = 0; sl < kTmSlots; ++sl) {
+    double2 c = fft::cmul(D[sl][0], b[0]);
+#pragma unroll
+    for (int r = 1; r < 4; ++r) {
+      c.x = fma(D[sl][r].x, b[r].x, fma(-D[sl][r].y, b[r].y, c.x));
+      c.y = fma(D[sl][r].x, b[r].y, fma(D[sl][r].y, b[r].x, c.y));
+    }
+    tm_st1(row_base + sl * 256 + q * 64 + 4 * fi, c);
+  }
+}
+// Slot fi = 4 s + F: the four digit spectra of both lanes are read into
+// registers first, so the four products can be written in place.  Both
+// slots are always computed (an idle slot's columns hold stale values that
+// nothing reads), so there is no data-dependent control flow here.
+template <int PD, int F>
+__device__ __forceinline__ void tm_pw_slot(const double2* bk_s, TmRing<PD>& ring, uint32_t row_base, int s) {
+  const int fi = 4 * s + F;
+  double2 D[2][4];
+#pragma unroll
+  for (int sl = 0; sl < kTmSlots; ++sl)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) tm_ld1(row_base + sl * 256 + r * 64 + 4 * fi, D[sl][r]);
+  tm_wait_ld();
+  tm_pw_unit<PD, 4 * F + 0>(bk_s, ring, D, row_base, fi);
+  tm_pw_unit<PD, 4 * F + 1>(bk_s, ring, D, row_base, fi);
+  tm_pw_unit<PD, 4 * F + 2>(bk_s, ring, D, row_base, fi);
+  tm_pw_unit<PD, 4 * F + 3>(bk_s, ring, D, row_base, fi);
+}
+template <int PD>
+__device__ __forceinline__ void tm_pointwise(const double2* bk_s, TmRing<PD>& ring, uint32_t row_base, int s) {
+  tm_pw_slot<PD, 0>(bk_s, ring, row_base, s);
+  tm_pw_slot<PD, 1>(bk_s, ring, row_base, s);
+  tm_pw_slot<PD, 2>(bk_s, ring, row_base, s);
+  tm_pw_slot<PD, 3>(bk_s, ring, row_base, s);
+}
+
+struct TmArgs {
+  GateSrc src;
+  const uint32_t* lanes;
+  const uint32_t* nlanes;
+  const double2* bkt;  // [n][16 fi][16 plane][32 t]
+  uint32_t* ext;
+  uint32_t ext_stride;
+  br::Geometry geo;
+  uint32_t stagger;  // ns of start delay per quarter index (phase offset)
+};
+
+__device__ __forceinline__ uint32_t tm_alloc_all(uint32_t* slot, int warp) {
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  return *slot;
+}
+__device__ __forceinline__ void tm_free_all(uint32_t tmem, int warp) {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// K3, TMEM engine: one persistent CTA of 16 warps per SM, four independent
+// quarter pipelines of two lanes each (see the file comment).
+template <int PD = kTmPrefetch>
+__global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
+  constexpr int N = fft::kN;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t tmem_slot;
+  const GateSrc& src = args.src;
+  const br::Geometry& geo = args.geo;
+  const uint32_t n = geo.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Q = warp & 3, s = warp >> 2, qt = s * 32 + lane;  // quarter, warp in quarter, thread in quarter
+  uint8_t* qb = smem + (size_t)Q * kTmQuarterBytes;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(qb);                     // [slot][c][N]
+  uint16_t* abar = reinterpret_cast<uint16_t*>(qb + kTmAccBytes);       // [slot][512]
+  double2* scratch = reinterpret_cast<double2*>(qb + kTmAccBytes + kTmAbarBytes) + s * fft::kRow;
+  double2* tw = reinterpret_cast<double2*>(smem + 4 * kTmQuarterBytes);
+  fft::make_tables2(tid, 512, tw, tw + fft::kTw2 * 32);
+  const uint32_t tmem = tm_alloc_all(&tmem_slot, warp);  // includes the table barrier
+  const uint32_t row_base = tmem + ((uint32_t)(32 * Q) << 16);
+
+  const uint32_t total = *args.nlanes;
+  const uint32_t nq = gridDim.x * 4, gq = blockIdx.x * 4 + Q;
+  const uint32_t first = (uint32_t)(((uint64_t)gq * total) / nq);
+  const uint32_t last = (uint32_t)(((uint64_t)(gq + 1) * total) / nq);
+  if (args.stagger && Q) __nanosleep(args.stagger * Q);
+  const int sl_f = s >> 1, c_f = s & 1;  // forward: slot, component (rows 2 c + j)
+  const int sl_i = s >> 1, o_i = s & 1;  // inverse: slot, output (rows 2 o + half)
+
+  for (uint32_t base = first; base < last; base += kTmSlots) {
+    const bool on[2] = {base < last, base + 1 < last};
+#pragma unroll
+    for (int sl = 0; sl < kTmSlots; ++sl) {
+      if (!on[sl]) continue;
+      const uint32_t e = args.lanes[base + sl];
+      const uint32_t gate = e & 0x7FFFFFFFu, hh = e >> 31;
+      const LaneForm f = lane_form(gate_op(src, gate), (int)hh);
+      bool n0, n1;
+      const uint32_t* x0 = gate_in(src, gate, 0, n0);
+      const uint32_t* x1 = gate_in(src, gate, f.j1, n1);
+      const uint32_t k0 = (uint32_t)(n0 ? -f.k0 : f.k0), k1 = (uint32_t)(n1 ? -f.k1 : f.k1);
+      for (uint32_t k = qt; k <= n; k += 128) {
+        uint32_t v = k0 * x0[k] + k1 * x1[k];
+        if (k == n) v += f.kappa;
+        abar[sl * 512 + k] = (uint16_t)br::modswitch(v, geo.lg2N);
+      }
+    }
+    tm_quarter_sync(Q);
+#pragma unroll
+    for (int sl = 0; sl < kTmSlots; ++sl) {
+      if (!on[sl]) continue;
+      const uint32_t bbar = abar[sl * 512 + n];
+      uint32_t* a = acc + sl * 2 * N;
+      for (int m = qt; m < N; m += 128) {
+        a[m] = 0;
+        a[N + m] = br::testvec_coeff(m, bbar, N);
+      }
+    }
+    tm_quarter_sync(Q);
+
+    for (uint32_t i = 0; i < n; ++i) {
+      // opaque per iteration: the lane-dependent addresses and table entries
+      // are recomputed inside each transform instead of being hoisted out of
+      // the CMux loop (which would hold ~40 more registers and spill)
+      int ln = lane;
+      double2 *scr = scratch, *twp = tw;
+      asm volatile("" : "+r"(ln), "+l"(scr), "+l"(twp));
+      if (sl_f ? on[1] : on[0]) {  // forward transforms of digit rows 2c, 2c + 1 of slot sl_f
+#pragma unroll 1
+        for (int j = 0; j < 2; ++j) {
+          const int w = 2 * c_f + j;
+          uint32_t u[32];
+          fbr_load_fields(geo, w, ln, acc + sl_f * 2 * N, abar[sl_f * 512 + i], u);
+          tm_forward_fields(u, (double)(1u << (geo.bg_bits - 1)), ln, twp, scr,
+                            row_base + sl_f * 256 + w * 64);
+        }
+      }
+      const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + ln;
+      TmRing<PD> ring;
+      tm_bk_prefetch<PD>(bk_s, ring);
+      tm_wait_st();
+      tm_quarter_sync(Q);
+      tm_pointwise<PD>(bk_s, ring, row_base, s);
+      tm_wait_st();
+      tm_quarter_sync(Q);
+      if (sl_i ? on[1] : on[0]) {  // inverse transforms of outputs (o, hi), (o, lo) of slot sl_i
+        uint32_t* acc_o = acc + (sl_i * 2 + o_i) * N;
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half)
+          tm_inverse_acc<false>(row_base + sl_i * 256 + (2 * o_i + half) * 64, ln, twp, scr, acc_o,
+                                half ? 0 : 16, nullptr);
+      }
+      tm_quarter_sync(Q);  // ACC complete before the next digits
+    }
+
+#pragma unroll
+    for (int sl = 0; sl < kTmSlots; ++sl) {
+      if (!on[sl]) continue;
+      const uint32_t* a = acc + sl * 2 * N;
+      const uint32_t le = args.lanes[base + sl];  // gate | h << 31
+      uint32_t* e = args.ext + (size_t)(2 * (le & 0x7FFFFFFFu) + (le >> 31)) * args.ext_stride;
+      for (int m = qt; m <= N; m += 128) {
+        uint32_t v;
+        if (m == 0) v = a[0];
+        else if (m < N) v = 0u - a[N - m];
+        else v = a[N];
+        e[m] = v;
+      }
+    }
+    tm_quarter_sync(Q);
+  }
+  tm_free_all(tmem, warp);
+}
+
+// K1 for the TMEM engine: BK poly (i, w, o) half -> the TRUE spectrum (the v1
+// transform: no scaling) / 512, scattered to [i][fi][plane][t] with the
+// frequency of (thread t, slot fi) in dft512_v2's register layout as
+// tm_store_spectrum places it: (k2, h) = (t >> 1, t & 1), j = fi >> 1,
+// k = k2 + 16 (8 h + j) for even fi (x[j]), k2 + 16 (16 + 8 h + j) for odd
+// fi (y[j]).  The pointwise product of a (scaled) digit
+// spectrum D' = s_p D with it is s_p (D B) / 512, the input inverse_tr
+// expects.
+__global__ void bk_tm_kernel(const uint32_t* bk, double2* out, uint32_t polys) {
+  __shared__ double2 row[fft::kRow];
+  __shared__ double2 tw[2 * 512];
+  const uint32_t item = blockIdx.x, poly = item >> 1, half = item & 1;
+  if (poly >= polys) return;
+  const int lane = threadIdx.x;
+  fft::make_tables(lane, 32, tw, tw + 512);
+  __syncwarp();
+  const uint32_t* b = bk + (size_t)poly * fft::kN;
+  double re[16], im[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int32_t v0 = (int32_t)b[lane + 32 * m], v1 = (int32_t)b[lane + 32 * m + 512];
+    const int32_t l0 = (int16_t)(v0 & 0xFFFF), l1 = (int16_t)(v1 & 0xFFFF);
+    re[m] = half ? (double)l0 : (double)((v0 - l0) >> 16);
+    im[m] = half ? (double)l1 : (double)((v1 - l1) >> 16);
+  }
+  fft::forward(re, im, lane, tw, row);
+  __syncwarp();
+  const uint32_t i = poly >> 3, plane = (poly & 7) * 2 + half;
+  for (int e = lane; e < fft::kM; e += 32) {
+    const int fi = e >> 5, t = e & 31, k2 = t >> 1, h = t & 1;
+    const int j = fi >> 1;
+    const int k = (fi & 1) ? k2 + 16 * (16 + 8 * h + j) : k2 + 16 * (8 * h + j);
+    const double2 v = row[fft::fpos(k)];
+    out[(((size_t)i * 16 + fi) * 16 + plane) * 32 + t] = make_double2(v.x * (1.0 / 512), v.y * (1.0 / 512));
+  }
+}
+
+// Test instrumentation (she_fft_product_selftest, variant 4): the TMEM
+// engine's CMux product on caller-given digit rows and BK rows, on its own
+// device functions (tm_forward_fields, tm_pointwise, tm_inverse_acc): quarter
+// Q of CTA b runs case 4 b + Q in slot 0 (warp s: forward of digit row s,
+// inverse of output (s >> 1, s & 1)).
+__global__ void __launch_bounds__(512, 1) fft_selftest_tm_kernel(const int32_t* digits, const double2* bkt,
+                                                                 uint32_t* out, unsigned long long* worst,
+                                                                 uint32_t count) {
+  constexpr int N = fft::kN;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Q = warp & 3, s = warp >> 2, qt = s * 32 + lane;
+  uint8_t* qb = smem + (size_t)Q * kTmQuarterBytes;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(qb);
+  double2* scratch = reinterpret_cast<double2*>(qb + kTmAccBytes + kTmAbarBytes) + s * fft::kRow;
+  double2* tw = reinterpret_cast<double2*>(smem + 4 * kTmQuarterBytes);
+  fft::make_tables2(tid, 512, tw, tw + fft::kTw2 * 32);
+  const uint32_t tmem = tm_alloc_all(&tmem_slot, warp);
+  const uint32_t row_base = tmem + ((uint32_t)(32 * Q) << 16);
+  const uint32_t c = blockIdx.x * 4 + Q;
+  const bool active = c < count;
+  if (active) {
+    for (int m = qt; m < 2 * N; m += 128) acc[m] = 0;
+    const int32_t* d = digits + ((size_t)c * 4 + s) * N;
+    uint32_t uu[32];
+#pragma unroll
+    for (int j2 = 0; j2 < 32; ++j2) uu[j2] = (uint32_t)(d[lane + 32 * j2] + 2048);
+    tm_forward_fields(uu, 2048.0, lane, tw, scratch, row_base + s * 64);
+  }
+  const double2* bk_s = bkt + ((size_t)c * 16 + 4 * s) * 16 * 32 + lane;
+  TmRing<kTmPrefetch> ring;
+  if (active) tm_bk_prefetch<kTmPrefetch>(bk_s, ring);
+  tm_wait_st();
+  tm_quarter_sync(Q);
+  if (active) tm_pointwise<kTmPrefetch>(bk_s, ring, row_base, s);
+  tm_wait_st();
+  tm_quarter_sync(Q);
+  if (active)
+    tm_inverse_acc<true>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, worst);
+  tm_quarter_sync(Q);
+  if (active)
+    for (int m = qt; m < 2 * N; m += 128) out[(size_t)c * 2 * N + m] = acc[m];
+  tm_free_all(tmem, warp);
+}

@@ -356,6 +356,7 @@ struct FftVar<3> {  // v2's tables and scaling, DIT/FMA DFT16s (fft_core.cuh)
 };
 constexpr int kFftDefaultVariant = 2;
 constexpr int kFftDefaultStreams = 1;  // br_fft_kernel (1) or the two-stream br_fft2s_kernel (2)
+constexpr int kFftDefaultStore = 1;    // spectra in shared memory (1) or tensor memory (2)
 template <int V>
 constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double2); }
 
@@ -801,6 +802,8 @@ __global__ void __launch_bounds__(256, 1) br_fft2s_kernel(BRFArgs args) {
     __syncthreads();
   }
 }
+
+#include "br_tmem.cuh"
 
 // K1 for the FP64 engine: BK poly (i, w, o) -> two planes (halves), forward
 // FFT, 1/512 folded.  One warp per (poly, half).
@@ -1452,7 +1455,10 @@ struct she_ctx {
   int fft_grp = 1;                 // independent lane groups per CTA (br_fft_kernel GRP)
   int fft_pre = 16;                // BK planes prefetched before the pre-pointwise barrier
   int fft_streams = 1;             // 2: br_fft2s_kernel (two lanes per warp, skewed)
-  double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain
+  int fft_store = kFftDefaultStore;  // 1: spectra in shared memory, 2: in TMEM (br_fft_tm_kernel)
+  uint32_t fft_stagger = 0;          // TMEM engine: start delay per quarter (ns)
+  double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain (shared-memory engine)
+  double2* bkt = nullptr;  // [n][16 fi][16 plane][32] the same for the TMEM engine
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
   // key switch on the tensor cores (ks_imma.cuh; base 4, t = 8): mma.sync
   // (IMMA) or, ksi_tc, tcgen05 kind::i8 with the accumulator in TMEM
@@ -1546,7 +1552,15 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
   }
-  if (ctx->fft_g && S::N == fft::kN) {  // FFT engine: BK halves in the FFT domain
+  if (ctx->fft_g && S::N == fft::kN && ctx->fft_store == 2) {  // TMEM engine
+    ctx->bk_bytes = (size_t)p.n * 16 * fft::kM * sizeof(double2);
+    CK(cudaMalloc(&ctx->bkt, ctx->bk_bytes));
+    bk_tm_kernel<<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkt, (uint32_t)polys);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaFuncSetAttribute(br_fft_tm_kernel<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kTmSmemBytes));
+  } else if (ctx->fft_g && S::N == fft::kN) {  // FFT engine: BK halves in the FFT domain
     ctx->bk_bytes = (size_t)p.n * 16 * fft::kM * sizeof(double2);
     CK(cudaMalloc(&ctx->bkf, ctx->bk_bytes));
     if (ctx->fft_v == 1)
@@ -1678,6 +1692,37 @@ she_status launch_br_fft2s(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cuda
   return SHE_OK;
 }
 
+she_status launch_br_fft_tm(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
+  TmArgs f;
+  f.src = a.src;
+  f.lanes = a.lanes;
+  f.nlanes = a.nlanes;
+  f.bkt = ctx->bkt;
+  f.ext = a.ext;
+  f.ext_stride = a.ext_stride;
+  f.geo = a.geo;
+  f.stagger = ctx->fft_stagger;
+  cudaLaunchConfig_t cfg = {};
+  // four two-lane quarter pipelines per CTA, one CTA per SM
+  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>((max_lanes + 7) / 8, (size_t)ctx->sms)));
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = kTmSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (ctx->persist) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = ctx->bkt;
+    attr[0].val.accessPolicyWindow.num_bytes = ctx->window_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = ctx->window_hit;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  CK(cudaLaunchKernelEx(&cfg, br_fft_tm_kernel<>, f));
+  return SHE_OK;
+}
+
 template <int G, int B, int V, int GRP = 1, int PRE = 16>
 she_status launch_br_fft(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cudaStream_t stream) {
   BRFArgs f;
@@ -1803,7 +1848,9 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     a.geo = ctx->geo;
     if (ctx->timing) mark(ctx, stream);
     st = fail(SHE_ERR_STATE, "no blind-rotation kernel for config %dx%d", ctx->br_g, ctx->br_b);
-    if (ctx->bkf && S::N == fft::kN) {
+    if (ctx->bkt && S::N == fft::kN) {
+      st = launch_br_fft_tm(ctx, a, 2 * cnt, stream);
+    } else if (ctx->bkf && S::N == fft::kN) {
       st = ctx->fft_streams == 2 ? launch_br_fft2s(ctx, a, 2 * cnt, stream)
            : ctx->fft_v == 1   ? launch_br_fft<4, 1, 1>(ctx, a, 2 * cnt, stream)
            : ctx->fft_v == 3 && ctx->fft_g == 5 ? launch_br_fft<5, 1, 3, 1, 0>(ctx, a, 2 * cnt, stream)
@@ -1911,6 +1958,12 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   if (o.fft_streams == 2 && (!use_fft || (o.fft_lanes && o.fft_lanes != 4) || o.fft_groups == 2 ||
                              (o.fft_variant && o.fft_variant != 2) || o.fft_prefetch >= 2))
     return fail(SHE_ERR_ARG, "fft_streams = 2 is instantiated for 4 lanes, variant 2");
+  if (o.fft_store < 0 || o.fft_store > 2) return fail(SHE_ERR_ARG, "fft_store=%d", o.fft_store);
+  if (o.fft_store == 2 && (!use_fft || o.fft_lanes || o.fft_variant > 2 || o.fft_variant == 1 ||
+                           o.fft_groups || o.fft_prefetch || o.fft_streams))
+    return fail(SHE_ERR_ARG, "fft_store = 2 (TMEM engine) has its own shape: no lane/group/prefetch/stream options");
+  if (o.fft_stagger_ns < 0 || o.fft_stagger_ns > 100000)
+    return fail(SHE_ERR_ARG, "fft_stagger_ns=%d", o.fft_stagger_ns);
   if (o.fft_prefetch < 0 || o.fft_prefetch > 3)
     return fail(SHE_ERR_ARG, "fft_prefetch=%d", o.fft_prefetch);
   if (o.fft_prefetch >= 2 && (o.fft_groups == 2 || o.fft_variant == 1 ||
@@ -1939,6 +1992,8 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   ctx->fft_v = o.fft_variant ? o.fft_variant : kFftDefaultVariant;
   ctx->fft_grp = o.fft_groups ? o.fft_groups : 1;
   ctx->fft_streams = o.fft_streams ? o.fft_streams : kFftDefaultStreams;
+  ctx->fft_store = use_fft ? (o.fft_store ? o.fft_store : kFftDefaultStore) : 1;
+  ctx->fft_stagger = (uint32_t)o.fft_stagger_ns;
   ctx->fft_pre = o.fft_prefetch == 0 ? 16 : o.fft_prefetch == 3 ? 0 : o.fft_prefetch == 2 ? 8 : 16;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
@@ -2028,6 +2083,7 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaDeviceSynchronize();
   cudaFree(ctx->bk);
   cudaFree(ctx->bkf);
+  cudaFree(ctx->bkt);
 
   cudaFree(ctx->ksk);
   cudaFree(ctx->ksi_bt);
@@ -2151,7 +2207,7 @@ she_status she_bench_fp64_peak(int device, double* ops_per_s, double* ms) {
 
 she_status she_ctx_br_engine(const she_ctx* ctx, int* fft_lanes) {
   if (!ctx || !fft_lanes) return fail(SHE_ERR_ARG, "null argument");
-  *fft_lanes = ctx->bkf ? ctx->fft_g : 0;
+  *fft_lanes = ctx->bkt ? 2 : ctx->bkf ? ctx->fft_g : 0;
   return SHE_OK;
 }
 
@@ -2230,8 +2286,8 @@ she_status she_fft_product_selftest(int device, int variant, const int32_t* digi
                                     double* worst_distance) {
   if (count == 0) return SHE_OK;
   if (!digits || !bk || !out) return fail(SHE_ERR_ARG, "NULL argument");
-  if (variant < 0 || variant > 3) return fail(SHE_ERR_ARG, "variant=%d", variant);
-  const int V = variant ? variant : kFftDefaultVariant;
+  if (variant < 0 || variant > 4) return fail(SHE_ERR_ARG, "variant=%d", variant);
+  const int V = variant ? variant : kFftDefaultVariant;  // 4: the TMEM engine (br_tmem.cuh)
   if (count > 65535) return fail(SHE_ERR_ARG, "count > 65535");
   constexpr size_t N = fft::kN;
   CK(cudaSetDevice(device));
@@ -2248,7 +2304,18 @@ she_status she_fft_product_selftest(int device, int variant, const int32_t* digi
   if (e == cudaSuccess) e = cudaMemset(dworst, 0, 8);
   if (e == cudaSuccess) e = cudaMemcpy(dd, digits, count * 4 * N * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(db, bk, count * 8 * N * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) {  // the setup transform of the engine (BK -> FFT domain, halves)
+  if (e == cudaSuccess && V == 4) {  // the TMEM engine's setup transform and product
+    bk_tm_kernel<<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
+    e = cudaGetLastError();
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fft_selftest_tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kTmSmemBytes);
+    if (e == cudaSuccess) {
+      fft_selftest_tm_kernel<<<(unsigned)((count + 3) / 4), 512, kTmSmemBytes>>>(dd, dbkf, dout, dworst,
+                                                                                (uint32_t)count);
+      e = cudaGetLastError();
+    }
+  } else if (e == cudaSuccess) {  // the setup transform of the engine (BK -> FFT domain, halves)
     if (V == 1) bk_fft_kernel<1><<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
     else if (V == 3) bk_fft_kernel<3><<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
     else bk_fft_kernel<2><<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
@@ -2257,9 +2324,9 @@ she_status she_fft_product_selftest(int device, int variant, const int32_t* digi
   constexpr size_t smem = (4 * fft::kRow + 2 * 512) * sizeof(double2) + 2 * N * 4;
   auto selftest = V == 1 ? fft_selftest_kernel<1> : V == 3 ? fft_selftest_kernel<3>
                                                             : fft_selftest_kernel<2>;
-  if (e == cudaSuccess)
+  if (e == cudaSuccess && V != 4)
     e = cudaFuncSetAttribute(selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) {
+  if (e == cudaSuccess && V != 4) {
     selftest<<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
     e = cudaGetLastError();
   }
@@ -2438,7 +2505,7 @@ she_status she_lvl_selectors_to_device(she_ctx* ctx, const uint32_t* sel, size_t
                                        void* out, void* stream) {
   if (count == 0) return SHE_OK;
   if (!ctx || !sel || !out) return fail(SHE_ERR_ARG, "NULL argument");
-  if (!ctx->bkf) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
+  if (!ctx->fft_g) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
   std::lock_guard<std::mutex> lk(ctx->mu);
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -2471,7 +2538,7 @@ she_status she_lvl_cmux_batch(she_ctx* ctx, const void* sel, const uint32_t* sel
                               void* stream) {
   if (count == 0) return SHE_OK;
   if (!ctx || !sel || !sel_idx || !d1 || !d0 || !out) return fail(SHE_ERR_ARG, "NULL argument");
-  if (!ctx->bkf) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
+  if (!ctx->fft_g) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
   if (count > 0x7FFFFFFFull) return fail(SHE_ERR_ARG, "count too large");
   const size_t bytes = count * 2 * ctx->p.N * 4;
   if (overlaps(out, bytes, d1, bytes) || overlaps(out, bytes, d0, bytes))
@@ -2496,7 +2563,7 @@ she_status she_lvl_unit(she_ctx* ctx, int op, const void* sel, const uint32_t* x
   if (count == 0) return SHE_OK;
   if (!ctx || !sel || !x_sel || !out || (op != SHE_LVL_RELU && !y_sel))
     return fail(SHE_ERR_ARG, "NULL argument");
-  if (!ctx->bkf) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
+  if (!ctx->fft_g) return fail(SHE_ERR_STATE, "the leveled mode runs on the FFT engine (N = 1024)");
   // ---- the CMux program (host): slots 0 = TRUE, 1 = FALSE; lit bit 31 = NOT
   constexpr uint32_t T = 0, F = 1, NEG = 0x80000000u;
   struct Item { uint32_t sel, in1, in0, out; };

@@ -184,6 +184,16 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
   return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
 }
 
+// W128[e] read at its point of use: the index carries an opaque zero, so the
+// compiler cannot hoist the constant-bank loads of a whole transform out of
+// the CMux loop into (spilled) registers; the load is one LDC per use, served
+// by the constant cache.
+__device__ __forceinline__ double2 cw(int e) {
+  int z;
+  asm volatile("mov.u32 %0, %%laneid;\n\tshr.u32 %0, %0, 5;" : "=r"(z));
+  return c_w128[e + z];
+}
+
 // a * W128[e]^SIGN for a compile-time e (after unrolling)
 template <int SIGN>
 __device__ __forceinline__ double2 rot(double2 a, int e) {
@@ -192,7 +202,7 @@ __device__ __forceinline__ double2 rot(double2 a, int e) {
   if (e == 64) return make_double2(-a.x, -a.y);
   if (e == 32) return SIGN > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
   if (e == 96) return SIGN > 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
-  return SIGN > 0 ? cmul(a, c_w128[e]) : cmulc(a, c_w128[e]);
+  return SIGN > 0 ? cmul(a, cw(e)) : cmulc(a, cw(e));
 }
 
 __device__ __forceinline__ constexpr int brev4(int k) {
@@ -250,7 +260,7 @@ __device__ __forceinline__ void dft16_dit(double2 (&a)[16]) {
           x = make_double2(u.x + v.y, u.y - v.x);
           y = make_double2(u.x - v.y, u.y + v.x);
         } else {
-          const double2 w = c_w128[e];
+          const double2 w = cw(e);
           x.x = fma(w.x, v.x, fma(-w.y, v.y, u.x));
           x.y = fma(w.x, v.y, fma(w.y, v.x, u.y));
           y.x = fma(2.0, u.x, -x.x);
@@ -332,8 +342,8 @@ __device__ __forceinline__ void inverse(const double2* row_in, int lane, const d
   const int h = lane & 1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {  // untwist zeta^(-16 k1) = conj(W128[k1])
-    x[j] = cmulc(x[j], c_w128[8 * h + j]);
-    y[j] = cmulc(y[j], c_w128[16 + 8 * h + j]);
+    x[j] = cmulc(x[j], cw(8 * h + j));
+    y[j] = cmulc(y[j], cw(16 + 8 * h + j));
   }
 }
 
@@ -415,7 +425,9 @@ __device__ __forceinline__ void dft512_v2(double2 (&a)[16], int lane, const doub
     scratch[tslot(lane, k2 + 8)] = cmul(a[brev4(k2 + 8)], cmul(p, r8));
   }
   __syncwarp();
-  const int k2 = lane >> 1, h = lane & 1;
+  const int k2 = lane >> 1;
+  int h = lane & 1;
+  asm volatile("" : "+r"(h));  // opaque: the selected constants below stay per call (no hoisting)
 #pragma unroll
   for (int m = 0; m < 16; ++m) a[m] = scratch[tslot(2 * m + h, k2)];
   dft16<SIGN>(a);
@@ -426,11 +438,7 @@ __device__ __forceinline__ void dft512_v2(double2 (&a)[16], int lane, const doub
     r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
     r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
     // c0 = w32^(SIGN j), c1 = w32^(-SIGN (8 + j)): compile-time constants
-    const double2 c0 = c_w128[(SIGN * 4 * j) & 127];
-    const double2 c1 = c_w128[(-SIGN * 4 * (8 + j)) & 127];
-    double2 c;
-    c.x = h ? c1.x : c0.x;
-    c.y = h ? c1.y : c0.y;
+    const double2 c = cw(h ? (-SIGN * 4 * (8 + j)) & 127 : (SIGN * 4 * j) & 127);  // one constant-cache load, two addresses per warp
     const double2 t = cmul(r, c);
     x[j] = cadd(keep, t);
     y[j] = csub(keep, t);
@@ -469,8 +477,8 @@ __device__ __forceinline__ void inverse_v2(const double2* row_in, int lane, cons
   const int h = lane & 1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    x[j] = cmulc(x[j], c_w128[h ? 40 + 5 * j : j]);
-    y[j] = cmulc(y[j], c_w128[h ? (5 * j - 8) & 127 : 16 + j]);
+    x[j] = cmulc(x[j], cw(h ? 40 + 5 * j : j));
+    y[j] = cmulc(y[j], cw(h ? (5 * j - 8) & 127 : 16 + j));
   }
 }
 
@@ -502,11 +510,7 @@ __device__ __forceinline__ void v2_exchange(const double2 (&a)[16], int lane, do
     double2 r;
     r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
     r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
-    const double2 c0 = c_w128[(SIGN * 4 * j) & 127];
-    const double2 c1 = c_w128[(-SIGN * 4 * (8 + j)) & 127];
-    double2 c;
-    c.x = h ? c1.x : c0.x;
-    c.y = h ? c1.y : c0.y;
+    const double2 c = cw(h ? (-SIGN * 4 * (8 + j)) & 127 : (SIGN * 4 * j) & 127);  // one constant-cache load, two addresses per warp
     const double2 t = cmul(r, c);
     x[j] = cadd(keep, t);
     y[j] = csub(keep, t);
@@ -534,8 +538,8 @@ __device__ __forceinline__ void v2_inv_untwist(int lane, double2 (&x)[8], double
   const int h = lane & 1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    x[j] = cmulc(x[j], c_w128[h ? 40 + 5 * j : j]);
-    y[j] = cmulc(y[j], c_w128[h ? (5 * j - 8) & 127 : 16 + j]);
+    x[j] = cmulc(x[j], cw(h ? 40 + 5 * j : j));
+    y[j] = cmulc(y[j], cw(h ? (5 * j - 8) & 127 : 16 + j));
   }
 }
 
@@ -563,11 +567,7 @@ __device__ __forceinline__ void dft512_v3(double2 (&a)[16], int lane, const doub
     r.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
     r.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
     // c0 = w32^(SIGN j), c1 = w32^(-SIGN (8 + j)): compile-time constants
-    const double2 c0 = c_w128[(SIGN * 4 * j) & 127];
-    const double2 c1 = c_w128[(-SIGN * 4 * (8 + j)) & 127];
-    double2 c;
-    c.x = h ? c1.x : c0.x;
-    c.y = h ? c1.y : c0.y;
+    const double2 c = cw(h ? (-SIGN * 4 * (8 + j)) & 127 : (SIGN * 4 * j) & 127);  // one constant-cache load, two addresses per warp
     // x = keep + c r (4 DFMA), y = 2 keep - x (2 DFMA)
     x[j].x = fma(c.x, r.x, fma(-c.y, r.y, keep.x));
     x[j].y = fma(c.x, r.y, fma(c.y, r.x, keep.y));
@@ -608,9 +608,78 @@ __device__ __forceinline__ void inverse_v3(const double2* row_in, int lane, cons
   const int h = lane & 1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    x[j] = cmulc(x[j], c_w128[h ? 40 + 5 * j : j]);
-    y[j] = cmulc(y[j], c_w128[h ? (5 * j - 8) & 127 : 16 + j]);
+    x[j] = cmulc(x[j], cw(h ? 40 + 5 * j : j));
+    y[j] = cmulc(y[j], cw(h ? (5 * j - 8) & 127 : 16 + j));
   }
+}
+
+// ---- the register-layout inverse of the TMEM engine -------
+// In-register 16-point DFT by radix-2 decimation in time on bit-reversed
+// input: a[brev4(k)] = X[k] on entry, a[n] = sum_k X[k] w16^(SIGN n k) on
+// exit (the inverse pairing of dft16: dft16<+1> then dft16_dit_br<-1> is 16x
+// the identity).
+template <int SIGN>
+__device__ __forceinline__ void dft16_dit_br(double2 (&a)[16]) {
+#pragma unroll
+  for (int s = 1; s <= 8; s <<= 1) {
+#pragma unroll
+    for (int g0 = 0; g0 < 16; g0 += 2 * s) {
+#pragma unroll
+      for (int j = 0; j < s; ++j) {
+        const double2 u = a[g0 + j], v = rot<SIGN>(a[g0 + j + s], j * (64 / s));  // w_(2s)^(SIGN j)
+        a[g0 + j] = cadd(u, v);
+        a[g0 + j + s] = csub(u, v);
+      }
+    }
+  }
+}
+
+// Exact step-by-step inverse (unnormalised: 512 x) of the v2 forward
+// transform, taking the spectrum in the REGISTER layout dft512_v2<1> leaves it
+// in -- thread (k2, h) = (lane >> 1, lane & 1), x[j] / y[j] at frequencies
+// k2 + 16 (8h + j) / k2 + 16 (16 + 8h + j), thread 1's values scaled by
+// sigma / -sigma (see dft512_v2) -- and returning the natural layout
+// a[n2] = (c_n + i c_{n+512}) for n = lane + 32 n2, untwisted.  The steps, in
+// reverse order of the forward:
+//   pair step   keep = x + y (= 2 keep'), r = (x - y) conj(c) (= 2 r'), the
+//               partner's r is this thread's a[brev(8 + j)];
+//   pass B      DIT DFT16 (conjugate) on the bit-reversed registers;
+//   transpose   back through the warp's scratch row (the forward's swizzle);
+//   pass A      conj(pass-A twiddle) from the forward table, DIT DFT16;
+//   twist       conj(w64^n2) (the forward's table carries zeta^lane).
+// Because the spectrum never leaves the registers in the forward's layout,
+// the inverse needs no shared-memory input row and its output is in natural
+// order (consecutive lanes, consecutive coefficients).
+__device__ __forceinline__ void inverse_tr(const double2 (&x)[8], const double2 (&y)[8], int lane,
+                                           const double2* tw, double2* scratch, double2 (&a)[16]) {
+  const int k2 = lane >> 1;
+  int h = lane & 1;
+  asm volatile("" : "+r"(h));  // opaque: keeps the 8 selected constants out of loop-invariant hoisting
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double2 c = cw(h ? (-4 * (8 + j)) & 127 : (4 * j) & 127);  // one constant-cache load, two addresses per warp
+    const double2 t = cmulc(csub(x[j], y[j]), c);
+    double2 r;
+    r.x = __shfl_xor_sync(0xffffffffu, t.x, 1);
+    r.y = __shfl_xor_sync(0xffffffffu, t.y, 1);
+    a[brev4(j)] = cadd(x[j], y[j]);
+    a[brev4(8 + j)] = r;
+  }
+  dft16_dit_br<-1>(a);
+#pragma unroll
+  for (int m = 0; m < 16; ++m) scratch[tslot(2 * m + h, k2)] = a[m];
+  __syncwarp();
+  const double2 r8 = tw[8 * 32 + lane];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 p = tw[k * 32 + lane];
+    a[brev4(k)] = cmulc(scratch[tslot(lane, k)], p);
+    a[brev4(k + 8)] = cmulc(scratch[tslot(lane, k + 8)], cmul(p, r8));
+  }
+  __syncwarp();  // scratch reads done before the caller reuses the row
+  dft16_dit_br<-1>(a);
+#pragma unroll
+  for (int m = 1; m < 16; ++m) a[m] = rot<-1>(a[m], 2 * m);  // conj(w64^m)
 }
 
 // sigma(k)^-2 of the v2 forward (BK setup): w16^(k1) for k1 & 8, 1 otherwise.

@@ -206,7 +206,7 @@ def test_ctx_options_reserved_and_params_checked():
     P = si.C0
     _, ck = she.she_keygen(P, 5)
     opt = she.she_ctx_options.of()
-    opt.reserved[2] = 1
+    opt.reserved[0] = 1
     h = ctypes.c_void_p()
     st = she.lib().she_ctx_create_ex(ctypes.byref(she.she_params.of(P)), ck.handle, 0, 0, 1,
                                      ctypes.byref(opt), ctypes.byref(h))

@@ -293,12 +293,14 @@ ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3
                "ks-tcgen05": dict(ks_kernel="tcgen05"),
                "fft-2streams": dict(engine="fft", fft_streams=2),
                "fft-v3": dict(engine="fft", fft_variant=3),
-               "fft5-v3": dict(engine="fft", fft_lanes=5, fft_prefetch=3, fft_variant=3)}
+               "fft5-v3": dict(engine="fft", fft_lanes=5, fft_prefetch=3, fft_variant=3),
+               "fft-tmem": dict(engine="fft", fft_store="tmem"),
+               "fft-tmem-stagger": dict(engine="fft", fft_store="tmem", fft_stagger_ns=20000)}
 
 
 @pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2", "fft-v1", "fft-2groups",
                                     "fft5-noprefetch", "ks-imma", "ks-cuda", "fft-v3", "fft5-v3",
-                                    "ks-tcgen05", "fft-2streams"])
+                                    "ks-tcgen05", "fft-2streams", "fft-tmem", "fft-tmem-stagger"])
 def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with 4 lanes per
     CTA; the Goldilocks NTT engine (she_ctx_options.br_engine = 2) and the other
@@ -311,7 +313,7 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
     assert she.br_engine(ctx) == {"ntt": 0, "fft3": 3, "fft2x2": 2, "fft-v1": 4,
                                   "fft-2groups": 4, "fft5-noprefetch": 5, "ks-imma": 4,
                                   "ks-cuda": 4, "fft-v3": 4, "fft5-v3": 5, "ks-tcgen05": 4,
-                                  "fft-2streams": 4}[engine]
+                                  "fft-2streams": 4, "fft-tmem": 2, "fft-tmem-stagger": 2}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
     she.she_gate_batch_ops(ctx, dev(np.asarray(ops, np.uint8)), dev(a), dev(b), dev(c), out)
