@@ -320,12 +320,9 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
     tm_quarter_sync(Q);
 
     for (uint32_t i = 0; i < n; ++i) {
-      // opaque per iteration: the lane-dependent addresses and table entries
-      // are recomputed inside each transform instead of being hoisted out of
-      // the CMux loop (which would hold ~40 more registers and spill)
-      int ln = lane;
-      double2 *scr = scratch, *twp = tw;
-      asm volatile("" : "+r"(ln), "+l"(scr), "+l"(twp));
+      const int ln = lane;
+      double2* const scr = scratch;
+      const double2* const twp = tw;
       if (sl_f ? on[1] : on[0]) {  // forward transforms of digit rows 2c, 2c + 1 of slot sl_f
 #pragma unroll 1
         for (int j = 0; j < 2; ++j) {
