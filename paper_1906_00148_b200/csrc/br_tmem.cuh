@@ -82,6 +82,22 @@ __device__ __forceinline__ void tm_ld1(uint32_t addr, double2& v) {
                : "memory");
   v = make_double2(__hiloint2double(r1, r0), __hiloint2double(r3, r2));
 }
+__device__ __forceinline__ void tm_st_u16(uint32_t addr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tm_ld_u16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr)
+      : "memory");
+}
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // Barrier over the 128 threads of quarter Q (id 1 + Q) with the tcgen05
@@ -112,6 +128,28 @@ __device__ __forceinline__ void tm_load_spectrum(uint32_t addr, double2 (&x)[8],
     y[2 * p] = v[p][1];
     x[2 * p + 1] = v[p][2];
     y[2 * p + 1] = v[p][3];
+  }
+}
+
+// Digit fields of BOTH rows (c, j = 0) and (c, j = 1) of ACC_c from one pass
+// over the rotation (X^a P)[m] - P[m] + offset (fbr_load_fields, R8): the
+// j = 0 fields in u0, the j = 1 fields packed two per register (bg_bits <= 12
+// on the FFT engine) for the second transform.
+__device__ __forceinline__ void tm_load_fields2(const br::Geometry& g, int lane, const uint32_t* P, uint32_t a,
+                                                uint32_t (&u0)[32], uint32_t (&pk1)[16]) {
+  constexpr int N = fft::kN;
+  const uint32_t sh0 = 32 - g.bg_bits, sh1 = 32 - 2 * g.bg_bits, mask = (1u << g.bg_bits) - 1;
+#pragma unroll
+  for (int j2 = 0; j2 < 32; ++j2) {
+    const uint32_t m = lane + 32 * j2;
+    const uint32_t idx = (m - a) & (2 * N - 1);  // (X^a P)[m] = +-P[m - a]
+    uint32_t v = P[idx & (N - 1)];
+    if (idx >= (uint32_t)N) v = 0u - v;
+    const uint32_t y = v - P[m] + g.dec_offset;
+    u0[j2] = y >> sh0;
+    const uint32_t f1 = (y >> sh1) & mask;
+    if (j2 & 1) pk1[j2 >> 1] |= f1 << 16;
+    else pk1[j2 >> 1] = f1;
   }
 }
 
@@ -324,14 +362,30 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       double2* const scr = scratch;
       const double2* const twp = tw;
       if (sl_f ? on[1] : on[0]) {  // forward transforms of digit rows 2c, 2c + 1 of slot sl_f
-#pragma unroll 1
-        for (int j = 0; j < 2; ++j) {
-          const int w = 2 * c_f + j;
-          uint32_t u[32];
-          fbr_load_fields(geo, w, ln, acc + sl_f * 2 * N, abar[sl_f * 512 + i], u);
-          tm_forward_fields(u, (double)(1u << (geo.bg_bits - 1)), ln, twp, scr,
-                            row_base + sl_f * 256 + w * 64);
+        // both rows' digit fields from one rotation pass; the j = 1 fields wait
+        // in the (not yet written) TMEM columns of row 2c + 1 during the first
+        // transform instead of in 16 registers
+        const uint32_t row0 = row_base + sl_f * 256 + (2 * c_f) * 64, row1 = row0 + 64;
+        uint32_t u[32];
+        {
+          uint32_t pk1[16];
+          tm_load_fields2(geo, ln, acc + (sl_f * 2 + c_f) * N, abar[sl_f * 512 + i], u, pk1);
+          tm_st_u16(row1, pk1);
         }
+        const double half = (double)(1u << (geo.bg_bits - 1));
+        tm_forward_fields(u, half, ln, twp, scr, row0);
+        {
+          uint32_t pk1[16];
+          tm_wait_st();  // this thread's stash store (long done) before reading it back
+          tm_ld_u16(row1, pk1);
+          tm_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            u[2 * k] = pk1[k] & 0xFFFFu;
+            u[2 * k + 1] = pk1[k] >> 16;
+          }
+        }
+        tm_forward_fields(u, half, ln, twp, scr, row1);
       }
       const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + ln;
       TmRing<PD> ring;
