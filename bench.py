@@ -52,7 +52,13 @@ FP64_OPS_PER_CMUX = 8 * 17_920 + 512 * 4 * 16
 # §4.2b), so the fraction measures useful work per second whichever transform
 # runs.  FP64 instructions the default transform (v2, §4.2c) actually executes
 # per CMux and lane, from ncu (profiles/r2/: DADD + DMUL + DFMA / lanes / n):
-FP64_EXECUTED_PER_CMUX = {1: 176_129, 2: 183_875}
+FP64_EXECUTED_PER_CMUX = {1: 176_129, 2: 183_875, 8: 183_778}  # 8: the TMEM engine (ncu, r2 tm6)
+# A lower bound on the FP64 instructions of one CMux of one lane, for scale:
+# 8 complex 512-point transforms at the best known real-flop count (split
+# radix, 4 M log2 M - 6 M + 8 = 15,368 flops) with every instruction a fused
+# multiply-add (2 flops), plus the pointwise sum (4 DFMA per complex
+# multiply-add, 512 x 4 outputs x 4 rows) = 8 x 7,684 + 32,768 = 94,240.
+FP64_LOWER_BOUND_PER_CMUX = 8 * (4 * 512 * 9 - 6 * 512 + 8) // 2 + 512 * 4 * 4 * 4
 MODMUL_PER_LANE = {1024: 19_456_000, 256: 1_048_576}  # n[(k+1)l+(k+1)](N/2)log2N + n(k+1)l(k+1)N
 WORKLOAD = ("config1: 4096 independent bootstrapped gates, ops uniform over "
             "NAND/AND/OR/XOR/XNOR/MUX, uniform input bits; TFHE N=1024 k=1 n=500 "
@@ -631,18 +637,25 @@ def run_she(args):
     if engine:  # FP64 FFT engine: bound by the FP64 pipe
         fp64_ops = lanes_rank * P.n * FP64_OPS_PER_CMUX
         achieved = fp64_ops / (br_ms_per_launch * 1e-3)
-        slots = sms * engine * (2 if engine == 2 else 1)  # fft2x2: 2 CTAs of 2 lanes per SM
+        # lanes resident per round: the TMEM engine 8 per SM (4 pipelines x 2),
+        # fft2x2 2 CTAs of 2 lanes, else G lanes per CTA, one CTA per SM
+        slots = sms * engine * (2 if engine == 2 else 1)
+        kname = "br_fft_tm_kernel" if engine == 8 else "br_fft_kernel"
         rounds = -(-lanes_rank // slots)
         roof = {"bound": "fp64", "achieved": round(achieved / 1e12, 3),
                 "peak": round(fp64_peak / 1e12, 3), "unit": "T FP64-instr/s",
-                "frac": round(achieved / fp64_peak, 4), "traffic": read_profile_traffic("br_fft_kernel"),
-                "kernel": f"br_fft_kernel<{engine}> (gate prologue + blind rotation by exact FP64 "
-                          "FFT + sample extract)",
+                "frac": round(achieved / fp64_peak, 4), "traffic": read_profile_traffic(kname),
+                "kernel": (("br_fft_tm_kernel (four two-lane pipelines per SM, spectra in TMEM)"
+                            if engine == 8 else f"br_fft_kernel<{engine}>")
+                           + ": gate prologue + blind rotation by exact FP64 FFT + sample extract"),
                 "algorithmic_per_launch": f"{lanes_rank} BR lanes x {P.n} CMux x {FP64_OPS_PER_CMUX} "
                                           "FP64 instr (DESIGN.md §4.2b)",
-                "fp64_executed_per_cmux_default_transform": FP64_EXECUTED_PER_CMUX[2],
-                "frac_of_executed": round(lanes_rank * P.n * FP64_EXECUTED_PER_CMUX[2]
+                "fp64_executed_per_cmux_default_transform": FP64_EXECUTED_PER_CMUX[8 if engine == 8 else 2],
+                "frac_of_executed": round(lanes_rank * P.n * FP64_EXECUTED_PER_CMUX[8 if engine == 8 else 2]
                                           / (br_ms_per_launch * 1e-3) / fp64_peak, 4),
+                "fp64_lower_bound_per_cmux": FP64_LOWER_BOUND_PER_CMUX,
+                "frac_of_lower_bound": round(lanes_rank * P.n * FP64_LOWER_BOUND_PER_CMUX
+                                             / (br_ms_per_launch * 1e-3) / fp64_peak, 4),
                 **common,
                 "wave_rounds": {"lanes": lanes_rank, "slots_per_round": slots, "rounds": rounds,
                                 "last_round_fill": round(lanes_rank / slots - (rounds - 1), 3)},
@@ -650,7 +663,7 @@ def run_she(args):
                                "(nominal 64 FP64 lanes/SM/clk)",
                 "ntt_engine_equivalent": {"achieved_gmodmul_s": round(lanes_rank * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3) / 1e9, 1),
                                           "ntt_peak_gmodmul_s": round(peak / 1e9, 1)},
-                "ncu_profile": read_ncu_summary("br_fft_kernel")}
+                "ncu_profile": read_ncu_summary(kname)}
     else:
         achieved = lanes_rank * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3)
         roof = {"bound": "alu", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),

@@ -179,8 +179,9 @@ typedef struct {
                      on 8 warps, variant 2) */
   int fft_store;  /* FFT engine: where the digit spectra and products live
                      between the transforms: 0 = default (1); 1 = shared
-                     memory (br_fft_kernel, CTA-wide pointwise step); 2 =
-                     tensor memory (br_fft_tm_kernel: four independent
+                     memory (br_fft_kernel, CTA-wide pointwise step; the
+                     default when any shape option above is given); 2 =
+                     tensor memory (the default; br_fft_tm_kernel: four independent
                      two-lane pipelines per SM, one per sub-partition, spectra
                      in TMEM, the inverse on the forward's register layout;
                      DESIGN.md §4.2e; no other shape option applies) */
@@ -231,10 +232,12 @@ she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms);
  * every SM, one DFMA = one op; the roofline denominator of the FFT engine). */
 she_status she_bench_fp64_peak(int device, double* ops_per_s, double* ms);
 
-/* Blind-rotation engine of a context: *fft_lanes = G > 0 for the FP64 FFT
- * engine (br_fft_kernel, G lanes per CTA; the default for N = 1024), 0 for the
- * Goldilocks NTT engine (br_kernel; N = 256, or br_engine = 2).  Both are
- * exact, so the outputs are bit-identical. */
+/* Blind-rotation engine of a context: *fft_lanes = 8 for the FP64 FFT engine
+ * with the spectra in tensor memory (br_fft_tm_kernel: 4 two-lane pipelines
+ * per SM; the default for N = 1024), G = 2..5 for the shared-memory FFT engine
+ * (br_fft_kernel, G lanes per CTA), 0 for the Goldilocks NTT engine
+ * (br_kernel; N = 256, or br_engine = 2).  All are exact, so the outputs are
+ * bit-identical. */
 she_status she_ctx_br_engine(const she_ctx* ctx, int* fft_lanes);
 
 /* Test instrumentation: evaluate the device Goldilocks primitives (hand-written

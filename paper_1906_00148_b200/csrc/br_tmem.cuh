@@ -69,10 +69,32 @@ __device__ __forceinline__ void tm_ld4(uint32_t addr, double2 (&v)[4]) {
     v[q] = make_double2(__hiloint2double(r[4 * q + 1], r[4 * q]), __hiloint2double(r[4 * q + 3], r[4 * q + 2]));
 }
 __device__ __forceinline__ void tm_st1(uint32_t addr, double2 v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr),
-               "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)),
-               "r"(__double2hiint(v.y))
-               : "memory");
+  // the b64 -> 2 x b32 split inside the asm, so that ptxas picks the register
+  // quad itself instead of copying two pairs into one
+  asm volatile(
+      "{\n\t.reg .b32 a, b, c, d;\n\tmov.b64 {a, b}, %1;\n\tmov.b64 {c, d}, %2;\n\t"
+      "tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {a, b, c, d};\n\t}" ::"r"(addr),
+      "d"(v.x), "d"(v.y)
+      : "memory");
+}
+// The four digit spectra (r = 0..3, columns col0 + 64 r) of one frequency slot,
+// loaded and waited for in one block (doubles out directly).
+__device__ __forceinline__ void tm_ld_rows4(uint32_t col0, double2 (&D)[4]) {
+  asm volatile(
+      "{\n\t.reg .b32 a<16>;\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {a0, a1, a2, a3}, [%8];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {a4, a5, a6, a7}, [%9];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {a8, a9, a10, a11}, [%10];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {a12, a13, a14, a15}, [%11];\n\t"
+      "tcgen05.wait::ld.sync.aligned;\n\t"
+      "mov.b64 %0, {a0, a1};\n\tmov.b64 %1, {a2, a3};\n\t"
+      "mov.b64 %2, {a4, a5};\n\tmov.b64 %3, {a6, a7};\n\t"
+      "mov.b64 %4, {a8, a9};\n\tmov.b64 %5, {a10, a11};\n\t"
+      "mov.b64 %6, {a12, a13};\n\tmov.b64 %7, {a14, a15};\n\t}"
+      : "=d"(D[0].x), "=d"(D[0].y), "=d"(D[1].x), "=d"(D[1].y), "=d"(D[2].x), "=d"(D[2].y), "=d"(D[3].x),
+        "=d"(D[3].y)
+      : "r"(col0), "r"(col0 + 64), "r"(col0 + 128), "r"(col0 + 192)
+      : "memory");
 }
 __device__ __forceinline__ void tm_ld1(uint32_t addr, double2& v) {
   int r0, r1, r2, r3;
@@ -224,14 +246,14 @@ __device__ __forceinline__ void tm_bk_prefetch(const double2* bk_s, TmRing<PD>& 
   if (PD > 2) tm_bk_unit<2>(bk_s, ring.b[2 % (PD + 1)]);
   if (PD > 3) tm_bk_unit<3>(bk_s, ring.b[3 % (PD + 1)]);
 }
-template <int PD, int U>
+template <int PD, int NS, int U>
 __device__ __forceinline__ void tm_pw_unit(const double2* bk_s, TmRing<PD>& ring, const double2 (&D)[2][4],
                                            uint32_t row_base, int fi) {
   if (U + PD < 16) tm_bk_unit<(U + PD < 16 ? U + PD : 0)>(bk_s, ring.b[(U + PD) % (PD + 1)]);
   constexpr int q = U & 3;
   const double2(&b)[4] = ring.b[U % (PD + 1)];
 #pragma unroll
-  for (int sl = 0; sl < kTmSlots; ++sl) {
+  for (int sl = 0; sl < NS; ++sl) {
     double2 c = fft::cmul(D[sl][0], b[0]);
 #pragma unroll
     for (int r = 1; r < 4; ++r) {
@@ -245,26 +267,24 @@ __device__ __forceinline__ void tm_pw_unit(const double2* bk_s, TmRing<PD>& ring
 // registers first, so the four products can be written in place.  Both
 // slots are always computed (an idle slot's columns hold stale values that
 // nothing reads), so there is no data-dependent control flow here.
-template <int PD, int F>
+template <int PD, int NS, int F>
 __device__ __forceinline__ void tm_pw_slot(const double2* bk_s, TmRing<PD>& ring, uint32_t row_base, int s) {
   const int fi = 4 * s + F;
   double2 D[2][4];
 #pragma unroll
-  for (int sl = 0; sl < kTmSlots; ++sl)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) tm_ld1(row_base + sl * 256 + r * 64 + 4 * fi, D[sl][r]);
-  tm_wait_ld();
-  tm_pw_unit<PD, 4 * F + 0>(bk_s, ring, D, row_base, fi);
-  tm_pw_unit<PD, 4 * F + 1>(bk_s, ring, D, row_base, fi);
-  tm_pw_unit<PD, 4 * F + 2>(bk_s, ring, D, row_base, fi);
-  tm_pw_unit<PD, 4 * F + 3>(bk_s, ring, D, row_base, fi);
+  for (int sl = 0; sl < NS; ++sl) tm_ld_rows4(row_base + sl * 256 + 4 * fi, D[sl]);
+  tm_pw_unit<PD, NS, 4 * F + 0>(bk_s, ring, D, row_base, fi);
+  tm_pw_unit<PD, NS, 4 * F + 1>(bk_s, ring, D, row_base, fi);
+  tm_pw_unit<PD, NS, 4 * F + 2>(bk_s, ring, D, row_base, fi);
+  tm_pw_unit<PD, NS, 4 * F + 3>(bk_s, ring, D, row_base, fi);
 }
-template <int PD>
+// NS = 2: a lane pair (slots 0, 1); NS = 1: slot 0 alone.
+template <int PD, int NS>
 __device__ __forceinline__ void tm_pointwise(const double2* bk_s, TmRing<PD>& ring, uint32_t row_base, int s) {
-  tm_pw_slot<PD, 0>(bk_s, ring, row_base, s);
-  tm_pw_slot<PD, 1>(bk_s, ring, row_base, s);
-  tm_pw_slot<PD, 2>(bk_s, ring, row_base, s);
-  tm_pw_slot<PD, 3>(bk_s, ring, row_base, s);
+  tm_pw_slot<PD, NS, 0>(bk_s, ring, row_base, s);
+  tm_pw_slot<PD, NS, 1>(bk_s, ring, row_base, s);
+  tm_pw_slot<PD, NS, 2>(bk_s, ring, row_base, s);
+  tm_pw_slot<PD, NS, 3>(bk_s, ring, row_base, s);
 }
 
 struct TmArgs {
@@ -307,7 +327,8 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   const GateSrc& src = args.src;
   const br::Geometry& geo = args.geo;
   const uint32_t n = geo.n;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform (uniform datapath)
   const int Q = warp & 3, s = warp >> 2, qt = s * 32 + lane;  // quarter, warp in quarter, thread in quarter
   uint8_t* qb = smem + (size_t)Q * kTmQuarterBytes;
   uint32_t* acc = reinterpret_cast<uint32_t*>(qb);                     // [slot][c][N]
@@ -316,7 +337,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   double2* tw = reinterpret_cast<double2*>(smem + 4 * kTmQuarterBytes);
   fft::make_tables2(tid, 512, tw, tw + fft::kTw2 * 32);
   const uint32_t tmem = tm_alloc_all(&tmem_slot, warp);  // includes the table barrier
-  const uint32_t row_base = tmem + ((uint32_t)(32 * Q) << 16);
+  const uint32_t row_base = __shfl_sync(0xffffffffu, tmem + ((uint32_t)(32 * Q) << 16), 0);
 
   const uint32_t total = *args.nlanes;
   const uint32_t nq = gridDim.x * 4, gq = blockIdx.x * 4 + Q;
@@ -326,11 +347,9 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   const int sl_f = s >> 1, c_f = s & 1;  // forward: slot, component (rows 2 c + j)
   const int sl_i = s >> 1, o_i = s & 1;  // inverse: slot, output (rows 2 o + half)
 
-  for (uint32_t base = first; base < last; base += kTmSlots) {
-    const bool on[2] = {base < last, base + 1 < last};
-#pragma unroll
-    for (int sl = 0; sl < kTmSlots; ++sl) {
-      if (!on[sl]) continue;
+  // the gate prologue of the lanes in slots 0 .. nsl - 1 (a-bar, test vector)
+  auto prologue = [&](uint32_t base, int nsl) {
+    for (int sl = 0; sl < nsl; ++sl) {
       const uint32_t e = args.lanes[base + sl];
       const uint32_t gate = e & 0x7FFFFFFFu, hh = e >> 31;
       const LaneForm f = lane_form(gate_op(src, gate), (int)hh);
@@ -345,9 +364,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       }
     }
     tm_quarter_sync(Q);
-#pragma unroll
-    for (int sl = 0; sl < kTmSlots; ++sl) {
-      if (!on[sl]) continue;
+    for (int sl = 0; sl < nsl; ++sl) {
       const uint32_t bbar = abar[sl * 512 + n];
       uint32_t* a = acc + sl * 2 * N;
       for (int m = qt; m < N; m += 128) {
@@ -356,12 +373,32 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       }
     }
     tm_quarter_sync(Q);
+  };
+  // sample extraction of slots 0 .. nsl - 1
+  auto extract = [&](uint32_t base, int nsl) {
+    for (int sl = 0; sl < nsl; ++sl) {
+      const uint32_t* a = acc + sl * 2 * N;
+      const uint32_t le = args.lanes[base + sl];  // gate | h << 31
+      uint32_t* e = args.ext + (size_t)(2 * (le & 0x7FFFFFFFu) + (le >> 31)) * args.ext_stride;
+      for (int m = qt; m <= N; m += 128) {
+        uint32_t v;
+        if (m == 0) v = a[0];
+        else if (m < N) v = 0u - a[N - m];
+        else v = a[N];
+        e[m] = v;
+      }
+    }
+    tm_quarter_sync(Q);
+  };
 
+  uint32_t base = first;
+  for (; base + 1 < last; base += kTmSlots) {  // lane pairs
+    prologue(base, 2);
     for (uint32_t i = 0; i < n; ++i) {
       const int ln = lane;
       double2* const scr = scratch;
       const double2* const twp = tw;
-      if (sl_f ? on[1] : on[0]) {  // forward transforms of digit rows 2c, 2c + 1 of slot sl_f
+      {  // forward transforms of digit rows 2c, 2c + 1 of slot sl_f
         // both rows' digit fields from one rotation pass; the j = 1 fields wait
         // in the (not yet written) TMEM columns of row 2c + 1 during the first
         // transform instead of in 16 registers
@@ -392,10 +429,10 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       tm_bk_prefetch<PD>(bk_s, ring);
       tm_wait_st();
       tm_quarter_sync(Q);
-      tm_pointwise<PD>(bk_s, ring, row_base, s);
+      tm_pointwise<PD, 2>(bk_s, ring, row_base, s);
       tm_wait_st();
       tm_quarter_sync(Q);
-      if (sl_i ? on[1] : on[0]) {  // inverse transforms of outputs (o, hi), (o, lo) of slot sl_i
+      {  // inverse transforms of outputs (o, hi), (o, lo) of slot sl_i
         uint32_t* acc_o = acc + (sl_i * 2 + o_i) * N;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half)
@@ -404,22 +441,29 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       }
       tm_quarter_sync(Q);  // ACC complete before the next digits
     }
-
-#pragma unroll
-    for (int sl = 0; sl < kTmSlots; ++sl) {
-      if (!on[sl]) continue;
-      const uint32_t* a = acc + sl * 2 * N;
-      const uint32_t le = args.lanes[base + sl];  // gate | h << 31
-      uint32_t* e = args.ext + (size_t)(2 * (le & 0x7FFFFFFFu) + (le >> 31)) * args.ext_stride;
-      for (int m = qt; m <= N; m += 128) {
-        uint32_t v;
-        if (m == 0) v = a[0];
-        else if (m < N) v = 0u - a[N - m];
-        else v = a[N];
-        e[m] = v;
+    extract(base, 2);
+  }
+  if (base < last) {  // the quarter's odd last lane: all four warps on it (slot 0)
+    prologue(base, 1);
+    for (uint32_t i = 0; i < n; ++i) {
+      {  // warp s: forward transform of digit row s
+        uint32_t u[32];
+        fbr_load_fields(geo, s, lane, acc, abar[i], u);
+        tm_forward_fields(u, (double)(1u << (geo.bg_bits - 1)), lane, tw, scratch, row_base + s * 64);
       }
+      const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + lane;
+      TmRing<PD> ring;
+      tm_bk_prefetch<PD>(bk_s, ring);
+      tm_wait_st();
+      tm_quarter_sync(Q);
+      tm_pointwise<PD, 1>(bk_s, ring, row_base, s);
+      tm_wait_st();
+      tm_quarter_sync(Q);
+      // warp s: inverse of product row s = (o, half) = (s >> 1, s & 1)
+      tm_inverse_acc<false>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, nullptr);
+      tm_quarter_sync(Q);
     }
-    tm_quarter_sync(Q);
+    extract(base, 1);
   }
   tm_free_all(tmem, warp);
 }
@@ -496,7 +540,7 @@ __global__ void __launch_bounds__(512, 1) fft_selftest_tm_kernel(const int32_t* 
   if (active) tm_bk_prefetch<kTmPrefetch>(bk_s, ring);
   tm_wait_st();
   tm_quarter_sync(Q);
-  if (active) tm_pointwise<kTmPrefetch>(bk_s, ring, row_base, s);
+  if (active) tm_pointwise<kTmPrefetch, 1>(bk_s, ring, row_base, s);
   tm_wait_st();
   tm_quarter_sync(Q);
   if (active)

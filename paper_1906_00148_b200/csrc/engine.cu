@@ -356,7 +356,7 @@ struct FftVar<3> {  // v2's tables and scaling, DIT/FMA DFT16s (fft_core.cuh)
 };
 constexpr int kFftDefaultVariant = 2;
 constexpr int kFftDefaultStreams = 1;  // br_fft_kernel (1) or the two-stream br_fft2s_kernel (2)
-constexpr int kFftDefaultStore = 1;    // spectra in shared memory (1) or tensor memory (2)
+constexpr int kFftDefaultStore = 2;    // spectra in shared memory (1) or tensor memory (2)
 template <int V>
 constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double2); }
 
@@ -1992,7 +1992,9 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   ctx->fft_v = o.fft_variant ? o.fft_variant : kFftDefaultVariant;
   ctx->fft_grp = o.fft_groups ? o.fft_groups : 1;
   ctx->fft_streams = o.fft_streams ? o.fft_streams : kFftDefaultStreams;
-  ctx->fft_store = use_fft ? (o.fft_store ? o.fft_store : kFftDefaultStore) : 1;
+  // the TMEM engine is the default; a shape option of the shared-memory engine selects that one
+  const bool smem_shape = o.fft_lanes || o.fft_variant || o.fft_groups || o.fft_prefetch || o.fft_streams;
+  ctx->fft_store = use_fft ? (o.fft_store ? o.fft_store : smem_shape ? 1 : kFftDefaultStore) : 1;
   ctx->fft_stagger = (uint32_t)o.fft_stagger_ns;
   ctx->fft_pre = o.fft_prefetch == 0 ? 16 : o.fft_prefetch == 3 ? 0 : o.fft_prefetch == 2 ? 8 : 16;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
@@ -2207,7 +2209,7 @@ she_status she_bench_fp64_peak(int device, double* ops_per_s, double* ms) {
 
 she_status she_ctx_br_engine(const she_ctx* ctx, int* fft_lanes) {
   if (!ctx || !fft_lanes) return fail(SHE_ERR_ARG, "null argument");
-  *fft_lanes = ctx->bkt ? 2 : ctx->bkf ? ctx->fft_g : 0;
+  *fft_lanes = ctx->bkt ? 8 : ctx->bkf ? ctx->fft_g : 0;  // TMEM engine: 4 pipelines x 2 lanes per SM
   return SHE_OK;
 }
 
