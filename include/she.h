@@ -166,7 +166,8 @@ typedef struct {
                      transform (16-entry twiddle tables, select-based pair
                      exchange; 4 lanes per CTA only), 2 = v2,
                      3 = v2 with DIT/FMA 16-point DFTs (4 lanes, or 5 lanes
-                     with fft_prefetch = 3) */
+                     with fft_prefetch = 3; with fft_store = 2 the TMEM
+                     engine with FMA butterflies in both directions) */
   int fft_groups; /* FFT engine: independent lane groups per CTA, 0 = default
                      (1); 2 = two groups of 2 lanes with their own pointwise
                      step and barriers (4 lanes per CTA, variant 2) */
@@ -256,7 +257,8 @@ she_status she_field_selftest(int device, const uint64_t* a, const uint64_t* b, 
  * model of it.  variant: the transform (she_ctx_options.fft_variant; 0 =
  * the default); 4 = the TMEM engine (fft_store = 2: bk_tm_kernel's setup, the
  * digit spectra and products in tensor memory, the register-layout inverse
- * inverse_tr; br_tmem.cuh).  N = 1024 only.  HOST buffers:
+ * inverse_tr; br_tmem.cuh), 5 = the TMEM engine with transform 3's FMA
+ * butterflies (fft_store = 2, fft_variant = 3).  N = 1024 only.  HOST buffers:
  *   digits int32[count][4][1024]      digit rows r = c*l + j, |d| <= 2^11
  *   bk     uint32[count][4][2][1024]  torus32 BK rows (r, output o)
  *   out    uint32[count][2][1024]     out[c][o] = sum_r digits[c][r] * bk[c][r][o]

@@ -177,6 +177,7 @@ __device__ __forceinline__ void tm_load_fields2(const br::Geometry& g, int lane,
 
 // Forward transform of one digit row given as fields u = d + Bg/2 (the
 // conversion of fbr_forward_fields) into the TMEM row at addr.
+template <bool FMA = false>
 __device__ __forceinline__ void tm_forward_fields(const uint32_t (&u)[32], double half, int lane,
                                                   const double2* tw, double2* scratch, uint32_t addr) {
   const double off = 4503599627370496.0 + half;  // 2^52 + Bg/2
@@ -188,19 +189,20 @@ __device__ __forceinline__ void tm_forward_fields(const uint32_t (&u)[32], doubl
   }
   double2 a[16], x[8], y[8];
   fft::v2_fwd_in(re, im, a);
-  fft::dft512_v2<1>(a, lane, tw, scratch, x, y);
+  if (FMA) fft::dft512_v3<1>(a, lane, tw, scratch, x, y);  // same layout and scaling
+  else fft::dft512_v2<1>(a, lane, tw, scratch, x, y);
   tm_store_spectrum(addr, x, y);
 }
 
 // Inverse of the product row at addr, rounded to the exact integer and added
 // into ACC_o at n = lane + 32 m (re) and n + 512 (im), shifted by sh (16 for
 // the hi half).  TRACK: the largest distance to an integer (self-test).
-template <bool TRACK>
+template <bool TRACK, bool FMA = false>
 __device__ __forceinline__ void tm_inverse_acc(uint32_t addr, int lane, const double2* tw, double2* scratch,
                                                uint32_t* acc_o, int sh, unsigned long long* worst) {
   double2 x[8], y[8], a[16];
   tm_load_spectrum(addr, x, y);
-  fft::inverse_tr(x, y, lane, tw, scratch, a);
+  fft::inverse_tr<FMA>(x, y, lane, tw, scratch, a);
   double dmax = 0.0;
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
@@ -319,7 +321,7 @@ __device__ __forceinline__ void tm_free_all(uint32_t tmem, int warp) {
 
 // K3, TMEM engine: one persistent CTA of 16 warps per SM, four independent
 // quarter pipelines of two lanes each (see the file comment).
-template <int PD = kTmPrefetch>
+template <int PD = kTmPrefetch, bool FMA = false>
 __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   constexpr int N = fft::kN;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
           tm_st_u16(row1, pk1);
         }
         const double half = (double)(1u << (geo.bg_bits - 1));
-        tm_forward_fields(u, half, ln, twp, scr, row0);
+        tm_forward_fields<FMA>(u, half, ln, twp, scr, row0);
         {
           uint32_t pk1[16];
           tm_wait_st();  // this thread's stash store (long done) before reading it back
@@ -422,7 +424,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
             u[2 * k + 1] = pk1[k] >> 16;
           }
         }
-        tm_forward_fields(u, half, ln, twp, scr, row1);
+        tm_forward_fields<FMA>(u, half, ln, twp, scr, row1);
       }
       const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + ln;
       TmRing<PD> ring;
@@ -436,7 +438,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
         uint32_t* acc_o = acc + (sl_i * 2 + o_i) * N;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half)
-          tm_inverse_acc<false>(row_base + sl_i * 256 + (2 * o_i + half) * 64, ln, twp, scr, acc_o,
+          tm_inverse_acc<false, FMA>(row_base + sl_i * 256 + (2 * o_i + half) * 64, ln, twp, scr, acc_o,
                                 half ? 0 : 16, nullptr);
       }
       tm_quarter_sync(Q);  // ACC complete before the next digits
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       {  // warp s: forward transform of digit row s
         uint32_t u[32];
         fbr_load_fields(geo, s, lane, acc, abar[i], u);
-        tm_forward_fields(u, (double)(1u << (geo.bg_bits - 1)), lane, tw, scratch, row_base + s * 64);
+        tm_forward_fields<FMA>(u, (double)(1u << (geo.bg_bits - 1)), lane, tw, scratch, row_base + s * 64);
       }
       const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + lane;
       TmRing<PD> ring;
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       tm_wait_st();
       tm_quarter_sync(Q);
       // warp s: inverse of product row s = (o, half) = (s >> 1, s & 1)
-      tm_inverse_acc<false>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, nullptr);
+      tm_inverse_acc<false, FMA>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, nullptr);
       tm_quarter_sync(Q);
     }
     extract(base, 1);
@@ -510,6 +512,7 @@ __global__ void bk_tm_kernel(const uint32_t* bk, double2* out, uint32_t polys) {
 // device functions (tm_forward_fields, tm_pointwise, tm_inverse_acc): quarter
 // Q of CTA b runs case 4 b + Q in slot 0 (warp s: forward of digit row s,
 // inverse of output (s >> 1, s & 1)).
+template <bool FMA>
 __global__ void __launch_bounds__(512, 1) fft_selftest_tm_kernel(const int32_t* digits, const double2* bkt,
                                                                  uint32_t* out, unsigned long long* worst,
                                                                  uint32_t count) {
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(512, 1) fft_selftest_tm_kernel(const int32_t* 
     uint32_t uu[32];
 #pragma unroll
     for (int j2 = 0; j2 < 32; ++j2) uu[j2] = (uint32_t)(d[lane + 32 * j2] + 2048);
-    tm_forward_fields(uu, 2048.0, lane, tw, scratch, row_base + s * 64);
+    tm_forward_fields<FMA>(uu, 2048.0, lane, tw, scratch, row_base + s * 64);
   }
   const double2* bk_s = bkt + ((size_t)c * 16 + 4 * s) * 16 * 32 + lane;
   TmRing<kTmPrefetch> ring;
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(512, 1) fft_selftest_tm_kernel(const int32_t* 
   tm_wait_st();
   tm_quarter_sync(Q);
   if (active)
-    tm_inverse_acc<true>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, worst);
+    tm_inverse_acc<true, FMA>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, worst);
   tm_quarter_sync(Q);
   if (active)
     for (int m = qt; m < 2 * N; m += 128) out[(size_t)c * 2 * N + m] = acc[m];

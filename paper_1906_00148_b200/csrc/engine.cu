@@ -1558,7 +1558,9 @@ she_status setup_shape(she_ctx* ctx, const she_cloud_key* ck) {
     bk_tm_kernel<<<(unsigned)(2 * polys), 32>>>(d_bk32, ctx->bkt, (uint32_t)polys);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
-    CK(cudaFuncSetAttribute(br_fft_tm_kernel<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(br_fft_tm_kernel<kTmPrefetch, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kTmSmemBytes));
+    CK(cudaFuncSetAttribute(br_fft_tm_kernel<kTmPrefetch, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kTmSmemBytes));
   } else if (ctx->fft_g && S::N == fft::kN) {  // FFT engine: BK halves in the FFT domain
     ctx->bk_bytes = (size_t)p.n * 16 * fft::kM * sizeof(double2);
@@ -1719,7 +1721,8 @@ she_status launch_br_fft_tm(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cud
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  CK(cudaLaunchKernelEx(&cfg, br_fft_tm_kernel<>, f));
+  if (ctx->fft_v == 3) CK(cudaLaunchKernelEx(&cfg, br_fft_tm_kernel<kTmPrefetch, true>, f));
+  else CK(cudaLaunchKernelEx(&cfg, br_fft_tm_kernel<kTmPrefetch, false>, f));
   return SHE_OK;
 }
 
@@ -1959,9 +1962,9 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
                              (o.fft_variant && o.fft_variant != 2) || o.fft_prefetch >= 2))
     return fail(SHE_ERR_ARG, "fft_streams = 2 is instantiated for 4 lanes, variant 2");
   if (o.fft_store < 0 || o.fft_store > 2) return fail(SHE_ERR_ARG, "fft_store=%d", o.fft_store);
-  if (o.fft_store == 2 && (!use_fft || o.fft_lanes || o.fft_variant > 2 || o.fft_variant == 1 ||
-                           o.fft_groups || o.fft_prefetch || o.fft_streams))
-    return fail(SHE_ERR_ARG, "fft_store = 2 (TMEM engine) has its own shape: no lane/group/prefetch/stream options");
+  if (o.fft_store == 2 && (!use_fft || o.fft_lanes || o.fft_variant == 1 || o.fft_groups ||
+                           o.fft_prefetch || o.fft_streams))
+    return fail(SHE_ERR_ARG, "fft_store = 2 (TMEM engine): transform 2 or 3 only, no lane/group/prefetch/stream options");
   if (o.fft_stagger_ns < 0 || o.fft_stagger_ns > 100000)
     return fail(SHE_ERR_ARG, "fft_stagger_ns=%d", o.fft_stagger_ns);
   if (o.fft_prefetch < 0 || o.fft_prefetch > 3)
@@ -2288,8 +2291,9 @@ she_status she_fft_product_selftest(int device, int variant, const int32_t* digi
                                     double* worst_distance) {
   if (count == 0) return SHE_OK;
   if (!digits || !bk || !out) return fail(SHE_ERR_ARG, "NULL argument");
-  if (variant < 0 || variant > 4) return fail(SHE_ERR_ARG, "variant=%d", variant);
-  const int V = variant ? variant : kFftDefaultVariant;  // 4: the TMEM engine (br_tmem.cuh)
+  if (variant < 0 || variant > 5) return fail(SHE_ERR_ARG, "variant=%d", variant);
+  // 4: the TMEM engine (br_tmem.cuh), 5: the same with the FMA butterflies (transform 3)
+  const int V = variant ? variant : kFftDefaultVariant;
   if (count > 65535) return fail(SHE_ERR_ARG, "count > 65535");
   constexpr size_t N = fft::kN;
   CK(cudaSetDevice(device));
@@ -2306,15 +2310,14 @@ she_status she_fft_product_selftest(int device, int variant, const int32_t* digi
   if (e == cudaSuccess) e = cudaMemset(dworst, 0, 8);
   if (e == cudaSuccess) e = cudaMemcpy(dd, digits, count * 4 * N * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(db, bk, count * 8 * N * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && V == 4) {  // the TMEM engine's setup transform and product
+  if (e == cudaSuccess && V >= 4) {  // the TMEM engine's setup transform and product
     bk_tm_kernel<<<(unsigned)(2 * count * 8), 32>>>(db, dbkf, (uint32_t)(count * 8));
     e = cudaGetLastError();
+    auto tmk = V == 5 ? fft_selftest_tm_kernel<true> : fft_selftest_tm_kernel<false>;
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fft_selftest_tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kTmSmemBytes);
+      e = cudaFuncSetAttribute(tmk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmSmemBytes);
     if (e == cudaSuccess) {
-      fft_selftest_tm_kernel<<<(unsigned)((count + 3) / 4), 512, kTmSmemBytes>>>(dd, dbkf, dout, dworst,
-                                                                                (uint32_t)count);
+      tmk<<<(unsigned)((count + 3) / 4), 512, kTmSmemBytes>>>(dd, dbkf, dout, dworst, (uint32_t)count);
       e = cudaGetLastError();
     }
   } else if (e == cudaSuccess) {  // the setup transform of the engine (BK -> FFT domain, halves)
@@ -2326,9 +2329,9 @@ she_status she_fft_product_selftest(int device, int variant, const int32_t* digi
   constexpr size_t smem = (4 * fft::kRow + 2 * 512) * sizeof(double2) + 2 * N * 4;
   auto selftest = V == 1 ? fft_selftest_kernel<1> : V == 3 ? fft_selftest_kernel<3>
                                                             : fft_selftest_kernel<2>;
-  if (e == cudaSuccess && V != 4)
+  if (e == cudaSuccess && V < 4)
     e = cudaFuncSetAttribute(selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess && V != 4) {
+  if (e == cudaSuccess && V < 4) {
     selftest<<<(unsigned)count, 128, smem>>>(dd, dbkf, dout, dworst);
     e = cudaGetLastError();
   }

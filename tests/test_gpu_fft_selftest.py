@@ -86,7 +86,8 @@ def cases():
     return out
 
 
-@pytest.mark.parametrize("variant", [2, 1, 3, 4], ids=["v2", "v1-round1", "v3-dit-fma", "tmem"])
+@pytest.mark.parametrize("variant", [2, 1, 3, 4, 5],
+                         ids=["v2", "v1-round1", "v3-dit-fma", "tmem", "tmem-fma"])
 def test_fft_product_selftest_matches_schoolbook_on_extreme_inputs(cuda, variant):
     cs = cases()
     digits = np.stack([d for _, d, _ in cs])
