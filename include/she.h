@@ -162,7 +162,8 @@ typedef struct {
                      3 = the tensor-core key switch (ks_imma.cuh: 0/1 digit
                      matrix x key byte planes on mma.sync u8, base 4, t = 8),
                      4 = the same product on tcgen05 (kind::i8, TMEM) */
-  int fft_variant;/* FFT engine transform: 0 = default (2), 1 = the round-1
+  int fft_variant;/* FFT engine transform: 0 = default (3 on the TMEM engine,
+                     2 on the shared-memory engine), 1 = the round-1
                      transform (16-entry twiddle tables, select-based pair
                      exchange; 4 lanes per CTA only), 2 = v2,
                      3 = v2 with DIT/FMA 16-point DFTs (4 lanes, or 5 lanes

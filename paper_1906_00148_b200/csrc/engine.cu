@@ -1992,12 +1992,15 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     ctx->br_b = o.ntt_ctas;
   }
   ctx->fft_g = use_fft ? (o.fft_lanes ? o.fft_lanes : 4) : 0;
-  ctx->fft_v = o.fft_variant ? o.fft_variant : kFftDefaultVariant;
+
   ctx->fft_grp = o.fft_groups ? o.fft_groups : 1;
   ctx->fft_streams = o.fft_streams ? o.fft_streams : kFftDefaultStreams;
   // the TMEM engine is the default; a shape option of the shared-memory engine selects that one
   const bool smem_shape = o.fft_lanes || o.fft_variant || o.fft_groups || o.fft_prefetch || o.fft_streams;
   ctx->fft_store = use_fft ? (o.fft_store ? o.fft_store : smem_shape ? 1 : kFftDefaultStore) : 1;
+  // transform: the TMEM engine defaults to transform 3 (FMA butterflies in both
+  // directions, §4.2e), the shared-memory engine to transform 2
+  ctx->fft_v = o.fft_variant ? o.fft_variant : ctx->fft_store == 2 ? 3 : kFftDefaultVariant;
   ctx->fft_stagger = (uint32_t)o.fft_stagger_ns;
   ctx->fft_pre = o.fft_prefetch == 0 ? 16 : o.fft_prefetch == 3 ? 0 : o.fft_prefetch == 2 ? 8 : 16;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);

@@ -296,13 +296,13 @@ ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3
                "fft5-v3": dict(engine="fft", fft_lanes=5, fft_prefetch=3, fft_variant=3),
                "fft-smem": dict(engine="fft", fft_store="smem"),
                "fft-tmem-stagger": dict(engine="fft", fft_store="tmem", fft_stagger_ns=20000),
-               "fft-tmem-fma": dict(engine="fft", fft_store="tmem", fft_variant=3)}
+               "fft-tmem-v2": dict(engine="fft", fft_store="tmem", fft_variant=2)}
 
 
 @pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2", "fft-v1", "fft-2groups",
                                     "fft5-noprefetch", "ks-imma", "ks-cuda", "fft-v3", "fft5-v3",
                                     "ks-tcgen05", "fft-2streams", "fft-smem", "fft-tmem-stagger",
-                                    "fft-tmem-fma"])
+                                    "fft-tmem-v2"])
 def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with the
     spectra in tensor memory (br_fft_tm_kernel); the Goldilocks
@@ -317,7 +317,7 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
                                   "fft-2groups": 4, "fft5-noprefetch": 5, "ks-imma": 8,
                                   "ks-cuda": 8, "fft-v3": 4, "fft5-v3": 5, "ks-tcgen05": 8,
                                   "fft-2streams": 4, "fft-smem": 4, "fft-tmem-stagger": 8,
-                                  "fft-tmem-fma": 8}[engine]
+                                  "fft-tmem-v2": 8}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
     she.she_gate_batch_ops(ctx, dev(np.asarray(ops, np.uint8)), dev(a), dev(b), dev(c), out)
