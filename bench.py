@@ -52,7 +52,7 @@ FP64_OPS_PER_CMUX = 8 * 17_920 + 512 * 4 * 16
 # §4.2b), so the fraction measures useful work per second whichever transform
 # runs.  FP64 instructions the default transform (v2, §4.2c) actually executes
 # per CMux and lane, from ncu (profiles/r2/: DADD + DMUL + DFMA / lanes / n):
-FP64_EXECUTED_PER_CMUX = {1: 176_129, 2: 183_875, 8: 183_778}  # 8: the TMEM engine (ncu, r2 tm6)
+FP64_EXECUTED_PER_CMUX = {1: 176_129, 2: 183_875, 8: 171_074}  # 8: the TMEM engine, transform 3 (ncu, r2 tm10)
 # A lower bound on the FP64 instructions of one CMux of one lane, for scale:
 # 8 complex 512-point transforms at the best known real-flop count (split
 # radix, 4 M log2 M - 6 M + 8 = 15,368 flops) with every instruction a fused
