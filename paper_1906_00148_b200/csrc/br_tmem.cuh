@@ -33,6 +33,7 @@
 // 8 KB transpose rows (one per warp): 50 KB; + the v2 twiddle tables.
 // TMEM: 512 columns x 128 lanes (all of it; one CTA per SM).
 #pragma once
+#include "dcheck.cuh"
 
 constexpr int kTmSlots = 2;
 constexpr size_t kTmAccBytes = (size_t)kTmSlots * 2 * fft::kN * 4;
@@ -40,10 +41,25 @@ constexpr size_t kTmAbarBytes = (size_t)kTmSlots * 512 * 2;
 constexpr size_t kTmScratchBytes = (size_t)4 * fft::kRow * 16;
 constexpr size_t kTmQuarterBytes = kTmAccBytes + kTmAbarBytes + kTmScratchBytes;
 constexpr size_t kTmSmemBytes = 4 * kTmQuarterBytes + 2 * fft::kTw2 * 32 * sizeof(double2);
-constexpr int kTmPrefetch = 3;  // BK units (4 planes each) in flight ahead of use
+#ifndef SHE_TM_PD
+#define SHE_TM_PD 3
+#endif
+#ifndef SHE_TM_FMA_FWD  // transform 3: FMA butterflies in the forward / inverse (A/B builds)
+#define SHE_TM_FMA_FWD 1
+#endif
+#ifndef SHE_TM_FMA_INV
+#define SHE_TM_FMA_INV 1
+#endif
+constexpr int kTmPrefetch = SHE_TM_PD;  // BK units (4 planes each) in flight ahead of use
 
 // ---- tensor-memory access (tcgen05, 32x32b shape: thread t <-> TMEM lane) ---
+// checked build: columns [col, col + ncols) inside the 512 allocated (base
+// column 0, asserted at allocation) and a lane field at a quarter boundary
+__device__ __forceinline__ void tm_check(uint32_t addr, uint32_t ncols) {
+  SHE_DCHECK((addr & 0xFFFFu) + ncols <= 512u && ((addr >> 16) & 31u) == 0 && (addr >> 16) < 128u);
+}
 __device__ __forceinline__ void tm_st4(uint32_t addr, const double2 (&v)[4]) {
+  tm_check(addr, 16);
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
           addr),
@@ -56,6 +72,7 @@ __device__ __forceinline__ void tm_st4(uint32_t addr, const double2 (&v)[4]) {
       : "memory");
 }
 __device__ __forceinline__ void tm_ld4(uint32_t addr, double2 (&v)[4]) {
+  tm_check(addr, 16);
   int r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -69,6 +86,7 @@ __device__ __forceinline__ void tm_ld4(uint32_t addr, double2 (&v)[4]) {
     v[q] = make_double2(__hiloint2double(r[4 * q + 1], r[4 * q]), __hiloint2double(r[4 * q + 3], r[4 * q + 2]));
 }
 __device__ __forceinline__ void tm_st1(uint32_t addr, double2 v) {
+  tm_check(addr, 4);
   // the b64 -> 2 x b32 split inside the asm, so that ptxas picks the register
   // quad itself instead of copying two pairs into one
   asm volatile(
@@ -80,6 +98,7 @@ __device__ __forceinline__ void tm_st1(uint32_t addr, double2 v) {
 // The four digit spectra (r = 0..3, columns col0 + 64 r) of one frequency slot,
 // loaded and waited for in one block (doubles out directly).
 __device__ __forceinline__ void tm_ld_rows4(uint32_t col0, double2 (&D)[4]) {
+  tm_check(col0 + 192, 4);
   asm volatile(
       "{\n\t.reg .b32 a<16>;\n\t"
       "tcgen05.ld.sync.aligned.32x32b.x4.b32 {a0, a1, a2, a3}, [%8];\n\t"
@@ -105,6 +124,7 @@ __device__ __forceinline__ void tm_ld1(uint32_t addr, double2& v) {
   v = make_double2(__hiloint2double(r1, r0), __hiloint2double(r3, r2));
 }
 __device__ __forceinline__ void tm_st_u16(uint32_t addr, const uint32_t (&v)[16]) {
+  tm_check(addr, 16);
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
           addr),
@@ -113,6 +133,7 @@ __device__ __forceinline__ void tm_st_u16(uint32_t addr, const uint32_t (&v)[16]
       : "memory");
 }
 __device__ __forceinline__ void tm_ld_u16(uint32_t addr, uint32_t (&v)[16]) {
+  tm_check(addr, 16);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
@@ -310,6 +331,7 @@ __device__ __forceinline__ uint32_t tm_alloc_all(uint32_t* slot, int warp) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  SHE_DCHECK((*slot & 0xFFFFu) == 0 && (*slot >> 16) == 0);  // all 512 columns from column 0
   return *slot;
 }
 __device__ __forceinline__ void tm_free_all(uint32_t tmem, int warp) {
@@ -350,10 +372,13 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   const int sl_i = s >> 1, o_i = s & 1;  // inverse: slot, output (rows 2 o + half)
 
   // the gate prologue of the lanes in slots 0 .. nsl - 1 (a-bar, test vector)
+  SHE_DCHECK(last <= total);
   auto prologue = [&](uint32_t base, int nsl) {
     for (int sl = 0; sl < nsl; ++sl) {
+      SHE_DCHECK(base + sl < last && n < 512);
       const uint32_t e = args.lanes[base + sl];
       const uint32_t gate = e & 0x7FFFFFFFu, hh = e >> 31;
+      SHE_DCHECK(gate < src.count && (hh == 0 || gate_op(src, gate) == SHE_MUX));
       const LaneForm f = lane_form(gate_op(src, gate), (int)hh);
       bool n0, n1;
       const uint32_t* x0 = gate_in(src, gate, 0, n0);
@@ -381,6 +406,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
     for (int sl = 0; sl < nsl; ++sl) {
       const uint32_t* a = acc + sl * 2 * N;
       const uint32_t le = args.lanes[base + sl];  // gate | h << 31
+      SHE_DCHECK((le & 0x7FFFFFFFu) < src.count);
       uint32_t* e = args.ext + (size_t)(2 * (le & 0x7FFFFFFFu) + (le >> 31)) * args.ext_stride;
       for (int m = qt; m <= N; m += 128) {
         uint32_t v;
@@ -412,7 +438,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
           tm_st_u16(row1, pk1);
         }
         const double half = (double)(1u << (geo.bg_bits - 1));
-        tm_forward_fields<FMA>(u, half, ln, twp, scr, row0);
+        tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, half, ln, twp, scr, row0);
         {
           uint32_t pk1[16];
           tm_wait_st();  // this thread's stash store (long done) before reading it back
@@ -424,7 +450,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
             u[2 * k + 1] = pk1[k] >> 16;
           }
         }
-        tm_forward_fields<FMA>(u, half, ln, twp, scr, row1);
+        tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, half, ln, twp, scr, row1);
       }
       const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + ln;
       TmRing<PD> ring;
@@ -438,7 +464,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
         uint32_t* acc_o = acc + (sl_i * 2 + o_i) * N;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half)
-          tm_inverse_acc<false, FMA>(row_base + sl_i * 256 + (2 * o_i + half) * 64, ln, twp, scr, acc_o,
+          tm_inverse_acc<false, FMA && SHE_TM_FMA_INV>(row_base + sl_i * 256 + (2 * o_i + half) * 64, ln, twp, scr, acc_o,
                                 half ? 0 : 16, nullptr);
       }
       tm_quarter_sync(Q);  // ACC complete before the next digits
@@ -451,7 +477,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       {  // warp s: forward transform of digit row s
         uint32_t u[32];
         fbr_load_fields(geo, s, lane, acc, abar[i], u);
-        tm_forward_fields<FMA>(u, (double)(1u << (geo.bg_bits - 1)), lane, tw, scratch, row_base + s * 64);
+        tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, (double)(1u << (geo.bg_bits - 1)), lane, tw, scratch, row_base + s * 64);
       }
       const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + lane;
       TmRing<PD> ring;
@@ -462,7 +488,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       tm_wait_st();
       tm_quarter_sync(Q);
       // warp s: inverse of product row s = (o, half) = (s >> 1, s & 1)
-      tm_inverse_acc<false, FMA>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, nullptr);
+      tm_inverse_acc<false, FMA && SHE_TM_FMA_INV>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, nullptr);
       tm_quarter_sync(Q);
     }
     extract(base, 1);
@@ -536,7 +562,7 @@ __global__ void __launch_bounds__(512, 1) fft_selftest_tm_kernel(const int32_t* 
     uint32_t uu[32];
 #pragma unroll
     for (int j2 = 0; j2 < 32; ++j2) uu[j2] = (uint32_t)(d[lane + 32 * j2] + 2048);
-    tm_forward_fields<FMA>(uu, 2048.0, lane, tw, scratch, row_base + s * 64);
+    tm_forward_fields<FMA && SHE_TM_FMA_FWD>(uu, 2048.0, lane, tw, scratch, row_base + s * 64);
   }
   const double2* bk_s = bkt + ((size_t)c * 16 + 4 * s) * 16 * 32 + lane;
   TmRing<kTmPrefetch> ring;
@@ -547,7 +573,7 @@ __global__ void __launch_bounds__(512, 1) fft_selftest_tm_kernel(const int32_t* 
   tm_wait_st();
   tm_quarter_sync(Q);
   if (active)
-    tm_inverse_acc<true, FMA>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, worst);
+    tm_inverse_acc<true, FMA && SHE_TM_FMA_INV>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, worst);
   tm_quarter_sync(Q);
   if (active)
     for (int m = qt; m < 2 * N; m += 128) out[(size_t)c * 2 * N + m] = acc[m];

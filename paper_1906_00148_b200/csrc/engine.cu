@@ -21,6 +21,7 @@
 #include "../../she_inputs/she_rng.h"
 #include "bootstrap_core.cuh"
 #include "fft_core.cuh"
+#include "dcheck.cuh"
 #include "ks_imma.cuh"
 #include "common.h"
 #include "engine.h"
@@ -985,6 +986,7 @@ __global__ void lvl_gather_kernel(uint32_t* out, const uint32_t* wires, const ui
 __global__ void lane_list_kernel(GateSrc src, uint32_t* lanes, uint32_t* nlanes) {
   __shared__ uint32_t part[1024];
   const uint32_t tid = threadIdx.x, T = blockDim.x, count = src.count;
+  SHE_DCHECK(T <= 1024);
   const uint32_t per = (count + T - 1) / T, g0 = tid * per, g1 = min(count, g0 + per);
   uint32_t cnt = 0;
   for (uint32_t g = g0; g < g1; ++g) {
@@ -1235,6 +1237,7 @@ __global__ void __launch_bounds__(kKs2T, 2) ks2_kernel(KSArgs args) {
 __global__ void ksi_prep_kernel(GateSrc src, const uint32_t* ext, uint32_t ext_stride, uint32_t N,
                                 uint8_t* A, uint32_t K, uint32_t* bprime) {
   const uint32_t g = blockIdx.x;
+  SHE_DCHECK(K == 24 * N && ext_stride >= N + 1);  // 6 words of A per i: 24 bytes
   const int op = g < src.count ? gate_op(src, g) : -1;
   const bool ks = op >= 0 && op < SHE_NOT;
   const uint32_t round = 1u << (32 - 2 * 8 - 1);
@@ -1274,6 +1277,7 @@ __global__ void ksi_prep_kernel(GateSrc src, const uint32_t* ext, uint32_t ext_s
 __global__ void ksi_combine_kernel(GateSrc src, const int32_t* C, uint32_t ncols,
                                    const uint32_t* bprime, uint32_t n) {
   const uint32_t g = blockIdx.x;
+  SHE_DCHECK(g < src.count && 4 * (n + 1) <= ncols && n < src.stride);
   const int op = gate_op(src, g);
   if (op < 0) return;
   uint32_t* o = gate_out(src, g);

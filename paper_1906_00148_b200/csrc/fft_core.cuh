@@ -26,6 +26,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace fft {
 
@@ -39,6 +40,12 @@ constexpr int kN = 1024, kM = 512, kRow = 512;  // complex per scratch row
 // k ^ (bit 7 of k) << 2 -- the forward's stores (k = k2 + 128 h + 16 j) and
 // the inverse's loads (k = lane + 32 m) are conflict-free.
 __device__ __forceinline__ int tslot(int n1, int k2) {
+#ifdef SHE_CHECKED
+  if (n1 < 0 || n1 >= 32 || k2 < 0 || k2 >= 16) {
+    printf("tslot(%d, %d) out of the 32 x 16 row\n", n1, k2);
+    __trap();
+  }
+#endif
   return n1 * 16 + (k2 ^ (((n1 & 1) << 2) | ((n1 >> 1) & 3)));
 }
 __device__ __forceinline__ int fpos(int k) { return k ^ (((k >> 7) & 1) << 2); }

@@ -324,8 +324,9 @@ class Context:
         self.stride = stride(params)
 
     def close(self):
-        if getattr(self, "handle", None):
-            lib().she_ctx_destroy(self.handle)
+        h = getattr(self, "handle", None)
+        if h and lib is not None:  # module globals are gone at interpreter teardown
+            lib().she_ctx_destroy(h)
             self.handle = None
 
     __del__ = close
