@@ -154,11 +154,22 @@ __device__ __forceinline__ void tm_quarter_sync(int q) {
 // Spectrum of one digit row to TMEM: x[j] at column 8 j, y[j] at 8 j + 4
 // (frequency slot fi = 2 j and 2 j + 1), in the order the pair exchange
 // produces them.
+#ifndef SHE_TM_ST_X16
+#define SHE_TM_ST_X16 0
+#endif
 __device__ __forceinline__ void tm_store_spectrum(uint32_t addr, const double2 (&x)[8], const double2 (&y)[8]) {
-  tm_st4(addr, {x[0], y[0], x[1], y[1]});
-  tm_st4(addr + 16, {x[2], y[2], x[3], y[3]});
-  tm_st4(addr + 32, {x[4], y[4], x[5], y[5]});
-  tm_st4(addr + 48, {x[6], y[6], x[7], y[7]});
+  if (SHE_TM_ST_X16) {  // four 16-column stores (needs 16 consecutive registers each)
+    tm_st4(addr, {x[0], y[0], x[1], y[1]});
+    tm_st4(addr + 16, {x[2], y[2], x[3], y[3]});
+    tm_st4(addr + 32, {x[4], y[4], x[5], y[5]});
+    tm_st4(addr + 48, {x[6], y[6], x[7], y[7]});
+  } else {  // sixteen 4-column stores: no register block to assemble
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      tm_st1(addr + 8 * j, x[j]);
+      tm_st1(addr + 8 * j + 4, y[j]);
+    }
+  }
 }
 __device__ __forceinline__ void tm_load_spectrum(uint32_t addr, double2 (&x)[8], double2 (&y)[8]) {
   double2 v[4][4];
