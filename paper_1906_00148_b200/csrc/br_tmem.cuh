@@ -478,8 +478,14 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
           tm_inverse_acc<false, FMA && SHE_TM_FMA_INV>(row_base + sl_i * 256 + (2 * o_i + half) * 64, ln, twp, scr, acc_o,
                                 half ? 0 : 16, nullptr);
       }
-      tm_quarter_sync(Q);  // ACC complete before the next digits
+      // No quarter barrier here: the next forward of warp s = (slot, c) reads
+      // only ACC_c of its slot and writes only rows 2c, 2c + 1 -- exactly what
+      // this warp's own inverse (slot, o = c) just wrote and read -- so the
+      // four warps may enter the next CMux independently (a warp barrier
+      // orders the lanes' shared-memory atomics before their digit loads).
+      __syncwarp();
     }
+    tm_quarter_sync(Q);  // all ACC complete before the extraction
     extract(base, 2);
   }
   if (base < last) {  // the quarter's odd last lane: all four warps on it (slot 0)
