@@ -42,7 +42,7 @@ constexpr size_t kTmScratchBytes = (size_t)4 * fft::kRow * 16;
 constexpr size_t kTmQuarterBytes = kTmAccBytes + kTmAbarBytes + kTmScratchBytes;
 constexpr size_t kTmSmemBytes = 4 * kTmQuarterBytes + 2 * fft::kTw2 * 32 * sizeof(double2);
 #ifndef SHE_TM_PD
-#define SHE_TM_PD 3
+#define SHE_TM_PD 2
 #endif
 #ifndef SHE_TM_FMA_FWD  // transform 3: FMA butterflies in the forward / inverse (A/B builds)
 #define SHE_TM_FMA_FWD 1
@@ -273,16 +273,18 @@ template <int PD>
 struct TmRing {
   double2 b[PD + 1][4];
 };
-template <int PD>
+template <int PD, int U = 0>
 __device__ __forceinline__ void tm_bk_prefetch(const double2* bk_s, TmRing<PD>& ring) {
-  if (PD > 0) tm_bk_unit<0>(bk_s, ring.b[0]);
-  if (PD > 1) tm_bk_unit<1>(bk_s, ring.b[1 % (PD + 1)]);
-  if (PD > 2) tm_bk_unit<2>(bk_s, ring.b[2 % (PD + 1)]);
-  if (PD > 3) tm_bk_unit<3>(bk_s, ring.b[3 % (PD + 1)]);
+  static_assert(PD >= 0 && PD <= 8, "BK prefetch distance");
+  if constexpr (U < PD) {
+    tm_bk_unit<U>(bk_s, ring.b[U % (PD + 1)]);
+    tm_bk_prefetch<PD, U + 1>(bk_s, ring);
+  }
 }
 template <int PD, int NS, int U>
 __device__ __forceinline__ void tm_pw_unit(const double2* bk_s, TmRing<PD>& ring, const double2 (&D)[2][4],
                                            uint32_t row_base, int fi) {
+  // unit U + PD into the buffer unit U - 1 used (PD = 0: unit U itself, just in time)
   if (U + PD < 16) tm_bk_unit<(U + PD < 16 ? U + PD : 0)>(bk_s, ring.b[(U + PD) % (PD + 1)]);
   constexpr int q = U & 3;
   const double2(&b)[4] = ring.b[U % (PD + 1)];
