@@ -226,6 +226,11 @@ she_status she_ctx_enable_timing(she_ctx* ctx, int on);
 she_status she_ctx_timing(she_ctx* ctx, int reset, double* br_ms, double* ks_ms,
                           uint64_t* br_launches, uint64_t* ks_launches);
 
+/* Kernels this library launched for the context's gate passes since the last
+ * reset (lane list, blind rotation, key switch: 4 or 6 per pass; bench.py's
+ * gpu_launches).  reset != 0 zeroes the counter after reading. */
+she_status she_ctx_kernel_launches(she_ctx* ctx, int reset, uint64_t* count);
+
 /* K6: peak Goldilocks modmul throughput of `device` (independent chains of the
  * kernel's own field multiplication on every SM; the roofline denominator). */
 she_status she_bench_modmul_peak(int device, double* modmul_per_s, double* ms);

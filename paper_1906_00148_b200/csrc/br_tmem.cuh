@@ -281,11 +281,11 @@ __device__ __forceinline__ void tm_bk_prefetch(const double2* bk_s, TmRing<PD>& 
     tm_bk_prefetch<PD, U + 1>(bk_s, ring);
   }
 }
-template <int PD, int NS, int U>
+template <int PD, int NS, int U, int NU = 16>
 __device__ __forceinline__ void tm_pw_unit(const double2* bk_s, TmRing<PD>& ring, const double2 (&D)[2][4],
                                            uint32_t row_base, int fi) {
   // unit U + PD into the buffer unit U - 1 used (PD = 0: unit U itself, just in time)
-  if (U + PD < 16) tm_bk_unit<(U + PD < 16 ? U + PD : 0)>(bk_s, ring.b[(U + PD) % (PD + 1)]);
+  if (U + PD < NU) tm_bk_unit<(U + PD < NU ? U + PD : 0)>(bk_s, ring.b[(U + PD) % (PD + 1)]);
   constexpr int q = U & 3;
   const double2(&b)[4] = ring.b[U % (PD + 1)];
 #pragma unroll
@@ -321,6 +321,30 @@ __device__ __forceinline__ void tm_pointwise(const double2* bk_s, TmRing<PD>& ri
   tm_pw_slot<PD, NS, 1>(bk_s, ring, row_base, s);
   tm_pw_slot<PD, NS, 2>(bk_s, ring, row_base, s);
   tm_pw_slot<PD, NS, 3>(bk_s, ring, row_base, s);
+}
+// One lane's pointwise over NF consecutive frequency slots fbase .. fbase +
+// NF - 1 (bk_s points at slot fbase): the per-slot pipelines variant.
+template <int PD, int NF, int F = 0>
+__device__ __forceinline__ void tm_pointwise_range(const double2* bk_s, TmRing<PD>& ring, uint32_t slot_base,
+                                                   int fbase) {
+  if constexpr (F < NF) {
+    const int fi = fbase + F;
+    double2 D[2][4];
+    tm_ld_rows4(slot_base + 4 * fi, D[0]);
+    tm_pw_unit<PD, 1, 4 * F + 0, 4 * NF>(bk_s, ring, D, slot_base, fi);
+    tm_pw_unit<PD, 1, 4 * F + 1, 4 * NF>(bk_s, ring, D, slot_base, fi);
+    tm_pw_unit<PD, 1, 4 * F + 2, 4 * NF>(bk_s, ring, D, slot_base, fi);
+    tm_pw_unit<PD, 1, 4 * F + 3, 4 * NF>(bk_s, ring, D, slot_base, fi);
+    tm_pointwise_range<PD, NF, F + 1>(bk_s, ring, slot_base, fbase);
+  }
+}
+#ifndef SHE_TM_INDEP  // 1: the two lanes of a pipeline as two independent 2-warp pipelines
+#define SHE_TM_INDEP 0
+#endif
+__device__ __forceinline__ void tm_slot_sync(int q, int sl) {  // the 64 threads of (quarter, slot)
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("bar.sync %0, 64;" ::"r"(5 + 2 * q + sl) : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
 struct TmArgs {
@@ -380,7 +404,9 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   const uint32_t nq = gridDim.x * 4, gq = blockIdx.x * 4 + Q;
   const uint32_t first = (uint32_t)(((uint64_t)gq * total) / nq);
   const uint32_t last = (uint32_t)(((uint64_t)(gq + 1) * total) / nq);
+#if !SHE_TM_INDEP
   if (args.stagger && Q) __nanosleep(args.stagger * Q);
+#endif
   const int sl_f = s >> 1, c_f = s & 1;  // forward: slot, component (rows 2 c + j)
   const int sl_i = s >> 1, o_i = s & 1;  // inverse: slot, output (rows 2 o + half)
 
@@ -435,6 +461,9 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   uint32_t base = first;
   for (; base + 1 < last; base += kTmSlots) {  // lane pairs
     prologue(base, 2);
+#if SHE_TM_INDEP
+    if (args.stagger && sl_f == 1) __nanosleep(args.stagger);  // slot 1 a phase behind slot 0
+#endif
     for (uint32_t i = 0; i < n; ++i) {
       const int ln = lane;
       double2* const scr = scratch;
@@ -465,6 +494,17 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
         }
         tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, half, ln, twp, scr, row1);
       }
+#if SHE_TM_INDEP
+      // each slot's two warps: pointwise of their slot over 8 frequency slots each
+      const double2* bk_s = args.bkt + ((size_t)i * 16 + 8 * (s & 1)) * 16 * 32 + ln;
+      TmRing<PD> ring;
+      tm_bk_prefetch<PD>(bk_s, ring);
+      tm_wait_st();
+      tm_slot_sync(Q, sl_f);
+      tm_pointwise_range<PD, 8>(bk_s, ring, row_base + sl_f * 256, 8 * (s & 1));
+      tm_wait_st();
+      tm_slot_sync(Q, sl_f);
+#else
       const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + ln;
       TmRing<PD> ring;
       tm_bk_prefetch<PD>(bk_s, ring);
@@ -473,6 +513,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       tm_pointwise<PD, 2>(bk_s, ring, row_base, s);
       tm_wait_st();
       tm_quarter_sync(Q);
+#endif
       {  // inverse transforms of outputs (o, hi), (o, lo) of slot sl_i
         uint32_t* acc_o = acc + (sl_i * 2 + o_i) * N;
 #pragma unroll 1

@@ -1500,6 +1500,7 @@ struct she_ctx {
   std::vector<cudaEvent_t> ev_marks;  // triples: before BR, after BR, after KS
   double br_ms = 0, ks_ms = 0;
   uint64_t br_launches = 0, ks_launches = 0;
+  uint64_t kernel_launches = 0;  // every kernel of the gate passes (she_ctx_kernel_launches)
   // gate capture (she_ctx_capture; test instrumentation)
   uint32_t cap_every = 0;
   uint64_t cap_seed = 0, cap_ordinal = 0;
@@ -1899,6 +1900,8 @@ she_status run_gates(she_ctx* ctx, GateSrc src, cudaStream_t stream) {
     if (ctx->timing) mark(ctx, stream);
     ctx->br_launches++;
     ctx->ks_launches++;
+    // lane list + blind rotation + key switch (tensor-core path: prep, GEMM, combine)
+    ctx->kernel_launches += 2 + (ctx->ksi ? 3 : 1);
   }
   return SHE_OK;
 }
@@ -2152,6 +2155,14 @@ she_status she_ctx_timing(she_ctx* ctx, int reset, double* br_ms, double* ks_ms,
     ctx->br_ms = ctx->ks_ms = 0;
     ctx->br_launches = ctx->ks_launches = 0;
   }
+  return SHE_OK;
+}
+
+she_status she_ctx_kernel_launches(she_ctx* ctx, int reset, uint64_t* count) {
+  if (!ctx || !count) return fail(SHE_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  *count = ctx->kernel_launches;
+  if (reset) ctx->kernel_launches = 0;
   return SHE_OK;
 }
 

@@ -113,6 +113,7 @@ def lib() -> ctypes.CDLL:
             "she_bench_fp64_peak": ([ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
             "she_ctx_br_engine": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+            "she_ctx_kernel_launches": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
             "she_conv_shift_acc": ([_vp, _vp] + [ctypes.c_int] * 5 + [_vp] + [ctypes.c_int] * 6
                                    + [_vp, ctypes.POINTER(ctypes.c_int), _vp], ctypes.c_int),
             "she_fc_shift_acc": ([_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
@@ -344,6 +345,12 @@ class Context:
                                     ctypes.byref(nb), ctypes.byref(nk)))
         return {"br_ms": br.value, "ks_ms": ks.value, "br_launches": nb.value,
                 "ks_launches": nk.value}
+
+    def kernel_launches(self, reset: bool = False) -> int:
+        """Kernels launched by this context's gate passes (she_ctx_kernel_launches)."""
+        c = ctypes.c_uint64()
+        _check(lib().she_ctx_kernel_launches(self.handle, int(reset), ctypes.byref(c)))
+        return c.value
 
 
 def modmul_peak(device: int = 0) -> tuple[float, float]:
