@@ -516,6 +516,8 @@ def engine_options(args) -> dict:
         opts["fft_store"] = args.fft_store
     if args.fft_stagger_ns:
         opts["fft_stagger_ns"] = args.fft_stagger_ns
+    if args.fft_chunk:
+        opts["fft_chunk"] = args.fft_chunk
     if args.ks_kernel != "default":
         opts["ks_kernel"] = args.ks_kernel
     return opts
@@ -884,6 +886,8 @@ def main():
                     help="FFT engine spectra store (she_ctx_options.fft_store): shared or tensor memory")
     ap.add_argument("--fft-stagger-ns", type=int, default=0,
                     help="TMEM engine: start delay per quarter pipeline (ns)")
+    ap.add_argument("--fft-chunk", type=int, default=0,
+                    help="TMEM engine: CMux iterations per work-queue unit (-1: static lane split)")
     ap.add_argument("--ks-kernel", default="default", choices=["default", "general", "cuda", "imma", "tcgen05"],
                     help="key-switch kernel (she_ctx_options.ks_kernel)")
     ap.add_argument("--count", type=int, default=COUNT,

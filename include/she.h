@@ -189,6 +189,10 @@ typedef struct {
                      DESIGN.md §4.2e; no other shape option applies) */
   int fft_stagger_ns;/* TMEM engine: start delay of quarter q = q x this (ns),
                      0..100000 (phase offset between the pipelines) */
+  int fft_chunk;  /* TMEM engine: CMux iterations per unit of the device-wide
+                     work queue that serves batches of more than two lanes per
+                     pipeline: 0 = default (32), 1..1024, or
+                     -1 = the static contiguous lane split only */
   int reserved[1];/* must be 0 */
 } she_ctx_options;
 

@@ -356,7 +356,33 @@ struct TmArgs {
   uint32_t ext_stride;
   br::Geometry geo;
   uint32_t stagger;  // ns of start delay per quarter index (phase offset)
+  // Work queue (wide batches; see br_fft_tm_kernel): sched[0] = next unit,
+  // sched[1 + p] = chunks of lane pair p completed; acc_save[p] = the pair's
+  // two accumulators between chunks.  chunk = CMux iterations per unit
+  // (>= n: the static contiguous split only).
+  uint32_t* sched;
+  uint32_t* acc_save;
+  uint32_t chunk;
 };
+
+// Completed-chunk counter of a lane pair: published with release semantics
+// after the pair's accumulators were written back (and fenced), awaited with
+// acquire loads by one thread of the quarter that runs the next chunk.  The
+// unit it waits for was taken from the queue earlier by a resident CTA that
+// waits only on still earlier units, so the wait is finite; the bound turns a
+// broken invariant into a launch error instead of a hang.
+__device__ __forceinline__ void tm_publish(uint32_t* flag, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tm_await(const uint32_t* flag, uint32_t want) {
+  for (uint32_t spins = 0;; ++spins) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= want) return;
+    __nanosleep(256);
+    if (spins > (1u << 23)) __trap();  // > 2 s
+  }
+}
 
 __device__ __forceinline__ uint32_t tm_alloc_all(uint32_t* slot, int warp) {
   if (warp == 0) {
@@ -380,11 +406,25 @@ __device__ __forceinline__ void tm_free_all(uint32_t tmem, int warp) {
 
 // K3, TMEM engine: one persistent CTA of 16 warps per SM, four independent
 // quarter pipelines of two lanes each (see the file comment).
+//
+// Work distribution.  A unit is (lane pair or single lane, CMux iterations
+// [i0, i1)).  Narrow batches (<= 2 lanes per pipeline) and chunk >= n use the
+// static split: pipeline gq runs the contiguous lanes [first, last) as pairs,
+// an odd last lane alone, each for all n iterations.  Wide batches go through
+// a device-wide queue of (pair, chunk) units in chunk-major order (every
+// pair's chunk k before any chunk k + 1; an odd lane first, whole): a pipeline
+// takes the next unit, waits until the pair's previous chunk is published,
+// reloads the two accumulators from acc_save, runs the chunk and writes them
+// back (or extracts after the last chunk).  All pipelines then finish within
+// one chunk of each other instead of one 500-iteration lane apart: the
+// static split of 4797 lanes over 592 pipelines leaves 61 of them a ninth
+// lane that runs alone at the end (wave tail).
 template <int PD = kTmPrefetch, bool FMA = false>
 __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   constexpr int N = fft::kN;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t tmem_slot;
+  __shared__ uint32_t unit_info[4][8];
   const GateSrc& src = args.src;
   const br::Geometry& geo = args.geo;
   const uint32_t n = geo.n;
@@ -400,21 +440,22 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   const uint32_t tmem = tm_alloc_all(&tmem_slot, warp);  // includes the table barrier
   const uint32_t row_base = __shfl_sync(0xffffffffu, tmem + ((uint32_t)(32 * Q) << 16), 0);
 
-  const uint32_t total = *args.nlanes;
-  const uint32_t nq = gridDim.x * 4, gq = blockIdx.x * 4 + Q;
-  const uint32_t first = (uint32_t)(((uint64_t)gq * total) / nq);
-  const uint32_t last = (uint32_t)(((uint64_t)(gq + 1) * total) / nq);
+  // the next unit of this pipeline, decoded by its thread 0 (nothing of the
+  // queue stays in registers across the CMux loop): lanes base .. base + nsl - 1
+  // (nsl = 0: no more work), iterations [i0, i1); [4] = the static split's cursor
+  uint32_t* const unit = unit_info[Q];
+  if (qt == 0) unit[4] = (uint32_t)(((uint64_t)(blockIdx.x * 4 + Q) * *args.nlanes) / (gridDim.x * 4));
 #if !SHE_TM_INDEP
   if (args.stagger && Q) __nanosleep(args.stagger * Q);
 #endif
   const int sl_f = s >> 1, c_f = s & 1;  // forward: slot, component (rows 2 c + j)
   const int sl_i = s >> 1, o_i = s & 1;  // inverse: slot, output (rows 2 o + half)
 
-  // the gate prologue of the lanes in slots 0 .. nsl - 1 (a-bar, test vector)
-  SHE_DCHECK(last <= total);
-  auto prologue = [&](uint32_t base, int nsl) {
+  // the gate prologue of the lanes in slots 0 .. nsl - 1: a-bar, then the
+  // accumulators (the test vector, or the pair's saved state `resume`)
+  auto prologue = [&](uint32_t base, int nsl, const uint32_t* resume) {
     for (int sl = 0; sl < nsl; ++sl) {
-      SHE_DCHECK(base + sl < last && n < 512);
+      SHE_DCHECK(base + sl < *args.nlanes && n < 512);
       const uint32_t e = args.lanes[base + sl];
       const uint32_t gate = e & 0x7FFFFFFFu, hh = e >> 31;
       SHE_DCHECK(gate < src.count && (hh == 0 || gate_op(src, gate) == SHE_MUX));
@@ -430,12 +471,18 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       }
     }
     tm_quarter_sync(Q);
-    for (int sl = 0; sl < nsl; ++sl) {
-      const uint32_t bbar = abar[sl * 512 + n];
-      uint32_t* a = acc + sl * 2 * N;
-      for (int m = qt; m < N; m += 128) {
-        a[m] = 0;
-        a[N + m] = br::testvec_coeff(m, bbar, N);
+    if (resume) {  // written by another SM: read through L2
+      const uint4* r4 = reinterpret_cast<const uint4*>(resume);
+      uint4* a4 = reinterpret_cast<uint4*>(acc);
+      for (int m = qt; m < kTmSlots * 2 * N / 4; m += 128) a4[m] = __ldcg(r4 + m);
+    } else {
+      for (int sl = 0; sl < nsl; ++sl) {
+        const uint32_t bbar = abar[sl * 512 + n];
+        uint32_t* a = acc + sl * 2 * N;
+        for (int m = qt; m < N; m += 128) {
+          a[m] = 0;
+          a[N + m] = br::testvec_coeff(m, bbar, N);
+        }
       }
     }
     tm_quarter_sync(Q);
@@ -458,100 +505,149 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
     tm_quarter_sync(Q);
   };
 
-  uint32_t base = first;
-  for (; base + 1 < last; base += kTmSlots) {  // lane pairs
-    prologue(base, 2);
-#if SHE_TM_INDEP
-    if (args.stagger && sl_f == 1) __nanosleep(args.stagger);  // slot 1 a phase behind slot 0
-#endif
-    for (uint32_t i = 0; i < n; ++i) {
-      const int ln = lane;
-      double2* const scr = scratch;
-      const double2* const twp = tw;
-      {  // forward transforms of digit rows 2c, 2c + 1 of slot sl_f
-        // both rows' digit fields from one rotation pass; the j = 1 fields wait
-        // in the (not yet written) TMEM columns of row 2c + 1 during the first
-        // transform instead of in 16 registers
-        const uint32_t row0 = row_base + sl_f * 256 + (2 * c_f) * 64, row1 = row0 + 64;
-        uint32_t u[32];
-        {
-          uint32_t pk1[16];
-          tm_load_fields2(geo, ln, acc + (sl_f * 2 + c_f) * N, abar[sl_f * 512 + i], u, pk1);
-          tm_st_u16(row1, pk1);
-        }
-        const double half = (double)(1u << (geo.bg_bits - 1));
-        tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, half, ln, twp, scr, row0);
-        {
-          uint32_t pk1[16];
-          tm_wait_st();  // this thread's stash store (long done) before reading it back
-          tm_ld_u16(row1, pk1);
-          tm_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            u[2 * k] = pk1[k] & 0xFFFFu;
-            u[2 * k + 1] = pk1[k] >> 16;
+  for (;;) {
+    if (qt == 0) {
+      const uint32_t total = *args.nlanes, nq = gridDim.x * 4;
+      const uint32_t chunk = args.chunk ? args.chunk : n;
+      uint32_t ubase = 0, unsl = 0, ui0 = 0, ui1 = n;
+      if (chunk < n && total > 2 * nq) {
+        // the queue: npairs pairs x nchunks chunks, chunk-major (+ an odd lane as unit 0)
+        const uint32_t npairs = total >> 1, odd = total & 1, nchunks = (n + chunk - 1) / chunk;
+        uint32_t u = atomicAdd(args.sched, 1u);
+        if (u < npairs * nchunks + odd) {
+          if (odd && u == 0) {
+            ubase = total - 1;
+            unsl = 1;
+          } else {
+            u -= odd;
+            const uint32_t k = u / npairs, pair = u - k * npairs;
+            ubase = 2 * pair;
+            unsl = 2;
+            ui0 = k * chunk;
+            ui1 = min(n, ui0 + chunk);
+            if (k) tm_await(args.sched + 1 + pair, k);  // the pair's previous chunk is written back
           }
         }
-        tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, half, ln, twp, scr, row1);
+      } else {
+        const uint32_t last = (uint32_t)(((uint64_t)(blockIdx.x * 4 + Q + 1) * total) / nq);
+        ubase = unit[4];
+        unsl = min(2u, last - min(last, ubase));
+        unit[4] = ubase + unsl;
       }
+      unit[0] = ubase;
+      unit[1] = unsl;
+      unit[2] = ui0;
+      unit[3] = ui1;
+    }
+    tm_quarter_sync(Q);  // unit[] is rewritten only after the barriers below
+    const int nsl = (int)unit[1];
+    if (nsl == 0) break;
+    {
+      const uint32_t base = unit[0], i0 = unit[2];
+      prologue(base, nsl, i0 ? args.acc_save + (size_t)(base >> 1) * (kTmSlots * 2 * N) : nullptr);
+    }
+    const uint32_t i0 = unit[2], i1 = unit[3];
+
+    if (nsl == 2) {  // a lane pair
 #if SHE_TM_INDEP
-      // each slot's two warps: pointwise of their slot over 8 frequency slots each
-      const double2* bk_s = args.bkt + ((size_t)i * 16 + 8 * (s & 1)) * 16 * 32 + ln;
-      TmRing<PD> ring;
-      tm_bk_prefetch<PD>(bk_s, ring);
-      tm_wait_st();
-      tm_slot_sync(Q, sl_f);
-      tm_pointwise_range<PD, 8>(bk_s, ring, row_base + sl_f * 256, 8 * (s & 1));
-      tm_wait_st();
-      tm_slot_sync(Q, sl_f);
-#else
-      const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + ln;
-      TmRing<PD> ring;
-      tm_bk_prefetch<PD>(bk_s, ring);
-      tm_wait_st();
-      tm_quarter_sync(Q);
-      tm_pointwise<PD, 2>(bk_s, ring, row_base, s);
-      tm_wait_st();
-      tm_quarter_sync(Q);
+      if (args.stagger && sl_f == 1) __nanosleep(args.stagger);  // slot 1 a phase behind slot 0
 #endif
-      {  // inverse transforms of outputs (o, hi), (o, lo) of slot sl_i
-        uint32_t* acc_o = acc + (sl_i * 2 + o_i) * N;
+      for (uint32_t i = i0; i < i1; ++i) {
+        const int ln = lane;
+        double2* const scr = scratch;
+        const double2* const twp = tw;
+        {  // forward transforms of digit rows 2c, 2c + 1 of slot sl_f
+          // both rows' digit fields from one rotation pass; the j = 1 fields wait
+          // in the (not yet written) TMEM columns of row 2c + 1 during the first
+          // transform instead of in 16 registers
+          const uint32_t row0 = row_base + sl_f * 256 + (2 * c_f) * 64, row1 = row0 + 64;
+          uint32_t u[32];
+          {
+            uint32_t pk1[16];
+            tm_load_fields2(geo, ln, acc + (sl_f * 2 + c_f) * N, abar[sl_f * 512 + i], u, pk1);
+            tm_st_u16(row1, pk1);
+          }
+          const double half = (double)(1u << (geo.bg_bits - 1));
+          tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, half, ln, twp, scr, row0);
+          {
+            uint32_t pk1[16];
+            tm_wait_st();  // this thread's stash store (long done) before reading it back
+            tm_ld_u16(row1, pk1);
+            tm_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              u[2 * k] = pk1[k] & 0xFFFFu;
+              u[2 * k + 1] = pk1[k] >> 16;
+            }
+          }
+          tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, half, ln, twp, scr, row1);
+        }
+#if SHE_TM_INDEP
+        // each slot's two warps: pointwise of their slot over 8 frequency slots each
+        const double2* bk_s = args.bkt + ((size_t)i * 16 + 8 * (s & 1)) * 16 * 32 + ln;
+        TmRing<PD> ring;
+        tm_bk_prefetch<PD>(bk_s, ring);
+        tm_wait_st();
+        tm_slot_sync(Q, sl_f);
+        tm_pointwise_range<PD, 8>(bk_s, ring, row_base + sl_f * 256, 8 * (s & 1));
+        tm_wait_st();
+        tm_slot_sync(Q, sl_f);
+#else
+        const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + ln;
+        TmRing<PD> ring;
+        tm_bk_prefetch<PD>(bk_s, ring);
+        tm_wait_st();
+        tm_quarter_sync(Q);
+        tm_pointwise<PD, 2>(bk_s, ring, row_base, s);
+        tm_wait_st();
+        tm_quarter_sync(Q);
+#endif
+        {  // inverse transforms of outputs (o, hi), (o, lo) of slot sl_i
+          uint32_t* acc_o = acc + (sl_i * 2 + o_i) * N;
 #pragma unroll 1
-        for (int half = 0; half < 2; ++half)
-          tm_inverse_acc<false, FMA && SHE_TM_FMA_INV>(row_base + sl_i * 256 + (2 * o_i + half) * 64, ln, twp, scr, acc_o,
-                                half ? 0 : 16, nullptr);
+          for (int half = 0; half < 2; ++half)
+            tm_inverse_acc<false, FMA && SHE_TM_FMA_INV>(row_base + sl_i * 256 + (2 * o_i + half) * 64, ln, twp, scr, acc_o,
+                                  half ? 0 : 16, nullptr);
+        }
+        // No quarter barrier here: the next forward of warp s = (slot, c) reads
+        // only ACC_c of its slot and writes only rows 2c, 2c + 1 -- exactly what
+        // this warp's own inverse (slot, o = c) just wrote and read -- so the
+        // four warps may enter the next CMux independently (a warp barrier
+        // orders the lanes' shared-memory atomics before their digit loads).
+        __syncwarp();
       }
-      // No quarter barrier here: the next forward of warp s = (slot, c) reads
-      // only ACC_c of its slot and writes only rows 2c, 2c + 1 -- exactly what
-      // this warp's own inverse (slot, o = c) just wrote and read -- so the
-      // four warps may enter the next CMux independently (a warp barrier
-      // orders the lanes' shared-memory atomics before their digit loads).
-      __syncwarp();
-    }
-    tm_quarter_sync(Q);  // all ACC complete before the extraction
-    extract(base, 2);
-  }
-  if (base < last) {  // the quarter's odd last lane: all four warps on it (slot 0)
-    prologue(base, 1);
-    for (uint32_t i = 0; i < n; ++i) {
-      {  // warp s: forward transform of digit row s
-        uint32_t u[32];
-        fbr_load_fields(geo, s, lane, acc, abar[i], u);
-        tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, (double)(1u << (geo.bg_bits - 1)), lane, tw, scratch, row_base + s * 64);
+      tm_quarter_sync(Q);  // all ACC complete before the extraction / the write-back
+    } else {  // a single lane: all four warps on it (slot 0)
+      for (uint32_t i = i0; i < i1; ++i) {
+        {  // warp s: forward transform of digit row s
+          uint32_t u[32];
+          fbr_load_fields(geo, s, lane, acc, abar[i], u);
+          tm_forward_fields<FMA && SHE_TM_FMA_FWD>(u, (double)(1u << (geo.bg_bits - 1)), lane, tw, scratch, row_base + s * 64);
+        }
+        const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + lane;
+        TmRing<PD> ring;
+        tm_bk_prefetch<PD>(bk_s, ring);
+        tm_wait_st();
+        tm_quarter_sync(Q);
+        tm_pointwise<PD, 1>(bk_s, ring, row_base, s);
+        tm_wait_st();
+        tm_quarter_sync(Q);
+        // warp s: inverse of product row s = (o, half) = (s >> 1, s & 1)
+        tm_inverse_acc<false, FMA && SHE_TM_FMA_INV>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, nullptr);
+        tm_quarter_sync(Q);
       }
-      const double2* bk_s = args.bkt + ((size_t)i * 16 + 4 * s) * 16 * 32 + lane;
-      TmRing<PD> ring;
-      tm_bk_prefetch<PD>(bk_s, ring);
-      tm_wait_st();
-      tm_quarter_sync(Q);
-      tm_pointwise<PD, 1>(bk_s, ring, row_base, s);
-      tm_wait_st();
-      tm_quarter_sync(Q);
-      // warp s: inverse of product row s = (o, half) = (s >> 1, s & 1)
-      tm_inverse_acc<false, FMA && SHE_TM_FMA_INV>(row_base + s * 64, lane, tw, scratch, acc + (s >> 1) * N, (s & 1) ? 0 : 16, nullptr);
-      tm_quarter_sync(Q);
     }
-    extract(base, 1);
+    const uint32_t base = unit[0];
+    if (unit[3] == n) {
+      extract(base, (int)unit[1]);
+    } else {  // hand the pair's accumulators to whichever pipeline takes its next chunk
+      const uint4* a4 = reinterpret_cast<const uint4*>(acc);
+      uint4* w4 = reinterpret_cast<uint4*>(args.acc_save + (size_t)(base >> 1) * (kTmSlots * 2 * N));
+      for (int m = qt; m < kTmSlots * 2 * N / 4; m += 128) __stcg(w4 + m, a4[m]);
+      __threadfence();
+      tm_quarter_sync(Q);
+      if (qt == 0) tm_publish(args.sched + 1 + (base >> 1), unit[3] / args.chunk);
+    }
   }
   tm_free_all(tmem, warp);
 }

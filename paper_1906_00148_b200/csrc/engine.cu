@@ -357,6 +357,7 @@ struct FftVar<3> {  // v2's tables and scaling, DIT/FMA DFT16s (fft_core.cuh)
 };
 constexpr int kFftDefaultVariant = 2;
 constexpr int kFftDefaultStreams = 1;  // br_fft_kernel (1) or the two-stream br_fft2s_kernel (2)
+constexpr uint32_t kTmDefaultChunk = 32;  // TMEM engine: CMux iterations per work-queue unit
 constexpr int kFftDefaultStore = 2;    // spectra in shared memory (1) or tensor memory (2)
 template <int V>
 constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double2); }
@@ -1446,6 +1447,10 @@ struct she_ctx {
   uint64_t* itw = nullptr;
   uint32_t* ext = nullptr;
   uint32_t* lane_buf = nullptr;  // compact lane list (+ count at [ext_lanes])
+  // TMEM engine work queue (br_tmem.cuh): next-unit counter + one progress word
+  // per lane pair; the pairs' accumulators between chunks (16 KB per pair)
+  uint32_t* tm_sched = nullptr;
+  uint32_t* tm_save = nullptr;
   size_t ext_lanes = 0;
   int sms = 148;
   // blind-rotation launch shape: G lanes served in lock step by one persistent
@@ -1461,6 +1466,7 @@ struct she_ctx {
   int fft_streams = 1;             // 2: br_fft2s_kernel (two lanes per warp, skewed)
   int fft_store = kFftDefaultStore;  // 1: spectra in shared memory, 2: in TMEM (br_fft_tm_kernel)
   uint32_t fft_stagger = 0;          // TMEM engine: start delay per quarter (ns)
+  uint32_t fft_chunk = kTmDefaultChunk;  // TMEM engine: CMux iterations per queue unit (>= n: static split)
   double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain (shared-memory engine)
   double2* bkt = nullptr;  // [n][16 fi][16 plane][32] the same for the TMEM engine
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
@@ -1619,12 +1625,20 @@ she_status ensure_ext(she_ctx* ctx, size_t lanes) {
     CK(cudaDeviceSynchronize());
     cudaFree(ctx->ext);
     cudaFree(ctx->lane_buf);
+    cudaFree(ctx->tm_sched);
+    cudaFree(ctx->tm_save);
     ctx->ext = nullptr;
     ctx->lane_buf = nullptr;
+    ctx->tm_sched = nullptr;
+    ctx->tm_save = nullptr;
   }
   size_t want = std::max(lanes, (size_t)1024);
   CK(cudaMalloc(&ctx->ext, want * ctx->ext_stride * 4));
   CK(cudaMalloc(&ctx->lane_buf, (want + 1) * 4));  // list + count
+  if (ctx->fft_g && ctx->fft_store == 2 && ctx->fft_chunk < ctx->p.n) {
+    CK(cudaMalloc(&ctx->tm_sched, (want / 2 + 1) * 4));
+    CK(cudaMalloc(&ctx->tm_save, (want / 2) * kTmAccBytes));
+  }
   ctx->ext_lanes = want;
   return SHE_OK;
 }
@@ -1712,6 +1726,12 @@ she_status launch_br_fft_tm(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cud
   cudaLaunchConfig_t cfg = {};
   // four two-lane quarter pipelines per CTA, one CTA per SM
   cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>((max_lanes + 7) / 8, (size_t)ctx->sms)));
+  // the work queue serves batches of more than two lanes per pipeline
+  const bool queued = ctx->tm_sched && max_lanes > (size_t)8 * cfg.gridDim.x;
+  f.sched = ctx->tm_sched;
+  f.acc_save = ctx->tm_save;
+  f.chunk = queued ? ctx->fft_chunk : ctx->p.n;
+  if (queued) CK(cudaMemsetAsync(ctx->tm_sched, 0, (std::min(max_lanes, ctx->ext_lanes) / 2 + 1) * 4, stream));
   cfg.blockDim = dim3(512);
   cfg.dynamicSmemBytes = kTmSmemBytes;
   cfg.stream = stream;
@@ -1974,6 +1994,11 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     return fail(SHE_ERR_ARG, "fft_store = 2 (TMEM engine): transform 2 or 3 only, no lane/group/prefetch/stream options");
   if (o.fft_stagger_ns < 0 || o.fft_stagger_ns > 100000)
     return fail(SHE_ERR_ARG, "fft_stagger_ns=%d", o.fft_stagger_ns);
+  if (o.fft_chunk < -1 || o.fft_chunk > 1024) return fail(SHE_ERR_ARG, "fft_chunk=%d", o.fft_chunk);
+  if (o.fft_chunk && (!use_fft || o.fft_store == 1 ||
+                      (o.fft_store == 0 && (o.fft_lanes || o.fft_variant || o.fft_groups || o.fft_prefetch ||
+                                            o.fft_streams))))
+    return fail(SHE_ERR_ARG, "fft_chunk applies to the TMEM engine only");
   if (o.fft_prefetch < 0 || o.fft_prefetch > 3)
     return fail(SHE_ERR_ARG, "fft_prefetch=%d", o.fft_prefetch);
   if (o.fft_prefetch >= 2 && (o.fft_groups == 2 || o.fft_variant == 1 ||
@@ -2009,6 +2034,7 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   // directions, §4.2e), the shared-memory engine to transform 2
   ctx->fft_v = o.fft_variant ? o.fft_variant : ctx->fft_store == 2 ? 3 : kFftDefaultVariant;
   ctx->fft_stagger = (uint32_t)o.fft_stagger_ns;
+  ctx->fft_chunk = o.fft_chunk < 0 ? 0xFFFFFFFFu : o.fft_chunk ? (uint32_t)o.fft_chunk : kTmDefaultChunk;
   ctx->fft_pre = o.fft_prefetch == 0 ? 16 : o.fft_prefetch == 3 ? 0 : o.fft_prefetch == 2 ? 8 : 16;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
@@ -2111,6 +2137,8 @@ she_status she_ctx_destroy(she_ctx* ctx) {
   cudaFree(ctx->itw);
   cudaFree(ctx->ext);
   cudaFree(ctx->lane_buf);
+  cudaFree(ctx->tm_sched);
+  cudaFree(ctx->tm_save);
   cudaFree(ctx->h_ops);
   cudaFree(ctx->h_io);
   cudaFree(ctx->table);

@@ -48,18 +48,19 @@ class she_ctx_options(ctypes.Structure):
                 ("ks_kernel", ctypes.c_int), ("fft_variant", ctypes.c_int),
                 ("fft_groups", ctypes.c_int), ("fft_prefetch", ctypes.c_int),
                 ("fft_streams", ctypes.c_int), ("fft_store", ctypes.c_int),
-                ("fft_stagger_ns", ctypes.c_int), ("reserved", ctypes.c_int * 1)]
+                ("fft_stagger_ns", ctypes.c_int), ("fft_chunk", ctypes.c_int),
+                ("reserved", ctypes.c_int * 1)]
 
     ENGINES = {"default": 0, "fft": 1, "ntt": 2}
 
     @classmethod
     def of(cls, engine="default", fft_lanes=0, ntt_shape=(0, 0), ks_kernel="default",
            fft_variant=0, fft_groups=0, fft_prefetch=0, fft_streams=0, fft_store="default",
-           fft_stagger_ns=0):
+           fft_stagger_ns=0, fft_chunk=0):
         return cls(cls.ENGINES[engine], fft_lanes, ntt_shape[0], ntt_shape[1],
                    {"default": 0, "general": 1, "cuda": 2, "imma": 3, "tcgen05": 4}[ks_kernel], fft_variant,
                    fft_groups, fft_prefetch, fft_streams,
-                   {"default": 0, "smem": 1, "tmem": 2}[fft_store], fft_stagger_ns)
+                   {"default": 0, "smem": 1, "tmem": 2}[fft_store], fft_stagger_ns, fft_chunk)
 
 
 class she_circuit_stats(ctypes.Structure):

@@ -296,13 +296,18 @@ ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3
                "fft5-v3": dict(engine="fft", fft_lanes=5, fft_prefetch=3, fft_variant=3),
                "fft-smem": dict(engine="fft", fft_store="smem"),
                "fft-tmem-stagger": dict(engine="fft", fft_store="tmem", fft_stagger_ns=20000),
-               "fft-tmem-v2": dict(engine="fft", fft_store="tmem", fft_variant=2)}
+               "fft-tmem-v2": dict(engine="fft", fft_store="tmem", fft_variant=2),
+               # TMEM engine work queue: static split only, ragged last chunk (500 = 71 x 7 + 3),
+               # two chunks of 499 + 1
+               "fft-tmem-static": dict(fft_chunk=-1), "fft-tmem-chunk7": dict(fft_chunk=7),
+               "fft-tmem-chunk499": dict(fft_store="tmem", fft_chunk=499)}
 
 
 @pytest.mark.parametrize("engine", ["ntt", "fft3", "fft2x2", "fft-v1", "fft-2groups",
                                     "fft5-noprefetch", "ks-imma", "ks-cuda", "fft-v3", "fft5-v3",
                                     "ks-tcgen05", "fft-2streams", "fft-smem", "fft-tmem-stagger",
-                                    "fft-tmem-v2"])
+                                    "fft-tmem-v2", "fft-tmem-static", "fft-tmem-chunk7",
+                                    "fft-tmem-chunk499"])
 def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with the
     spectra in tensor memory (br_fft_tm_kernel); the Goldilocks
@@ -317,7 +322,8 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
                                   "fft-2groups": 4, "fft5-noprefetch": 5, "ks-imma": 8,
                                   "ks-cuda": 8, "fft-v3": 4, "fft5-v3": 5, "ks-tcgen05": 8,
                                   "fft-2streams": 4, "fft-smem": 4, "fft-tmem-stagger": 8,
-                                  "fft-tmem-v2": 8}[engine]
+                                  "fft-tmem-v2": 8, "fft-tmem-static": 8, "fft-tmem-chunk7": 8,
+                                  "fft-tmem-chunk499": 8}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
     she.she_gate_batch_ops(ctx, dev(np.asarray(ops, np.uint8)), dev(a), dev(b), dev(c), out)
@@ -327,6 +333,29 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
     bad = [g for g, op, d, bit in rows if digest(got[g, : P.n + 1]) != d]
     assert not bad, f"{engine}: {len(bad)} gates differ from the oracle, first {bad[:8]}"
     ctx.close()
+
+
+@pytest.mark.parametrize("parity", [0, 1])
+def test_config1_work_queue_even_and_odd_lane_counts(cuda, env1, config1_outputs, parity):
+    """The TMEM engine's work queue (wide batches: (lane pair, chunk) units, an
+    odd lane first and whole) on prefixes of config 1 with an even and an odd
+    lane count, both wide enough for the queue (> 2 lanes per pipeline), and
+    twice on the same context (the queue words are reset per launch)."""
+    P = env1.P
+    ops, bits, (a, b, c), _ = config1_outputs
+    m = 2000  # a multiple of 4 (the op bytes travel as int32 words)
+    while si.br_lanes(ops[:m]) % 2 != parity:
+        m += 4
+    assert si.br_lanes(ops[:m]) > 2 * 4 * 160
+    rows = read_digests(1)
+    for rep in range(2):
+        out = torch.zeros((m, P.stride), dtype=torch.int32, device="cuda")
+        she.she_gate_batch_ops(env1.ctx, dev(np.asarray(ops[:m], np.uint8)), dev(a[:m]), dev(b[:m]),
+                               dev(c[:m]), out)
+        torch.cuda.synchronize()
+        got = host(out)
+        bad = [g for g, op, d, bit in rows[:m] if digest(got[g, : P.n + 1]) != d]
+        assert not bad, f"{len(bad)} gates differ from the oracle, first {bad[:8]}"
 
 
 def env0_ctx():
