@@ -58,6 +58,7 @@ FP64_EXECUTED_PER_CMUX = {1: 176_129, 2: 183_875, 8: 171_074}  # 8: the TMEM eng
 # radix, 4 M log2 M - 6 M + 8 = 15,368 flops) with every instruction a fused
 # multiply-add (2 flops), plus the pointwise sum (4 DFMA per complex
 # multiply-add, 512 x 4 outputs x 4 rows) = 8 x 7,684 + 32,768 = 94,240.
+TM_DEFAULT_CHUNK = 32  # include/she.h she_ctx_options.fft_chunk default
 FP64_LOWER_BOUND_PER_CMUX = 8 * (4 * 512 * 9 - 6 * 512 + 8) // 2 + 512 * 4 * 4 * 4
 MODMUL_PER_LANE = {1024: 19_456_000, 256: 1_048_576}  # n[(k+1)l+(k+1)](N/2)log2N + n(k+1)l(k+1)N
 WORKLOAD = ("config1: 4096 independent bootstrapped gates, ops uniform over "
@@ -464,10 +465,10 @@ def leveled_units(ctx, sk, P, words=720, width=16):
     return res
 
 
-def batch_sweep(ctx, sk, P, sizes=(148, 740, 1480, 4096, 8192, 16384, 32768)):
-    """Gates/s against the batch size (config-1 gates; one lane per CTA below
-    148 lanes, G = 5 lock-step lanes per CTA above): where the persistent
-    kernel's waves fill the 148 SMs (`--sweep`)."""
+def batch_sweep(ctx, sk, P, sizes=(40, 148, 300, 500, 740, 1000, 1480, 4096, 8192, 16384, 32768)):
+    """Gates/s against the batch size (config-1 gates): where the persistent
+    kernel's pipelines fill the 148 SMs and how narrow levels of a circuit run
+    (`--sweep`)."""
     import torch
     from paper_1906_00148_b200 import she
     res = []
@@ -646,6 +647,16 @@ def run_she(args):
         slots = sms * engine * (2 if engine == 2 else 1)
         kname = "br_fft_tm_kernel" if engine == 8 else "br_fft_kernel"
         rounds = -(-lanes_rank // slots)
+        wave = {"lanes": lanes_rank, "slots_per_round": slots, "rounds": rounds,
+                "last_round_fill": round(lanes_rank / slots - (rounds - 1), 3)}
+        chunk = args.fft_chunk or TM_DEFAULT_CHUNK
+        if engine == 8 and 0 < chunk < P.n and lanes_rank > 2 * 4 * sms:
+            # the TMEM engine's work queue (she_ctx_options.fft_chunk): (lane pair, chunk) units
+            units = (lanes_rank // 2) * -(-P.n // chunk) + lanes_rank % 2
+            wave = {"lanes": lanes_rank, "work_queue": {
+                "chunk_cmux": chunk, "units": units, "pipelines": 4 * sms,
+                "unit_rounds": -(-units // (4 * sms)),
+                "last_round_fill": round(units / (4 * sms) - (-(-units // (4 * sms)) - 1), 3)}}
         roof = {"bound": "fp64", "achieved": round(achieved / 1e12, 3),
                 "peak": round(fp64_peak / 1e12, 3), "unit": "T FP64-instr/s",
                 "frac": round(achieved / fp64_peak, 4), "traffic": read_profile_traffic(kname),
@@ -661,8 +672,7 @@ def run_she(args):
                 "frac_of_lower_bound": round(lanes_rank * P.n * FP64_LOWER_BOUND_PER_CMUX
                                              / (br_ms_per_launch * 1e-3) / fp64_peak, 4),
                 **common,
-                "wave_rounds": {"lanes": lanes_rank, "slots_per_round": slots, "rounds": rounds,
-                                "last_round_fill": round(lanes_rank / slots - (rounds - 1), 3)},
+                "wave_rounds": wave,
                 "peak_source": f"K7 measured {fp64_peak / 1e12:.2f} T DFMA/s on {sms} SMs "
                                "(nominal 64 FP64 lanes/SM/clk)",
                 "ntt_engine_equivalent": {"achieved_gmodmul_s": round(lanes_rank * MODMUL_PER_LANE[P.N] / (br_ms_per_launch * 1e-3) / 1e9, 1),

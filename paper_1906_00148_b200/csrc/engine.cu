@@ -1724,8 +1724,13 @@ she_status launch_br_fft_tm(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cud
   f.geo = a.geo;
   f.stagger = ctx->fft_stagger;
   cudaLaunchConfig_t cfg = {};
-  // four two-lane quarter pipelines per CTA, one CTA per SM
+  // four two-lane quarter pipelines per CTA, one CTA per SM; a narrow batch is
+  // spread over all SMs (the static split then gives a pipeline one lane, which
+  // runs on all four of its warps, before any pipeline gets a pair)
+  cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>(max_lanes, (size_t)ctx->sms)));
+#ifdef SHE_TM_GRID8  // A/B: the round-2c grid (pairs on as few SMs as hold the batch)
   cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>((max_lanes + 7) / 8, (size_t)ctx->sms)));
+#endif
   // the work queue serves batches of more than two lanes per pipeline
   const bool queued = ctx->tm_sched && max_lanes > (size_t)8 * cfg.gridDim.x;
   f.sched = ctx->tm_sched;
