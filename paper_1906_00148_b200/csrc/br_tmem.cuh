@@ -34,6 +34,7 @@
 // TMEM: 512 columns x 128 lanes (all of it; one CTA per SM).
 #pragma once
 #include "dcheck.cuh"
+#include "tm_queue.h"
 
 constexpr int kTmSlots = 2;
 constexpr size_t kTmAccBytes = (size_t)kTmSlots * 2 * fft::kN * 4;
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   // queue stays in registers across the CMux loop): lanes base .. base + nsl - 1
   // (nsl = 0: no more work), iterations [i0, i1); [4] = the static split's cursor
   uint32_t* const unit = unit_info[Q];
-  if (qt == 0) unit[4] = (uint32_t)(((uint64_t)(blockIdx.x * 4 + Q) * *args.nlanes) / (gridDim.x * 4));
+  if (qt == 0) unit[4] = tmq::first(blockIdx.x * 4 + Q, *args.nlanes, gridDim.x * 4);
 #if !SHE_TM_INDEP
   if (args.stagger && Q) __nanosleep(args.stagger * Q);
 #endif
@@ -509,35 +510,19 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
     if (qt == 0) {
       const uint32_t total = *args.nlanes, nq = gridDim.x * 4;
       const uint32_t chunk = args.chunk ? args.chunk : n;
-      uint32_t ubase = 0, unsl = 0, ui0 = 0, ui1 = n;
-      if (chunk < n && total > 2 * nq) {
-        // the queue: npairs pairs x nchunks chunks, chunk-major (+ an odd lane as unit 0)
-        const uint32_t npairs = total >> 1, odd = total & 1, nchunks = (n + chunk - 1) / chunk;
-        uint32_t u = atomicAdd(args.sched, 1u);
-        if (u < npairs * nchunks + odd) {
-          if (odd && u == 0) {
-            ubase = total - 1;
-            unsl = 1;
-          } else {
-            u -= odd;
-            const uint32_t k = u / npairs, pair = u - k * npairs;
-            ubase = 2 * pair;
-            unsl = 2;
-            ui0 = k * chunk;
-            ui1 = min(n, ui0 + chunk);
-            if (k) tm_await(args.sched + 1 + pair, k);  // the pair's previous chunk is written back
-          }
-        }
+      tmq::Unit w;
+      if (tmq::queued(total, n, chunk, nq)) {
+        w = tmq::unit(atomicAdd(args.sched, 1u), total, n, chunk);
+        // the pair's previous chunk is written back
+        if (w.nsl == 2 && w.i0) tm_await(args.sched + 1 + (w.base >> 1), w.i0 / chunk);
       } else {
-        const uint32_t last = (uint32_t)(((uint64_t)(blockIdx.x * 4 + Q + 1) * total) / nq);
-        ubase = unit[4];
-        unsl = min(2u, last - min(last, ubase));
-        unit[4] = ubase + unsl;
+        w = tmq::next_static(unit[4], blockIdx.x * 4 + Q, total, nq, n);
+        unit[4] = w.base + w.nsl;
       }
-      unit[0] = ubase;
-      unit[1] = unsl;
-      unit[2] = ui0;
-      unit[3] = ui1;
+      unit[0] = w.base;
+      unit[1] = w.nsl;
+      unit[2] = w.i0;
+      unit[3] = w.i1;
     }
     tm_quarter_sync(Q);  // unit[] is rewritten only after the barriers below
     const int nsl = (int)unit[1];

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "bootstrap_core.cuh"
+#include "tm_queue.h"
 
 namespace {
 
@@ -233,4 +234,40 @@ uint64_t she_emu_gl_shl_le(uint64_t v, int s) { return gl::shl_le(v, s); }
 uint64_t she_emu_gl_add_le(uint64_t a, uint64_t b) { return gl::add_le(a, b); }
 uint64_t she_emu_gl_sub_le(uint64_t a, uint64_t b) { return gl::sub_le(a, b); }
 uint32_t she_emu_gl_lift32_neg(uint64_t t) { return gl::lift32_neg(t); }
+
+// The TMEM engine's work distribution (tm_queue.h, the kernel's own
+// functions): the schedule of one launch written out.  Queue mode: every unit
+// u < units as (base, nsl, i0, i1) into out[4 u ..]; returns the unit count.
+// Static mode (the queue does not apply): per pipeline gq the units it runs in
+// order, appended to out with the pipeline index as a fifth word; returns the
+// number of rows.  *mode = 1 queue, 0 static.
+uint32_t she_emu_tm_schedule(uint32_t total, uint32_t n, uint32_t chunk, uint32_t pipelines, uint32_t cap,
+                             uint32_t* out, int* mode) {
+  uint32_t rows = 0;
+  if (tmq::queued(total, n, chunk, pipelines)) {
+    *mode = 1;
+    const uint32_t nu = tmq::units(total, n, chunk);
+    for (uint32_t u = 0; u < nu && rows < cap; ++u, ++rows) {
+      const tmq::Unit w = tmq::unit(u, total, n, chunk);
+      const uint32_t r[5] = {w.base, w.nsl, w.i0, w.i1, 0};
+      memcpy(out + 5 * rows, r, sizeof r);
+    }
+    // one past the end must be "no more work"
+    if (tmq::unit(nu, total, n, chunk).nsl != 0) return 0xFFFFFFFFu;
+    return rows;
+  }
+  *mode = 0;
+  for (uint32_t gq = 0; gq < pipelines; ++gq) {
+    uint32_t cursor = tmq::first(gq, total, pipelines);
+    for (;;) {
+      const tmq::Unit w = tmq::next_static(cursor, gq, total, pipelines, n);
+      if (w.nsl == 0 || rows >= cap) break;
+      const uint32_t r[5] = {w.base, w.nsl, w.i0, w.i1, gq};
+      memcpy(out + 5 * rows, r, sizeof r);
+      ++rows;
+      cursor = w.base + w.nsl;
+    }
+  }
+  return rows;
+}
 }
