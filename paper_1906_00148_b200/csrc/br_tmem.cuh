@@ -357,13 +357,14 @@ struct TmArgs {
   uint32_t ext_stride;
   br::Geometry geo;
   uint32_t stagger;  // ns of start delay per quarter index (phase offset)
-  // Work queue (wide batches; see br_fft_tm_kernel): sched[0] = next unit,
-  // sched[1 + p] = chunks of lane pair p completed; acc_save[p] = the pair's
-  // two accumulators between chunks.  chunk = CMux iterations per unit
-  // (>= n: the static contiguous split only).
+  // Work queue (see br_fft_tm_kernel, tm_queue.h): sched[0] = next unit,
+  // sched[1 + s] = chunks of slot s (a lane pair, or a lane) completed;
+  // acc_save[s] = the slot's accumulators between chunks.  chunk = CMux
+  // iterations per unit (>= n: the static contiguous split only).
   uint32_t* sched;
   uint32_t* acc_save;
   uint32_t chunk;
+  uint32_t save_slots;  // slots acc_save and sched hold (checked build)
 };
 
 // Completed-chunk counter of a lane pair: published with release semantics
@@ -511,14 +512,17 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       const uint32_t total = *args.nlanes, nq = gridDim.x * 4;
       const uint32_t chunk = args.chunk ? args.chunk : n;
       tmq::Unit w;
-      if (tmq::queued(total, n, chunk, nq)) {
-        w = tmq::unit(atomicAdd(args.sched, 1u), total, n, chunk);
-        // the pair's previous chunk is written back
-        if (w.nsl == 2 && w.i0) tm_await(args.sched + 1 + (w.base >> 1), w.i0 / chunk);
+      const int m = tmq::mode(total, n, chunk, nq);
+      if (m != tmq::kStatic) {
+        w = tmq::unit(atomicAdd(args.sched, 1u), total, n, chunk, m);
+        SHE_DCHECK(args.sched && args.acc_save && w.slot < args.save_slots);
+        // the slot's previous chunk is written back
+        if (w.i0) tm_await(args.sched + 1 + w.slot, w.i0 / chunk);
       } else {
         w = tmq::next_static(unit[4], blockIdx.x * 4 + Q, total, nq, n);
         unit[4] = w.base + w.nsl;
       }
+      unit[5] = w.slot;
       unit[0] = w.base;
       unit[1] = w.nsl;
       unit[2] = w.i0;
@@ -529,7 +533,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
     if (nsl == 0) break;
     {
       const uint32_t base = unit[0], i0 = unit[2];
-      prologue(base, nsl, i0 ? args.acc_save + (size_t)(base >> 1) * (kTmSlots * 2 * N) : nullptr);
+      prologue(base, nsl, i0 ? args.acc_save + (size_t)unit[5] * (kTmSlots * 2 * N) : nullptr);
     }
     const uint32_t i0 = unit[2], i1 = unit[3];
 
@@ -625,13 +629,13 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
     const uint32_t base = unit[0];
     if (unit[3] == n) {
       extract(base, (int)unit[1]);
-    } else {  // hand the pair's accumulators to whichever pipeline takes its next chunk
+    } else {  // hand the accumulators to whichever pipeline takes the slot's next chunk
       const uint4* a4 = reinterpret_cast<const uint4*>(acc);
-      uint4* w4 = reinterpret_cast<uint4*>(args.acc_save + (size_t)(base >> 1) * (kTmSlots * 2 * N));
+      uint4* w4 = reinterpret_cast<uint4*>(args.acc_save + (size_t)unit[5] * (kTmSlots * 2 * N));
       for (int m = qt; m < kTmSlots * 2 * N / 4; m += 128) __stcg(w4 + m, a4[m]);
       __threadfence();
       tm_quarter_sync(Q);
-      if (qt == 0) tm_publish(args.sched + 1 + (base >> 1), unit[3] / args.chunk);
+      if (qt == 0) tm_publish(args.sched + 1 + unit[5], unit[3] / args.chunk);
     }
   }
   tm_free_all(tmem, warp);

@@ -1636,8 +1636,9 @@ she_status ensure_ext(she_ctx* ctx, size_t lanes) {
   CK(cudaMalloc(&ctx->ext, want * ctx->ext_stride * 4));
   CK(cudaMalloc(&ctx->lane_buf, (want + 1) * 4));  // list + count
   if (ctx->fft_g && ctx->fft_store == 2 && ctx->fft_chunk < ctx->p.n) {
-    CK(cudaMalloc(&ctx->tm_sched, (want / 2 + 1) * 4));
-    CK(cudaMalloc(&ctx->tm_save, (want / 2) * kTmAccBytes));
+    const size_t slots = tmq::slots((uint32_t)want, 4u * (uint32_t)ctx->sms);
+    CK(cudaMalloc(&ctx->tm_sched, (slots + 1) * 4));
+    CK(cudaMalloc(&ctx->tm_save, slots * kTmAccBytes));
   }
   ctx->ext_lanes = want;
   return SHE_OK;
@@ -1731,12 +1732,16 @@ she_status launch_br_fft_tm(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cud
 #ifdef SHE_TM_GRID8  // A/B: the round-2c grid (pairs on as few SMs as hold the batch)
   cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>((max_lanes + 7) / 8, (size_t)ctx->sms)));
 #endif
-  // the work queue serves batches of more than two lanes per pipeline
-  const bool queued = ctx->tm_sched && max_lanes > (size_t)8 * cfg.gridDim.x;
+  // the work queue serves batches of more than one lane per pipeline (the
+  // kernel picks the mode from the actual lane count, tm_queue.h)
+  const uint32_t nq = 4 * cfg.gridDim.x;
+  const bool queued = ctx->tm_sched && max_lanes > nq;
+  const uint32_t slots = tmq::slots((uint32_t)std::min(max_lanes, ctx->ext_lanes), 4u * (uint32_t)ctx->sms);
   f.sched = ctx->tm_sched;
   f.acc_save = ctx->tm_save;
   f.chunk = queued ? ctx->fft_chunk : ctx->p.n;
-  if (queued) CK(cudaMemsetAsync(ctx->tm_sched, 0, (std::min(max_lanes, ctx->ext_lanes) / 2 + 1) * 4, stream));
+  f.save_slots = ctx->tm_sched ? slots : 0;
+  if (queued) CK(cudaMemsetAsync(ctx->tm_sched, 0, ((size_t)slots + 1) * 4, stream));
   cfg.blockDim = dim3(512);
   cfg.dynamicSmemBytes = kTmSmemBytes;
   cfg.stream = stream;

@@ -236,34 +236,34 @@ uint64_t she_emu_gl_sub_le(uint64_t a, uint64_t b) { return gl::sub_le(a, b); }
 uint32_t she_emu_gl_lift32_neg(uint64_t t) { return gl::lift32_neg(t); }
 
 // The TMEM engine's work distribution (tm_queue.h, the kernel's own
-// functions): the schedule of one launch written out.  Queue mode: every unit
-// u < units as (base, nsl, i0, i1) into out[4 u ..]; returns the unit count.
-// Static mode (the queue does not apply): per pipeline gq the units it runs in
-// order, appended to out with the pipeline index as a fifth word; returns the
-// number of rows.  *mode = 1 queue, 0 static.
+// functions): the schedule of one launch written out as rows (base, nsl, i0,
+// i1, slot, pipeline).  Queue modes: every unit u < units in order (pipeline =
+// 0); static mode: per pipeline gq the units it runs, in order.  Returns the
+// number of rows; *mode = tmq::Mode.
 uint32_t she_emu_tm_schedule(uint32_t total, uint32_t n, uint32_t chunk, uint32_t pipelines, uint32_t cap,
                              uint32_t* out, int* mode) {
   uint32_t rows = 0;
-  if (tmq::queued(total, n, chunk, pipelines)) {
-    *mode = 1;
-    const uint32_t nu = tmq::units(total, n, chunk);
+  const int m = tmq::mode(total, n, chunk, pipelines);
+  *mode = m;
+  if (m != tmq::kStatic) {
+    const uint32_t nu = tmq::units(total, n, chunk, m);
     for (uint32_t u = 0; u < nu && rows < cap; ++u, ++rows) {
-      const tmq::Unit w = tmq::unit(u, total, n, chunk);
-      const uint32_t r[5] = {w.base, w.nsl, w.i0, w.i1, 0};
-      memcpy(out + 5 * rows, r, sizeof r);
+      const tmq::Unit w = tmq::unit(u, total, n, chunk, m);
+      const uint32_t r[6] = {w.base, w.nsl, w.i0, w.i1, w.slot, 0};
+      memcpy(out + 6 * rows, r, sizeof r);
+      if (w.slot >= tmq::slots(total, pipelines)) return 0xFFFFFFFFu;
     }
     // one past the end must be "no more work"
-    if (tmq::unit(nu, total, n, chunk).nsl != 0) return 0xFFFFFFFFu;
+    if (tmq::unit(nu, total, n, chunk, m).nsl != 0) return 0xFFFFFFFFu;
     return rows;
   }
-  *mode = 0;
   for (uint32_t gq = 0; gq < pipelines; ++gq) {
     uint32_t cursor = tmq::first(gq, total, pipelines);
     for (;;) {
       const tmq::Unit w = tmq::next_static(cursor, gq, total, pipelines, n);
       if (w.nsl == 0 || rows >= cap) break;
-      const uint32_t r[5] = {w.base, w.nsl, w.i0, w.i1, gq};
-      memcpy(out + 5 * rows, r, sizeof r);
+      const uint32_t r[6] = {w.base, w.nsl, w.i0, w.i1, 0, gq};
+      memcpy(out + 6 * rows, r, sizeof r);
       ++rows;
       cursor = w.base + w.nsl;
     }

@@ -13,33 +13,53 @@
 
 namespace tmq {
 
-// Lanes base .. base + nsl - 1 (nsl = 0: no more work), iterations [i0, i1).
+// Lanes base .. base + nsl - 1 (nsl = 0: no more work), iterations [i0, i1);
+// slot = where the unit's accumulators wait between chunks (acc_save, progress
+// word): the pair index (pair queue) or the lane index (single-lane queue).
 struct Unit {
-  uint32_t base, nsl, i0, i1;
+  uint32_t base, nsl, i0, i1, slot;
 };
 
-// The queue serves batches of more than two lanes per pipeline; chunk >= n
-// (or fewer lanes) means the static contiguous split.
-TMQ_HD bool queued(uint32_t total, uint32_t n, uint32_t chunk, uint32_t pipelines) {
-  return chunk < n && total > 2 * pipelines;
+// How a batch of `total` lanes is spread over `pipelines` two-lane pipelines.
+//  kStatic   the contiguous split, every lane for all n iterations: up to one
+//            lane per pipeline (a lane alone runs on all four warps of its
+//            pipeline, the shortest latency), or chunk >= n;
+//  kSingles  a queue of (lane, chunk) units, each lane alone on a pipeline:
+//            batches a little wider than the pipelines.  A pair takes ~1.75x
+//            as long as a single lane, so up to ~1.65 lanes per pipeline the
+//            single-lane chunks, spread evenly, finish before one pair would;
+//  kPairs    a queue of (lane pair, chunk) units (+ an odd lane, whole): the
+//            highest throughput per pipeline, for everything wider.
+enum Mode { kStatic = 0, kPairs = 1, kSingles = 2 };
+TMQ_HD int mode(uint32_t total, uint32_t n, uint32_t chunk, uint32_t pipelines) {
+  if (chunk >= n || total <= pipelines) return kStatic;
+  if ((uint64_t)total * 100 <= (uint64_t)pipelines * 165) return kSingles;
+  return total > 2 * pipelines ? kPairs : kStatic;
 }
 
-// total / 2 lane pairs x ceil(n / chunk) chunks, + an odd last lane (whole).
-TMQ_HD uint32_t units(uint32_t total, uint32_t n, uint32_t chunk) {
-  return (total >> 1) * ((n + chunk - 1) / chunk) + (total & 1);
+TMQ_HD uint32_t units(uint32_t total, uint32_t n, uint32_t chunk, int m) {
+  const uint32_t nchunks = (n + chunk - 1) / chunk;
+  return m == kSingles ? total * nchunks : (total >> 1) * nchunks + (total & 1);
 }
 
-// Unit u of the queue, chunk-major: an odd lane is unit 0 and runs all n
-// iterations (the longest unit first); then chunk 0 of every pair, chunk 1 of
-// every pair, ...  Chunk k of a pair depends on its chunk k - 1, which is a
-// smaller unit number.
-TMQ_HD Unit unit(uint32_t u, uint32_t total, uint32_t n, uint32_t chunk) {
-  const uint32_t npairs = total >> 1, odd = total & 1;
-  if (u >= units(total, n, chunk)) return {0, 0, 0, n};
-  if (odd && u == 0) return {total - 1, 1, 0, n};
+// Unit u of the queue, chunk-major: chunk 0 of every pair (lane), then chunk 1
+// of every pair (lane), ...  Chunk k depends on chunk k - 1 of the same slot,
+// which is a smaller unit number.  Pair queue: an odd last lane is unit 0 and
+// runs all n iterations (the longest unit first).
+TMQ_HD Unit unit(uint32_t u, uint32_t total, uint32_t n, uint32_t chunk, int m) {
+  if (u >= units(total, n, chunk, m)) return {0, 0, 0, n, 0};
+  const uint32_t odd = m == kPairs ? (total & 1) : 0;
+  if (odd && u == 0) return {total - 1, 1, 0, n, 0};
   u -= odd;
-  const uint32_t k = u / npairs, pair = u - k * npairs, i0 = k * chunk;
-  return {2 * pair, 2, i0, n < i0 + chunk ? n : i0 + chunk};
+  const uint32_t per = m == kSingles ? total : total >> 1;  // slots
+  const uint32_t k = u / per, slot = u - k * per, i0 = k * chunk;
+  const uint32_t i1 = n < i0 + chunk ? n : i0 + chunk;
+  return m == kSingles ? Unit{slot, 1, i0, i1, slot} : Unit{2 * slot, 2, i0, i1, slot};
+}
+// Save slots a batch of up to max_lanes lanes can need on `pipelines` pipelines.
+TMQ_HD uint32_t slots(uint32_t max_lanes, uint32_t pipelines) {
+  const uint32_t singles = max_lanes < 2 * pipelines ? max_lanes : 2 * pipelines;
+  return (max_lanes >> 1) > singles ? (max_lanes >> 1) : singles;
 }
 
 // Static split: pipeline gq of nq runs the contiguous lanes [first(gq),
@@ -50,7 +70,7 @@ TMQ_HD uint32_t first(uint32_t gq, uint32_t total, uint32_t nq) {
 TMQ_HD Unit next_static(uint32_t cursor, uint32_t gq, uint32_t total, uint32_t nq, uint32_t n) {
   const uint32_t last = first(gq + 1, total, nq);
   const uint32_t left = cursor < last ? last - cursor : 0;
-  return {cursor, left < 2 ? left : 2, 0, n};
+  return {cursor, left < 2 ? left : 2, 0, n, 0};
 }
 
 }  // namespace tmq

@@ -335,18 +335,22 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
     ctx.close()
 
 
-@pytest.mark.parametrize("parity", [0, 1])
-def test_config1_work_queue_even_and_odd_lane_counts(cuda, env1, config1_outputs, parity):
-    """The TMEM engine's work queue (wide batches: (lane pair, chunk) units, an
-    odd lane first and whole) on prefixes of config 1 with an even and an odd
-    lane count, both wide enough for the queue (> 2 lanes per pipeline), and
-    twice on the same context (the queue words are reset per launch)."""
+@pytest.mark.parametrize("m", [148, 512, 800, 1000, 2000, 2008])
+def test_config1_work_distribution_modes(cuda, env1, config1_outputs, m):
+    """The TMEM engine's work distribution (csrc/tm_queue.h) on prefixes of
+    config 1, against the oracle digests: 148 gates (one lane per pipeline,
+    static), 512 and 800 gates (~600 / ~940 lanes: the single-lane chunk
+    queue), 1000 gates (~1170 lanes: one pair per pipeline, static), 2000 and
+    2008 gates (the pair queue with an odd / an even lane count); each twice
+    on the same context (the queue words are reset per launch)."""
     P = env1.P
     ops, bits, (a, b, c), _ = config1_outputs
-    m = 2000  # a multiple of 4 (the op bytes travel as int32 words)
-    while si.br_lanes(ops[:m]) % 2 != parity:
-        m += 4
-    assert si.br_lanes(ops[:m]) > 2 * 4 * 160
+    lanes = si.br_lanes(ops[:m])
+    pipelines = 4 * torch.cuda.get_device_properties(0).multi_processor_count
+    if m in (512, 800):
+        assert pipelines < lanes <= 1.65 * pipelines
+    if m >= 2000:
+        assert lanes > 2 * pipelines and lanes % 2 == (1 if m == 2000 else 0)
     rows = read_digests(1)
     for rep in range(2):
         out = torch.zeros((m, P.stride), dtype=torch.int32, device="cuda")

@@ -1,10 +1,11 @@
 """Work distribution of the TMEM blind-rotation engine (csrc/tm_queue.h, the
 functions br_fft_tm_kernel itself calls), run on the CPU
 through the host emulation library: every (lane, CMux iteration) of a launch
-is run exactly once, a pair's chunks are numbered in dependency order (the
+is run exactly once, a slot's chunks are numbered in dependency order (the
 kernel waits for chunk k - 1, which must be a smaller unit number for the wait
-to terminate), an odd lane is the first unit and runs whole, and narrow
-batches fall back to the static contiguous split."""
+to terminate), an odd lane of the pair queue is the first unit and runs whole,
+batches a little wider than the pipelines run as single-lane chunks, and
+narrow batches fall back to the static contiguous split."""
 import ctypes
 
 import numpy as np
@@ -12,12 +13,14 @@ import pytest
 
 from paper_1906_00148_b200 import build
 
+STATIC, PAIRS, SINGLES = 0, 1, 2
+
 
 def schedule(total, n, chunk, pipelines):
     L = ctypes.CDLL(build.build_emu())
     L.she_emu_tm_schedule.restype = ctypes.c_uint32
     cap = total * (n // max(1, min(chunk, n)) + 2) + pipelines + 8
-    out = np.zeros((cap, 5), np.uint32)
+    out = np.zeros((cap, 6), np.uint32)
     mode = ctypes.c_int(-1)
     rows = L.she_emu_tm_schedule(total, n, chunk, pipelines, cap,
                                  out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(mode))
@@ -27,62 +30,90 @@ def schedule(total, n, chunk, pipelines):
 
 def coverage(units, total, n):
     cov = np.zeros((total, n), np.int32)
-    for base, nsl, i0, i1, _ in units:
+    for base, nsl, i0, i1, _, _ in units:
         assert nsl in (1, 2) and i0 < i1 <= n and base + nsl <= total
         cov[base:base + nsl, i0:i1] += 1
     return cov
 
 
+def check_queue(units, total, n, chunk, lanes_per_slot):
+    """Chunks of a slot in increasing unit order, each continuing where the
+    previous one ended; chunk-major over the slots."""
+    seen = {}
+    for base, nsl, i0, i1, slot, _ in units:
+        if nsl != lanes_per_slot:
+            continue
+        assert base == lanes_per_slot * slot and i0 % chunk == 0 and i1 == min(n, i0 + chunk)
+        assert seen.get(slot, 0) == i0
+        seen[slot] = i1
+    assert all(v == n for v in seen.values())
+    k = [i0 // chunk for _, nsl, i0, _, _, _ in units if nsl == lanes_per_slot]
+    assert k == sorted(k)
+    return len(seen)
+
+
 @pytest.mark.parametrize("total,n,chunk,pipelines", [
     (4797, 500, 32, 592),     # config 1: odd lane count, ragged last chunk
     (4796, 500, 32, 592),
-    (1185, 500, 7, 592),      # just wide enough for the queue
+    (1185, 500, 7, 592),      # just wide enough for the pair queue
     (2343, 500, 499, 592),    # chunks of 499 + 1
     (100, 128, 1, 16), (101, 128, 127, 16), (33, 5, 2, 4), (9, 3, 1, 4),
 ])
-def test_queue_units_cover_every_iteration_once_in_dependency_order(total, n, chunk, pipelines):
+def test_pair_queue_covers_every_iteration_once_in_dependency_order(total, n, chunk, pipelines):
     units, mode = schedule(total, n, chunk, pipelines)
-    assert mode == 1
+    assert mode == PAIRS
     assert (coverage(units, total, n) == 1).all()
-    nchunks = -(-n // chunk)
-    assert len(units) == (total // 2) * nchunks + total % 2
+    assert len(units) == (total // 2) * -(-n // chunk) + total % 2
     if total % 2:  # the odd lane: unit 0, all n iterations (the longest unit first)
         assert tuple(units[0][:4]) == (total - 1, 1, 0, n)
-    seen = {}
-    for u, (base, nsl, i0, i1, _) in enumerate(units):
-        if nsl == 2:
-            assert base % 2 == 0 and i0 % chunk == 0 and i1 == min(n, i0 + chunk)
-            # chunk k comes after chunk k - 1 of the same pair and continues where it ended
-            assert seen.get(base, 0) == i0
-            seen[base] = i1
-    assert all(v == n for v in seen.values()) and len(seen) == total // 2
-    # chunk-major: every pair's chunk k before any chunk k + 1
-    k = [i0 // chunk for _, nsl, i0, _, _ in units if nsl == 2]
-    assert k == sorted(k)
+        units = units[1:]
+    assert check_queue(units, total, n, chunk, 2) == total // 2
+
+
+@pytest.mark.parametrize("total,n,chunk,pipelines", [
+    (593, 500, 32, 592),      # one lane more than the pipelines
+    (600, 500, 32, 592),      # a 512-gate rank shard of config 1 (8 ranks)
+    (976, 500, 32, 592),      # the widest single-lane queue (1.65 lanes per pipeline)
+    (700, 500, 7, 592), (5, 9, 2, 4), (26, 16, 5, 16),
+])
+def test_single_lane_queue(total, n, chunk, pipelines):
+    units, mode = schedule(total, n, chunk, pipelines)
+    assert mode == SINGLES
+    assert (coverage(units, total, n) == 1).all()
+    assert len(units) == total * -(-n // chunk)
+    assert check_queue(units, total, n, chunk, 1) == total
 
 
 @pytest.mark.parametrize("total,n,chunk,pipelines", [
     (0, 500, 32, 592), (1, 500, 32, 592), (46, 500, 32, 592), (591, 500, 32, 592),
-    (592, 500, 32, 592), (599, 500, 32, 592), (1184, 500, 32, 592),   # <= 2 lanes per pipeline
-    (4797, 500, 500, 592), (4797, 500, 0xFFFFFFFF, 592),               # chunk >= n: static only
+    (592, 500, 32, 592),                                               # <= 1 lane per pipeline
+    (977, 500, 32, 592), (1184, 500, 32, 592),                         # up to 2: one pair each
+    (4797, 500, 500, 592), (4797, 500, 0xFFFFFFFF, 592), (600, 500, 500, 592),  # chunk >= n
     (37, 16, 4, 20), (9, 4, 2, 4 * 3),
 ])
 def test_static_split_covers_every_lane_once(total, n, chunk, pipelines):
     units, mode = schedule(total, n, chunk, pipelines)
-    assert mode == 0
+    assert mode == STATIC
     assert (coverage(units, total, n) == 1).all() if total else len(units) == 0
-    for base, nsl, i0, i1, _ in units:
+    for base, nsl, i0, i1, _, _ in units:
         assert (i0, i1) == (0, n)
     per = np.zeros(pipelines, np.int64)
     last_end = {}
-    for base, nsl, _, _, gq in units:
+    for base, nsl, _, _, _, gq in units:
         per[gq] += nsl
         assert last_end.get(gq, base) == base  # contiguous, in order
         last_end[gq] = base + nsl
     assert per.max() - per.min() <= 1  # balanced: at most one lane more than any other pipeline
     if total <= pipelines:  # narrow: every lane alone on a pipeline (all four warps on it)
-        assert all(nsl == 1 for _, nsl, _, _, _ in units)
+        assert all(nsl == 1 for _, nsl, _, _, _, _ in units)
     # a pipeline runs pairs first and at most one single lane, last
-    for gq in set(int(g) for g in units[:, 4]) if len(units) else ():
-        mine = [int(nsl) for _, nsl, _, _, g in units if g == gq]
+    for gq in set(int(g) for g in units[:, 5]) if len(units) else ():
+        mine = [int(nsl) for _, nsl, _, _, _, g in units if g == gq]
         assert mine == sorted(mine, reverse=True) and mine.count(1) <= 1
+
+
+def test_mode_thresholds():
+    """<= 1 lane per pipeline: static; up to 1.65: single-lane chunks; up to 2:
+    static pairs; wider: the pair queue."""
+    modes = {t: schedule(t, 500, 32, 592)[1] for t in (592, 593, 976, 977, 1184, 1185)}
+    assert modes == {592: STATIC, 593: SINGLES, 976: SINGLES, 977: STATIC, 1184: STATIC, 1185: PAIRS}
