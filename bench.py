@@ -465,10 +465,11 @@ def leveled_units(ctx, sk, P, words=720, width=16):
     return res
 
 
-def batch_sweep(ctx, sk, P, sizes=(40, 148, 300, 500, 740, 1000, 1480, 4096, 8192, 16384, 32768)):
+def batch_sweep(ctx, sk, P, sizes=(40, 148, 300, 512, 740, 1024, 1480, 2048, 4096, 8192, 16384, 32768)):
     """Gates/s against the batch size (config-1 gates): where the persistent
     kernel's pipelines fill the 148 SMs and how narrow levels of a circuit run
-    (`--sweep`)."""
+    (`--sweep`); 512 / 1024 / 2048 gates are one rank's shard of config 1 on
+    8 / 4 / 2 GPUs."""
     import torch
     from paper_1906_00148_b200 import she
     res = []

@@ -190,9 +190,11 @@ typedef struct {
   int fft_stagger_ns;/* TMEM engine: start delay of quarter q = q x this (ns),
                      0..100000 (phase offset between the pipelines) */
   int fft_chunk;  /* TMEM engine: CMux iterations per unit of the device-wide
-                     work queue that serves batches of more than two lanes per
-                     pipeline: 0 = default (32), 1..1024, or
-                     -1 = the static contiguous lane split only */
+                     work queue (csrc/tm_queue.h) that serves
+                     batches of more than two lanes per pipeline as (lane
+                     pair, chunk) units and batches of 1 to 1.65 lanes per
+                     pipeline as (lane, chunk) units: 0 = default (32),
+                     1..1024, or -1 = the static contiguous lane split only */
   int reserved[1];/* must be 0 */
 } she_ctx_options;
 
