@@ -69,6 +69,8 @@ def kernel(path, lanes, n):
             out.setdefault("fp64_metrics", {})[k] = raw[k]
     work = lanes * n
     wf = g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+    if wf is None:
+        wf = g("memory_l1_wavefronts_shared")  # the SourceCounters roll-up
     if wf is not None:
         out["smem_wavefronts_per_launch"] = wf
         out["smem_wavefronts_per_lane_cmux"] = round(wf / work, 1)
