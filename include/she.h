@@ -189,12 +189,14 @@ typedef struct {
                      DESIGN.md §4.2e; no other shape option applies) */
   int fft_stagger_ns;/* TMEM engine: start delay of quarter q = q x this (ns),
                      0..100000 (phase offset between the pipelines) */
-  int fft_chunk;  /* TMEM engine: CMux iterations per unit of the device-wide
-                     work queue (csrc/tm_queue.h) that serves
-                     batches of more than two lanes per pipeline as (lane
-                     pair, chunk) units and batches of 1 to 1.65 lanes per
-                     pipeline as (lane, chunk) units: 0 = default (32),
-                     1..1024, or -1 = the static contiguous lane split only */
+  int fft_chunk;  /* TMEM engine, how batches of more than one blind-rotation
+                     lane per pipeline are balanced (DESIGN.md §4.2e,
+                     csrc/tm_queue.h): 0 = default, the wrap-around schedule
+                     (every pipeline the same number of CMux iterations, one
+                     accumulator hand-over per pipeline); 1..1024 = a
+                     device-wide queue of (lane pair | lane, chunk of that
+                     many iterations) units; -1 = the static contiguous lane
+                     split only */
   int reserved[1];/* must be 0 */
 } she_ctx_options;
 

@@ -358,21 +358,25 @@ struct TmArgs {
   br::Geometry geo;
   uint32_t stagger;  // ns of start delay per quarter index (phase offset)
   // Work queue (see br_fft_tm_kernel, tm_queue.h): sched[0] = next unit,
-  // sched[1 + s] = chunks of slot s (a lane pair, or a lane) completed;
+  // sched[1 + s] = iterations of slot s (a lane pair, or a lane) completed;
   // acc_save[s] = the slot's accumulators between chunks.  chunk = CMux
   // iterations per unit (>= n: the static contiguous split only).
   uint32_t* sched;
   uint32_t* acc_save;
   uint32_t chunk;
+  uint32_t wrap;        // 1: the wrap-around schedule instead of the chunk queue (tm_queue.h)
   uint32_t save_slots;  // slots acc_save and sched hold (checked build)
 };
 
-// Completed-chunk counter of a lane pair: published with release semantics
-// after the pair's accumulators were written back (and fenced), awaited with
-// acquire loads by one thread of the quarter that runs the next chunk.  The
-// unit it waits for was taken from the queue earlier by a resident CTA that
-// waits only on still earlier units, so the wait is finite; the bound turns a
-// broken invariant into a launch error instead of a hang.
+// Progress word of a slot (a lane pair, or a lane): the CMux iterations done,
+// published with release semantics after the slot's accumulators were written
+// back (and fenced), awaited with acquire loads by one thread of the quarter
+// that continues the slot.  The unit it waits for is run by a resident CTA
+// (one CTA per SM, grid <= SM count) before any unit that waits itself (wrap
+// schedule: a pipeline runs its dependency-free first part first; queue: the
+// awaited unit was taken earlier and waits only on still earlier units), so
+// the wait is finite; the bound turns a broken invariant into a launch error
+// instead of a hang.
 __device__ __forceinline__ void tm_publish(uint32_t* flag, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
 }
@@ -409,18 +413,20 @@ __device__ __forceinline__ void tm_free_all(uint32_t tmem, int warp) {
 // K3, TMEM engine: one persistent CTA of 16 warps per SM, four independent
 // quarter pipelines of two lanes each (see the file comment).
 //
-// Work distribution.  A unit is (lane pair or single lane, CMux iterations
-// [i0, i1)).  Narrow batches (<= 2 lanes per pipeline) and chunk >= n use the
-// static split: pipeline gq runs the contiguous lanes [first, last) as pairs,
-// an odd last lane alone, each for all n iterations.  Wide batches go through
-// a device-wide queue of (pair, chunk) units in chunk-major order (every
-// pair's chunk k before any chunk k + 1; an odd lane first, whole): a pipeline
-// takes the next unit, waits until the pair's previous chunk is published,
-// reloads the two accumulators from acc_save, runs the chunk and writes them
-// back (or extracts after the last chunk).  All pipelines then finish within
-// one chunk of each other instead of one 500-iteration lane apart: the
-// static split of 4797 lanes over 592 pipelines leaves 61 of them a ninth
-// lane that runs alone at the end (wave tail).
+// Work distribution (tm_queue.h).  A unit is (lane pair or single lane, CMux
+// iterations [i0, i1)).  Narrow batches (<= 1 lane per pipeline, or 1.65 .. 2)
+// use the static split: pipeline gq runs the contiguous lanes [first, last),
+// each for all n iterations.  Wider batches are balanced by splitting units in
+// time: a lane is n dependent iterations, so the static split of config 1's
+// 4797 lanes over 592 pipelines leaves 61 of them a ninth lane that runs alone
+// at the end (wave tail).  Default: the wrap-around schedule
+// (every pipeline the same number of iterations; a unit cut at most once, its
+// first part run first by one pipeline, its last part run last by the next).
+// Option fft_chunk > 0: a device-wide queue of (unit, chunk) items in
+// chunk-major order.  Either way the pipeline that ends a part writes the
+// accumulators to acc_save and publishes the iteration count; the pipeline
+// that continues waits for it, reloads them, recomputes a-bar and goes on
+// (or extracts after iteration n).
 template <int PD = kTmPrefetch, bool FMA = false>
 __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   constexpr int N = fft::kN;
@@ -446,7 +452,10 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
   // queue stays in registers across the CMux loop): lanes base .. base + nsl - 1
   // (nsl = 0: no more work), iterations [i0, i1); [4] = the static split's cursor
   uint32_t* const unit = unit_info[Q];
-  if (qt == 0) unit[4] = tmq::first(blockIdx.x * 4 + Q, *args.nlanes, gridDim.x * 4);
+  if (qt == 0) {
+    unit[4] = tmq::first(blockIdx.x * 4 + Q, *args.nlanes, gridDim.x * 4);
+    unit[6] = 0;  // the wrap-around schedule's step
+  }
 #if !SHE_TM_INDEP
   if (args.stagger && Q) __nanosleep(args.stagger * Q);
 #endif
@@ -512,12 +521,13 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       const uint32_t total = *args.nlanes, nq = gridDim.x * 4;
       const uint32_t chunk = args.chunk ? args.chunk : n;
       tmq::Unit w;
-      const int m = tmq::mode(total, n, chunk, nq);
+      const int m = tmq::mode(total, n, args.wrap ? 1u : chunk, nq);
       if (m != tmq::kStatic) {
-        w = tmq::unit(atomicAdd(args.sched, 1u), total, n, chunk, m);
+        if (args.wrap) w = tmq::wrap_unit(blockIdx.x * 4 + Q, unit[6]++, total, n, nq, m);
+        else w = tmq::unit(atomicAdd(args.sched, 1u), total, n, chunk, m);
         SHE_DCHECK(args.sched && args.acc_save && w.slot < args.save_slots);
-        // the slot's previous chunk is written back
-        if (w.i0) tm_await(args.sched + 1 + w.slot, w.i0 / chunk);
+        // the iterations before i0 are done and the accumulators written back
+        if (w.nsl && w.i0) tm_await(args.sched + 1 + w.slot, w.i0);
       } else {
         w = tmq::next_static(unit[4], blockIdx.x * 4 + Q, total, nq, n);
         unit[4] = w.base + w.nsl;
@@ -635,7 +645,7 @@ __global__ void __launch_bounds__(512, 1) br_fft_tm_kernel(TmArgs args) {
       for (int m = qt; m < kTmSlots * 2 * N / 4; m += 128) __stcg(w4 + m, a4[m]);
       __threadfence();
       tm_quarter_sync(Q);
-      if (qt == 0) tm_publish(args.sched + 1 + unit[5], unit[3] / args.chunk);
+      if (qt == 0) tm_publish(args.sched + 1 + unit[5], unit[3]);
     }
   }
   tm_free_all(tmem, warp);

@@ -357,7 +357,6 @@ struct FftVar<3> {  // v2's tables and scaling, DIT/FMA DFT16s (fft_core.cuh)
 };
 constexpr int kFftDefaultVariant = 2;
 constexpr int kFftDefaultStreams = 1;  // br_fft_kernel (1) or the two-stream br_fft2s_kernel (2)
-constexpr uint32_t kTmDefaultChunk = 32;  // TMEM engine: CMux iterations per work-queue unit
 constexpr int kFftDefaultStore = 2;    // spectra in shared memory (1) or tensor memory (2)
 template <int V>
 constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double2); }
@@ -1466,7 +1465,7 @@ struct she_ctx {
   int fft_streams = 1;             // 2: br_fft2s_kernel (two lanes per warp, skewed)
   int fft_store = kFftDefaultStore;  // 1: spectra in shared memory, 2: in TMEM (br_fft_tm_kernel)
   uint32_t fft_stagger = 0;          // TMEM engine: start delay per quarter (ns)
-  uint32_t fft_chunk = kTmDefaultChunk;  // TMEM engine: CMux iterations per queue unit (>= n: static split)
+  uint32_t fft_chunk = 0;  // TMEM engine: 0 = wrap-around schedule, else CMux iterations per queue unit (>= n: static split)
   double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain (shared-memory engine)
   double2* bkt = nullptr;  // [n][16 fi][16 plane][32] the same for the TMEM engine
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
@@ -1732,14 +1731,15 @@ she_status launch_br_fft_tm(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cud
 #ifdef SHE_TM_GRID8  // A/B: the round-2c grid (pairs on as few SMs as hold the batch)
   cfg.gridDim = dim3((unsigned)std::max<size_t>(1, std::min<size_t>((max_lanes + 7) / 8, (size_t)ctx->sms)));
 #endif
-  // the work queue serves batches of more than one lane per pipeline (the
-  // kernel picks the mode from the actual lane count, tm_queue.h)
+  // units are split in time for batches of more than one lane per pipeline
+  // (the kernel picks the mode from the actual lane count, tm_queue.h)
   const uint32_t nq = 4 * cfg.gridDim.x;
   const bool queued = ctx->tm_sched && max_lanes > nq;
   const uint32_t slots = tmq::slots((uint32_t)std::min(max_lanes, ctx->ext_lanes), 4u * (uint32_t)ctx->sms);
   f.sched = ctx->tm_sched;
   f.acc_save = ctx->tm_save;
-  f.chunk = queued ? ctx->fft_chunk : ctx->p.n;
+  f.chunk = queued && ctx->fft_chunk ? ctx->fft_chunk : ctx->p.n;
+  f.wrap = queued && ctx->fft_chunk == 0;
   f.save_slots = ctx->tm_sched ? slots : 0;
   if (queued) CK(cudaMemsetAsync(ctx->tm_sched, 0, ((size_t)slots + 1) * 4, stream));
   cfg.blockDim = dim3(512);
@@ -2044,7 +2044,7 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   // directions, §4.2e), the shared-memory engine to transform 2
   ctx->fft_v = o.fft_variant ? o.fft_variant : ctx->fft_store == 2 ? 3 : kFftDefaultVariant;
   ctx->fft_stagger = (uint32_t)o.fft_stagger_ns;
-  ctx->fft_chunk = o.fft_chunk < 0 ? 0xFFFFFFFFu : o.fft_chunk ? (uint32_t)o.fft_chunk : kTmDefaultChunk;
+  ctx->fft_chunk = o.fft_chunk < 0 ? 0xFFFFFFFFu : (uint32_t)o.fft_chunk;  // 0: the wrap-around schedule
   ctx->fft_pre = o.fft_prefetch == 0 ? 16 : o.fft_prefetch == 3 ? 0 : o.fft_prefetch == 2 ? 8 : 16;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {

@@ -270,4 +270,25 @@ uint32_t she_emu_tm_schedule(uint32_t total, uint32_t n, uint32_t chunk, uint32_
   }
   return rows;
 }
+
+// The wrap-around schedule (tmq::wrap_unit): per pipeline gq its units in
+// execution order as rows (base, nsl, i0, i1, slot, pipeline).  Returns the
+// number of rows, or 0xFFFFFFFF if the mode is static; *mode = tmq::Mode.
+uint32_t she_emu_tm_wrap_schedule(uint32_t total, uint32_t n, uint32_t pipelines, uint32_t cap, uint32_t* out,
+                                  int* mode) {
+  const int m = tmq::mode(total, n, 1, pipelines);
+  *mode = m;
+  if (m == tmq::kStatic) return 0xFFFFFFFFu;
+  uint32_t rows = 0;
+  for (uint32_t gq = 0; gq < pipelines; ++gq)
+    for (uint32_t step = 0;; ++step) {
+      const tmq::Unit w = tmq::wrap_unit(gq, step, total, n, pipelines, m);
+      if (w.nsl == 0 || rows >= cap) break;
+      if (w.slot >= tmq::slots(total, pipelines)) return 0xFFFFFFFEu;
+      const uint32_t r[6] = {w.base, w.nsl, w.i0, w.i1, w.slot, gq};
+      memcpy(out + 6 * rows, r, sizeof r);
+      ++rows;
+    }
+  return rows;
+}
 }

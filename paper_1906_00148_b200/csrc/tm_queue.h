@@ -56,10 +56,51 @@ TMQ_HD Unit unit(uint32_t u, uint32_t total, uint32_t n, uint32_t chunk, int m) 
   const uint32_t i1 = n < i0 + chunk ? n : i0 + chunk;
   return m == kSingles ? Unit{slot, 1, i0, i1, slot} : Unit{2 * slot, 2, i0, i1, slot};
 }
+// ---- the wrap-around schedule (the default for kPairs / kSingles) -----------
+// McNaughton's rule for identical machines with preemption: lay the units'
+// n iterations end to end (unit p = lane pair p, or lane p; an odd last lane
+// is a unit of one lane) and cut the line into `pipelines` equal ranges.
+// With at least n iterations per pipeline a unit is cut at most once, into a
+// first part [0, x) that ends one pipeline's range and a last part [x, n) that
+// starts the next pipeline's range.  A pipeline runs the END of its range
+// first (a first part: no dependency), then its whole units, and the START of
+// its range last (a last part: it waits for the first part, which its
+// neighbour ran first, tens of milliseconds earlier).  Every pipeline gets the
+// same number of iterations (+- 1) and there is one hand-over per pipeline,
+// instead of one per (unit, chunk) as in the queue.
+TMQ_HD uint32_t wrap_units(uint32_t total, int m) { return m == kSingles ? total : (total + 1) >> 1; }
+TMQ_HD Unit wrap_make(uint32_t p, uint32_t i0, uint32_t i1, uint32_t total, int m) {
+  if (m == kSingles) return {p, 1, i0, i1, p};
+  return {2 * p, 2 * p + 1 < total ? 2u : 1u, i0, i1, p};
+}
+// The step-th unit, in execution order, of pipeline gq (nsl = 0: done).
+TMQ_HD Unit wrap_unit(uint32_t gq, uint32_t step, uint32_t total, uint32_t n, uint32_t nq, int m) {
+  const uint64_t W = (uint64_t)wrap_units(total, m) * n;
+  const uint64_t s0 = W * gq / nq, s1 = W * (gq + 1) / nq;
+  if (s1 <= s0) return {0, 0, 0, n, 0};
+  const uint32_t a = (uint32_t)(s0 / n), b = (uint32_t)((s1 - 1) / n);
+  const uint32_t a0 = (uint32_t)(s0 - (uint64_t)a * n);  // unit a from iteration a0
+  const uint32_t b1 = (uint32_t)(s1 - (uint64_t)b * n);  // unit b up to iteration b1 (1 .. n)
+  const bool first_part = b > a && b1 < n, last_part = a0 > 0;
+  uint32_t k = step;
+  if (first_part) {
+    if (k == 0) return wrap_make(b, 0, b1, total, m);
+    --k;
+  }
+  const uint32_t lo = a + (last_part ? 1 : 0), hi = first_part ? b : b + 1;  // units [lo, hi) from their start
+  if (lo < hi) {
+    if (k < hi - lo) return wrap_make(lo + k, 0, lo + k == b ? b1 : n, total, m);
+    k -= hi - lo;
+  }
+  if (last_part && k == 0) return wrap_make(a, a0, a == b ? b1 : n, total, m);
+  return {0, 0, 0, n, 0};
+}
+
 // Save slots a batch of up to max_lanes lanes can need on `pipelines` pipelines.
 TMQ_HD uint32_t slots(uint32_t max_lanes, uint32_t pipelines) {
   const uint32_t singles = max_lanes < 2 * pipelines ? max_lanes : 2 * pipelines;
-  return (max_lanes >> 1) > singles ? (max_lanes >> 1) : singles;
+  const uint32_t pairs = (max_lanes + 1) >> 1;
+  return pairs > singles ? pairs : singles;
 }
 
 // Static split: pipeline gq of nq runs the contiguous lanes [first(gq),

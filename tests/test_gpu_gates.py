@@ -297,9 +297,11 @@ ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3
                "fft-smem": dict(engine="fft", fft_store="smem"),
                "fft-tmem-stagger": dict(engine="fft", fft_store="tmem", fft_stagger_ns=20000),
                "fft-tmem-v2": dict(engine="fft", fft_store="tmem", fft_variant=2),
-               # TMEM engine work queue: static split only, ragged last chunk (500 = 71 x 7 + 3),
-               # two chunks of 499 + 1
+               # TMEM engine work distribution (the default is the wrap-around schedule): static
+               # split only; the chunk queue with a ragged last chunk (500 = 71 x 7 + 3), with 32
+               # iterations, with two chunks of 499 + 1
                "fft-tmem-static": dict(fft_chunk=-1), "fft-tmem-chunk7": dict(fft_chunk=7),
+               "fft-tmem-chunk32": dict(fft_chunk=32),
                "fft-tmem-chunk499": dict(fft_store="tmem", fft_chunk=499)}
 
 
@@ -307,7 +309,7 @@ ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3
                                     "fft5-noprefetch", "ks-imma", "ks-cuda", "fft-v3", "fft5-v3",
                                     "ks-tcgen05", "fft-2streams", "fft-smem", "fft-tmem-stagger",
                                     "fft-tmem-v2", "fft-tmem-static", "fft-tmem-chunk7",
-                                    "fft-tmem-chunk499"])
+                                    "fft-tmem-chunk32", "fft-tmem-chunk499"])
 def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with the
     spectra in tensor memory (br_fft_tm_kernel); the Goldilocks
@@ -323,6 +325,7 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
                                   "ks-cuda": 8, "fft-v3": 4, "fft5-v3": 5, "ks-tcgen05": 8,
                                   "fft-2streams": 4, "fft-smem": 4, "fft-tmem-stagger": 8,
                                   "fft-tmem-v2": 8, "fft-tmem-static": 8, "fft-tmem-chunk7": 8,
+                                  "fft-tmem-chunk32": 8,
                                   "fft-tmem-chunk499": 8}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
@@ -335,14 +338,16 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
     ctx.close()
 
 
+@pytest.mark.parametrize("chunk", [0, 32], ids=["wrap", "queue32"])
 @pytest.mark.parametrize("m", [148, 512, 800, 1000, 2000, 2008])
-def test_config1_work_distribution_modes(cuda, env1, config1_outputs, m):
+def test_config1_work_distribution_modes(cuda, env1, config1_outputs, m, chunk):
     """The TMEM engine's work distribution (csrc/tm_queue.h) on prefixes of
     config 1, against the oracle digests: 148 gates (one lane per pipeline,
-    static), 512 and 800 gates (~600 / ~940 lanes: the single-lane chunk
-    queue), 1000 gates (~1170 lanes: one pair per pipeline, static), 2000 and
-    2008 gates (the pair queue with an odd / an even lane count); each twice
-    on the same context (the queue words are reset per launch)."""
+    static), 512 and 800 gates (~600 / ~940 lanes: single lanes split in time),
+    1000 gates (~1170 lanes: one pair per pipeline, static), 2000 and 2008
+    gates (lane pairs split in time, an odd / an even lane count); with the
+    default wrap-around schedule and with the chunk queue; each twice on the
+    same context (the progress words are reset per launch)."""
     P = env1.P
     ops, bits, (a, b, c), _ = config1_outputs
     lanes = si.br_lanes(ops[:m])
@@ -351,15 +356,18 @@ def test_config1_work_distribution_modes(cuda, env1, config1_outputs, m):
         assert pipelines < lanes <= 1.65 * pipelines
     if m >= 2000:
         assert lanes > 2 * pipelines and lanes % 2 == (1 if m == 2000 else 0)
+    ctx = env1.ctx if chunk == 0 else she.Context(P, env1.ck, device=0, fft_chunk=chunk)
     rows = read_digests(1)
     for rep in range(2):
         out = torch.zeros((m, P.stride), dtype=torch.int32, device="cuda")
-        she.she_gate_batch_ops(env1.ctx, dev(np.asarray(ops[:m], np.uint8)), dev(a[:m]), dev(b[:m]),
+        she.she_gate_batch_ops(ctx, dev(np.asarray(ops[:m], np.uint8)), dev(a[:m]), dev(b[:m]),
                                dev(c[:m]), out)
         torch.cuda.synchronize()
         got = host(out)
         bad = [g for g, op, d, bit in rows[:m] if digest(got[g, : P.n + 1]) != d]
         assert not bad, f"{len(bad)} gates differ from the oracle, first {bad[:8]}"
+    if chunk:
+        ctx.close()
 
 
 def env0_ctx():

@@ -117,3 +117,69 @@ def test_mode_thresholds():
     static pairs; wider: the pair queue."""
     modes = {t: schedule(t, 500, 32, 592)[1] for t in (592, 593, 976, 977, 1184, 1185)}
     assert modes == {592: STATIC, 593: SINGLES, 976: SINGLES, 977: STATIC, 1184: STATIC, 1185: PAIRS}
+
+
+def wrap_schedule(total, n, pipelines):
+    L = ctypes.CDLL(build.build_emu())
+    L.she_emu_tm_wrap_schedule.restype = ctypes.c_uint32
+    cap = total + 3 * pipelines + 8
+    out = np.zeros((cap, 6), np.uint32)
+    mode = ctypes.c_int(-1)
+    rows = L.she_emu_tm_wrap_schedule(total, n, pipelines, cap, out.ctypes.data_as(ctypes.c_void_p),
+                                      ctypes.byref(mode))
+    assert rows < 0xFFFFFFF0 and rows <= cap
+    return out[:rows], mode.value
+
+
+@pytest.mark.parametrize("total,n,pipelines,mode", [
+    (4797, 500, 592, PAIRS), (4796, 500, 592, PAIRS), (1185, 500, 592, PAIRS), (1186, 500, 592, PAIRS),
+    (9548, 500, 592, PAIRS), (131072, 500, 592, PAIRS), (2368, 500, 592, PAIRS),  # 2368 = 4 x 592: no cut at all
+    (593, 500, 592, SINGLES), (612, 500, 592, SINGLES), (976, 500, 592, SINGLES),
+    (33, 5, 4, PAIRS), (9, 3, 4, PAIRS), (5, 9, 4, SINGLES), (26, 16, 16, SINGLES), (101, 128, 16, PAIRS),
+])
+def test_wrap_around_schedule(total, n, pipelines, mode):
+    """The default distribution of wide batches: every (lane, iteration) once;
+    every pipeline the same number of iterations (+- 1); a unit is cut at most
+    once; a pipeline runs a first part first and a last part last; and an
+    execution that honours the progress words (a part with i0 > 0 waits until
+    its slot has published i0) terminates whatever the pipelines' speeds."""
+    units, m = wrap_schedule(total, n, pipelines)
+    assert m == mode
+    assert (coverage(units, total, n) == 1).all()
+    lanes_per = 1 if mode == SINGLES else 2
+    nunits = total if mode == SINGLES else (total + 1) // 2
+    per = np.zeros(pipelines, np.int64)
+    parts = {}
+    order = {g: [] for g in range(pipelines)}
+    for base, nsl, i0, i1, slot, gq in units:
+        assert base == lanes_per * slot and slot < nunits
+        assert nsl == (lanes_per if base + lanes_per <= total else 1)  # an odd last lane: a unit of one
+        per[gq] += i1 - i0
+        parts.setdefault(int(slot), []).append((int(i0), int(i1), int(gq)))
+        order[int(gq)].append((int(slot), int(i0), int(i1)))
+    assert per.max() - per.min() <= 1 and per.sum() == nunits * n
+    for slot, ps in parts.items():
+        ps.sort()
+        assert len(ps) <= 2 and ps[0][0] == 0 and ps[-1][1] == n
+        if len(ps) == 2:  # first part on one pipeline, last part on the next
+            assert ps[0][1] == ps[1][0] and ps[1][2] == ps[0][2] + 1
+    for gq, us in order.items():
+        kinds = [0 if (i0 == 0 and i1 < n) else 2 if i0 > 0 else 1 for _, i0, i1 in us]
+        assert kinds == sorted(kinds) and kinds.count(0) <= 1 and kinds.count(2) <= 1
+    # adversarial execution: always advance the LAST pipeline that can move
+    done = {s: 0 for s in parts}
+    pos = {g: 0 for g in order}
+    left = sum(len(v) for v in order.values())
+    while left:
+        moved = False
+        for gq in sorted(order, reverse=True):
+            if pos[gq] < len(order[gq]):
+                slot, i0, i1 = order[gq][pos[gq]]
+                if done[slot] >= i0:
+                    assert done[slot] == i0
+                    done[slot] = i1
+                    pos[gq] += 1
+                    left -= 1
+                    moved = True
+        assert moved, "deadlock"
+    assert all(v == n for v in done.values())
