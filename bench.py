@@ -58,6 +58,7 @@ FP64_EXECUTED_PER_CMUX = {1: 176_129, 2: 183_875, 8: 171_074}  # 8: the TMEM eng
 # radix, 4 M log2 M - 6 M + 8 = 15,368 flops) with every instruction a fused
 # multiply-add (2 flops), plus the pointwise sum (4 DFMA per complex
 # multiply-add, 512 x 4 outputs x 4 rows) = 8 x 7,684 + 32,768 = 94,240.
+TM_DEFAULT_CHUNK = 32  # include/she.h she_ctx_options.fft_chunk default
 FP64_LOWER_BOUND_PER_CMUX = 8 * (4 * 512 * 9 - 6 * 512 + 8) // 2 + 512 * 4 * 4 * 4
 MODMUL_PER_LANE = {1024: 19_456_000, 256: 1_048_576}  # n[(k+1)l+(k+1)](N/2)log2N + n(k+1)l(k+1)N
 WORKLOAD = ("config1: 4096 independent bootstrapped gates, ops uniform over "
@@ -649,7 +650,7 @@ def run_she(args):
         rounds = -(-lanes_rank // slots)
         wave = {"lanes": lanes_rank, "slots_per_round": slots, "rounds": rounds,
                 "last_round_fill": round(lanes_rank / slots - (rounds - 1), 3)}
-        if engine == 8 and args.fft_chunk >= 0 and lanes_rank > 4 * sms:
+        if engine == 8 and args.fft_chunk != -1 and lanes_rank > 4 * sms:
             # the TMEM engine splits units (lane pairs; single lanes up to 1.65 per pipeline)
             # in time (she_ctx_options.fft_chunk, csrc/tm_queue.h)
             singles = lanes_rank * 100 <= 4 * sms * 165
@@ -657,13 +658,14 @@ def run_she(args):
             if singles or lanes_rank > 2 * 4 * sms:
                 wave = {"lanes": lanes_rank, "unit": "lane" if singles else "lane pair", "units": units,
                         "pipelines": 4 * sms}
-                if args.fft_chunk == 0:
+                if args.fft_chunk == -2:
                     wave["wrap_around_schedule"] = {
                         "iterations_per_pipeline": round(units * P.n / (4 * sms), 1),
                         "handovers": 4 * sms}
                 else:
-                    items = units * -(-P.n // args.fft_chunk)
-                    wave["chunk_queue"] = {"chunk_cmux": args.fft_chunk, "items": items,
+                    chunk = args.fft_chunk or TM_DEFAULT_CHUNK
+                    items = units * -(-P.n // chunk)
+                    wave["chunk_queue"] = {"chunk_cmux": chunk, "items": items,
                                            "item_rounds": round(items / (4 * sms), 2)}
         roof = {"bound": "fp64", "achieved": round(achieved / 1e12, 3),
                 "peak": round(fp64_peak / 1e12, 3), "unit": "T FP64-instr/s",
@@ -905,8 +907,8 @@ def main():
     ap.add_argument("--fft-stagger-ns", type=int, default=0,
                     help="TMEM engine: start delay per quarter pipeline (ns)")
     ap.add_argument("--fft-chunk", type=int, default=0,
-                    help="TMEM engine: 0 wrap-around schedule (default), N > 0 chunk queue of N CMux "
-                         "iterations per item, -1 static lane split")
+                    help="TMEM engine: 0 chunk queue of 32 CMux iterations per item (default), N > 0 that "
+                         "queue with N, -1 static lane split, -2 wrap-around schedule")
     ap.add_argument("--ks-kernel", default="default", choices=["default", "general", "cuda", "imma", "tcgen05"],
                     help="key-switch kernel (she_ctx_options.ks_kernel)")
     ap.add_argument("--count", type=int, default=COUNT,

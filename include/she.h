@@ -191,12 +191,12 @@ typedef struct {
                      0..100000 (phase offset between the pipelines) */
   int fft_chunk;  /* TMEM engine, how batches of more than one blind-rotation
                      lane per pipeline are balanced (DESIGN.md §4.2e,
-                     csrc/tm_queue.h): 0 = default, the wrap-around schedule
-                     (every pipeline the same number of CMux iterations, one
-                     accumulator hand-over per pipeline); 1..1024 = a
-                     device-wide queue of (lane pair | lane, chunk of that
-                     many iterations) units; -1 = the static contiguous lane
-                     split only */
+                     csrc/tm_queue.h): 0 = default, a device-wide queue of
+                     (lane pair | lane, chunk of 32 CMux iterations) items;
+                     1..1024 = that queue with chunks of this many iterations;
+                     -1 = the static contiguous lane split only; -2 = the
+                     wrap-around schedule (every pipeline the same number of
+                     iterations, one accumulator hand-over per pipeline) */
   int reserved[1];/* must be 0 */
 } she_ctx_options;
 
@@ -206,8 +206,10 @@ typedef struct {
  * halves, 1/512 folded in; 65.5 MB at the default parameters; the product is
  * exact), for the NTT engine into the Goldilocks NTT domain
  * (N^-1 folded in; 32.8 MB).  Only the selected engine's BK is built.  The
- * BK in use gets an L2 persisting access-policy window on the blind-rotation
- * launches when the device allows one (cudaLimitPersistingL2CacheSize).
+ * BK of the NTT engine and of the shared-memory FFT engine gets an L2
+ * persisting access-policy window on the blind-rotation launches when the
+ * device allows one (cudaLimitPersistingL2CacheSize); the TMEM engine keeps
+ * the part of BK in use L2-resident by its schedule instead.
  * Unknown or inapplicable option values are SHE_ERR_ARG.  rank/world describe
  * the multi-GPU group this context belongs to (world = 1 for single GPU; the
  * exchange between ranks is done by the caller's process group).

@@ -357,6 +357,7 @@ struct FftVar<3> {  // v2's tables and scaling, DIT/FMA DFT16s (fft_core.cuh)
 };
 constexpr int kFftDefaultVariant = 2;
 constexpr int kFftDefaultStreams = 1;  // br_fft_kernel (1) or the two-stream br_fft2s_kernel (2)
+constexpr uint32_t kTmDefaultChunk = 32;  // TMEM engine: CMux iterations per chunk-queue item
 constexpr int kFftDefaultStore = 2;    // spectra in shared memory (1) or tensor memory (2)
 template <int V>
 constexpr size_t fft_tables_bytes() { return 2 * FftVar<V>::kTab * sizeof(double2); }
@@ -1465,7 +1466,8 @@ struct she_ctx {
   int fft_streams = 1;             // 2: br_fft2s_kernel (two lanes per warp, skewed)
   int fft_store = kFftDefaultStore;  // 1: spectra in shared memory, 2: in TMEM (br_fft_tm_kernel)
   uint32_t fft_stagger = 0;          // TMEM engine: start delay per quarter (ns)
-  uint32_t fft_chunk = 0;  // TMEM engine: 0 = wrap-around schedule, else CMux iterations per queue unit (>= n: static split)
+  uint32_t fft_chunk = kTmDefaultChunk;  // TMEM engine: CMux iterations per item of the chunk queue (>= n: static split)
+  bool fft_wrap = false;                 // TMEM engine: the wrap-around schedule instead of the chunk queue
   double2* bkf = nullptr;  // [n][16][512] BK halves in the FFT domain (shared-memory engine)
   double2* bkt = nullptr;  // [n][16 fi][16 plane][32] the same for the TMEM engine
   bool ks2 = false;  // key switch by ks2_kernel (base 4, t = 8; KSK rows K1, K2, K1+K2-K3)
@@ -1634,7 +1636,7 @@ she_status ensure_ext(she_ctx* ctx, size_t lanes) {
   size_t want = std::max(lanes, (size_t)1024);
   CK(cudaMalloc(&ctx->ext, want * ctx->ext_stride * 4));
   CK(cudaMalloc(&ctx->lane_buf, (want + 1) * 4));  // list + count
-  if (ctx->fft_g && ctx->fft_store == 2 && ctx->fft_chunk < ctx->p.n) {
+  if (ctx->fft_g && ctx->fft_store == 2 && (ctx->fft_wrap || ctx->fft_chunk < ctx->p.n)) {
     const size_t slots = tmq::slots((uint32_t)want, 4u * (uint32_t)ctx->sms);
     CK(cudaMalloc(&ctx->tm_sched, (slots + 1) * 4));
     CK(cudaMalloc(&ctx->tm_save, slots * kTmAccBytes));
@@ -1738,8 +1740,8 @@ she_status launch_br_fft_tm(she_ctx* ctx, const BRArgs& a, size_t max_lanes, cud
   const uint32_t slots = tmq::slots((uint32_t)std::min(max_lanes, ctx->ext_lanes), 4u * (uint32_t)ctx->sms);
   f.sched = ctx->tm_sched;
   f.acc_save = ctx->tm_save;
-  f.chunk = queued && ctx->fft_chunk ? ctx->fft_chunk : ctx->p.n;
-  f.wrap = queued && ctx->fft_chunk == 0;
+  f.chunk = queued && !ctx->fft_wrap ? ctx->fft_chunk : ctx->p.n;
+  f.wrap = queued && ctx->fft_wrap;
   f.save_slots = ctx->tm_sched ? slots : 0;
   if (queued) CK(cudaMemsetAsync(ctx->tm_sched, 0, ((size_t)slots + 1) * 4, stream));
   cfg.blockDim = dim3(512);
@@ -2004,7 +2006,7 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     return fail(SHE_ERR_ARG, "fft_store = 2 (TMEM engine): transform 2 or 3 only, no lane/group/prefetch/stream options");
   if (o.fft_stagger_ns < 0 || o.fft_stagger_ns > 100000)
     return fail(SHE_ERR_ARG, "fft_stagger_ns=%d", o.fft_stagger_ns);
-  if (o.fft_chunk < -1 || o.fft_chunk > 1024) return fail(SHE_ERR_ARG, "fft_chunk=%d", o.fft_chunk);
+  if (o.fft_chunk < -2 || o.fft_chunk > 1024) return fail(SHE_ERR_ARG, "fft_chunk=%d", o.fft_chunk);
   if (o.fft_chunk && (!use_fft || o.fft_store == 1 ||
                       (o.fft_store == 0 && (o.fft_lanes || o.fft_variant || o.fft_groups || o.fft_prefetch ||
                                             o.fft_streams))))
@@ -2044,7 +2046,8 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   // directions, §4.2e), the shared-memory engine to transform 2
   ctx->fft_v = o.fft_variant ? o.fft_variant : ctx->fft_store == 2 ? 3 : kFftDefaultVariant;
   ctx->fft_stagger = (uint32_t)o.fft_stagger_ns;
-  ctx->fft_chunk = o.fft_chunk < 0 ? 0xFFFFFFFFu : (uint32_t)o.fft_chunk;  // 0: the wrap-around schedule
+  ctx->fft_wrap = o.fft_chunk == -2;
+  ctx->fft_chunk = o.fft_chunk < 0 ? 0xFFFFFFFFu : o.fft_chunk ? (uint32_t)o.fft_chunk : kTmDefaultChunk;
   ctx->fft_pre = o.fft_prefetch == 0 ? 16 : o.fft_prefetch == 3 ? 0 : o.fft_prefetch == 2 ? 8 : 16;
   st = p->N == 1024 ? setup_shape<ntt::Shape<1024>>(ctx, ck) : setup_shape<ntt::Shape<256>>(ctx, ck);
   if (st != SHE_OK) {
@@ -2113,6 +2116,12 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
   {
     int maxp = 0;
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
+    // Not for the TMEM engine: its chunk queue keeps all pipelines inside the
+    // same few MB of BK, which stay L2-resident by schedule, and a persisting
+    // set-aside for the whole 65.5 MB BK would push the accumulator hand-overs
+    // out to DRAM (ncu: 586 MB written per config-1 launch with the window,
+    // 126 MB without; the same kernel time; profiles/r2e/persist_ab.txt).
+    if (ctx->bkt) maxp = 0;
     if (maxp > 0) {
       int maxw = 0;
       cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device);

@@ -192,7 +192,7 @@ def test_encrypt_noise_is_the_host_clients_noise(params):
     (dict(ntt_shape=(9, 9)), "uninstantiated NTT shape"),
     (dict(fft_lanes=7), "unknown FFT lane count"),
     (dict(fft_chunk=32), "fft_chunk at N = 256 (NTT engine)"),
-    (dict(fft_chunk=-2), "fft_chunk out of range"),
+    (dict(fft_chunk=-3), "fft_chunk out of range"),
 ], ids=["fft-at-N256", "lanes-for-ntt", "shape-9x9", "lanes-7", "chunk-for-ntt", "chunk-range"])
 def test_ctx_options_rejected_before_any_device_work(opts, why):
     """she_ctx_create_ex validates she_ctx_options on the host (SHE_ERR_ARG)

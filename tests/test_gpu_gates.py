@@ -297,11 +297,12 @@ ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3
                "fft-smem": dict(engine="fft", fft_store="smem"),
                "fft-tmem-stagger": dict(engine="fft", fft_store="tmem", fft_stagger_ns=20000),
                "fft-tmem-v2": dict(engine="fft", fft_store="tmem", fft_variant=2),
-               # TMEM engine work distribution (the default is the wrap-around schedule): static
-               # split only; the chunk queue with a ragged last chunk (500 = 71 x 7 + 3), with 32
-               # iterations, with two chunks of 499 + 1
+               # TMEM engine work distribution (the default is the chunk queue, 32 iterations):
+               # static split only; the chunk queue with a ragged last chunk (500 = 71 x 7 + 3),
+               # with 32 iterations given explicitly, with two chunks of 499 + 1; the wrap-around
+               # schedule
                "fft-tmem-static": dict(fft_chunk=-1), "fft-tmem-chunk7": dict(fft_chunk=7),
-               "fft-tmem-chunk32": dict(fft_chunk=32),
+               "fft-tmem-chunk32": dict(fft_chunk=32), "fft-tmem-wrap": dict(fft_chunk=-2),
                "fft-tmem-chunk499": dict(fft_store="tmem", fft_chunk=499)}
 
 
@@ -309,7 +310,7 @@ ENGINE_OPTS = {"ntt": dict(engine="ntt"), "fft3": dict(engine="fft", fft_lanes=3
                                     "fft5-noprefetch", "ks-imma", "ks-cuda", "fft-v3", "fft5-v3",
                                     "ks-tcgen05", "fft-2streams", "fft-smem", "fft-tmem-stagger",
                                     "fft-tmem-v2", "fft-tmem-static", "fft-tmem-chunk7",
-                                    "fft-tmem-chunk32", "fft-tmem-chunk499"])
+                                    "fft-tmem-chunk32", "fft-tmem-wrap", "fft-tmem-chunk499"])
 def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engine):
     """The default context of N = 1024 runs the FP64 FFT engine with the
     spectra in tensor memory (br_fft_tm_kernel); the Goldilocks
@@ -325,7 +326,7 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
                                   "ks-cuda": 8, "fft-v3": 4, "fft5-v3": 5, "ks-tcgen05": 8,
                                   "fft-2streams": 4, "fft-smem": 4, "fft-tmem-stagger": 8,
                                   "fft-tmem-v2": 8, "fft-tmem-static": 8, "fft-tmem-chunk7": 8,
-                                  "fft-tmem-chunk32": 8,
+                                  "fft-tmem-chunk32": 8, "fft-tmem-wrap": 8,
                                   "fft-tmem-chunk499": 8}[engine]
     ops, bits, (a, b, c), _ = config1_outputs
     out = torch.zeros((a.shape[0], P.stride), dtype=torch.int32, device="cuda")
@@ -338,7 +339,7 @@ def test_config1_other_blind_rotation_engines(cuda, env1, config1_outputs, engin
     ctx.close()
 
 
-@pytest.mark.parametrize("chunk", [0, 32], ids=["wrap", "queue32"])
+@pytest.mark.parametrize("chunk", [0, -2], ids=["queue32", "wrap"])
 @pytest.mark.parametrize("m", [148, 512, 800, 1000, 2000, 2008])
 def test_config1_work_distribution_modes(cuda, env1, config1_outputs, m, chunk):
     """The TMEM engine's work distribution (csrc/tm_queue.h) on prefixes of
@@ -346,7 +347,7 @@ def test_config1_work_distribution_modes(cuda, env1, config1_outputs, m, chunk):
     static), 512 and 800 gates (~600 / ~940 lanes: single lanes split in time),
     1000 gates (~1170 lanes: one pair per pipeline, static), 2000 and 2008
     gates (lane pairs split in time, an odd / an even lane count); with the
-    default wrap-around schedule and with the chunk queue; each twice on the
+    default chunk queue and with the wrap-around schedule; each twice on the
     same context (the progress words are reset per launch)."""
     P = env1.P
     ops, bits, (a, b, c), _ = config1_outputs
