@@ -2120,7 +2120,7 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     // same few MB of BK, which stay L2-resident by schedule, and a persisting
     // set-aside for the whole 65.5 MB BK would push the accumulator hand-overs
     // out to DRAM (ncu: 586 MB written per config-1 launch with the window,
-    // 126 MB without; the same kernel time; profiles/r2e/persist_ab.txt).
+    // 126 MB without; the same kernel time; profiles/r2f/persist_ab.txt).
     if (ctx->bkt) maxp = 0;
     if (maxp > 0) {
       int maxw = 0;
