@@ -2121,7 +2121,9 @@ she_status she_ctx_create_ex(const she_params* p, const she_cloud_key* ck, int d
     // set-aside for the whole 65.5 MB BK would push the accumulator hand-overs
     // out to DRAM (ncu: 586 MB written per config-1 launch with the window,
     // 126 MB without; the same kernel time; profiles/r2f/persist_ab.txt).
+#ifndef SHE_TM_PERSIST  // -DSHE_TM_PERSIST: the window for the TMEM engine too (A/B, tools/gpu_persist.sh)
     if (ctx->bkt) maxp = 0;
+#endif
     if (maxp > 0) {
       int maxw = 0;
       cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device);
